@@ -1,0 +1,287 @@
+"""Pins for the fp64 oracle (CPU only, -m "not gpu").
+
+Each test ties an oracle function to something other than itself: the paper's printed
+structural examples and SPEC's hand-derived worked examples (tests/golden/), closed forms,
+numpy.fft as a library special case, and brute-force loops on tiny inputs.  Chosen so that a
+dropped term, a wrong sign or index, or a transposed operand anywhere fails at least one."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import CONFIGS, normal
+
+RNG = np.random.default_rng(12345)
+
+
+def rand(*shape):
+    return RNG.standard_normal(shape)
+
+
+def tube(v):
+    return np.asarray(v, dtype=np.float64).reshape(1, 1, -1)
+
+
+# ---------------------------------------------------------------- worked examples (golden)
+def test_dft_worked_examples(golden):
+    for key in ("dft_1x1x2", "dft_delta_1x1x4", "dft_1x1x1"):
+        g = golden[key]
+        got = O.dft_mode3(tube(g["tube"]))[0, 0]
+        np.testing.assert_allclose(got.real, g["dft_re"], atol=1e-14)
+        np.testing.assert_allclose(got.imag, g["dft_im"], atol=1e-14)
+
+
+def test_idft_worked_example(golden):
+    g = golden["idft_1x1x2"]
+    got = O.idft_mode3(np.asarray(g["spec_re"], dtype=np.complex128).reshape(1, 1, -1))[0, 0]
+    np.testing.assert_allclose(got.real, g["tube"], atol=1e-14)
+    np.testing.assert_allclose(got.imag, 0, atol=1e-14)
+
+
+def test_circ_display(golden):
+    g = golden["circ_3"]
+    np.testing.assert_array_equal(O.circ(np.array(g["v"])), np.array(g["circ"]))
+    # bcirc of a 1x1xn3 tensor is circ of its tube (Eq. (6) reduces to the circ display)
+    np.testing.assert_array_equal(O.bcirc(tube(g["v"])), np.array(g["circ"]))
+
+
+def test_bcirc_block_pattern(golden):
+    g = golden["bcirc_blocks_n3_4"]
+    n3 = g["n3"]
+    # tensor whose slice k (0-based) is filled with the value k+1 -> each block reveals its slice
+    A = np.zeros((2, 3, n3))
+    for k in range(n3):
+        A[:, :, k] = k + 1
+    M = O.bcirc(A)
+    got = [[int(M[r * 2, c * 3]) for c in range(n3)] for r in range(n3)]
+    assert got == g["slice_index"]
+
+
+def test_tprod_worked_examples(golden):
+    g = golden["tprod_n3_1"]
+    A = np.array(g["A"], float)[:, :, None]
+    B = np.array(g["B"], float)[:, :, None]
+    np.testing.assert_array_equal(O.tprod_bcirc(A, B)[:, :, 0], np.array(g["C"], float))
+    for key in ("tprod_tubes_1x1x2", "tprod_tubes_1x1x3"):
+        g = golden[key]
+        c = O.tprod_bcirc(tube(g["a"]), tube(g["b"]))[0, 0]
+        np.testing.assert_array_equal(c, g["c"])
+        c1 = O.tprod_alg1(tube(g["a"]), tube(g["b"]))[0, 0]
+        np.testing.assert_allclose(c1.real, g["c"], atol=1e-13)
+        cb = O.tprod_blockrow(tube(g["a"]), tube(g["b"]))[0, 0]
+        np.testing.assert_array_equal(cb, g["c"])
+
+
+def test_tran_example(golden):
+    g = golden["tran_n3_4"]
+    A = rand(3, 2, g["n3"]) + 1j * rand(3, 2, g["n3"])
+    T = O.tran(A)
+    for k, src in enumerate(g["source_slice_of_output"]):
+        np.testing.assert_array_equal(T[:, :, k], A[:, :, src - 1].conj().T)
+
+
+def test_teye_and_frobenius(golden):
+    g = golden["teye_2_1"]
+    np.testing.assert_array_equal(O.teye(g["n"], g["n3"]).transpose(2, 0, 1), np.array(g["slices"]))
+    g = golden["frobenius_3_4"]
+    assert O.frobenius(tube(g["tube"])) == pytest.approx(g["norm"], abs=0)
+
+
+# ---------------------------------------------------------------- DFT machinery
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 10, 31, 32, 64])
+def test_dft_matrix_vs_library_and_eq1(n):
+    F = O.dft_matrix(n)
+    # Eq. (1): F^* F = n I
+    np.testing.assert_allclose(F.conj().T @ F, n * np.eye(n), atol=1e-11 * n)
+    # library special case: numpy.fft.fft uses the same unnormalised omega = e^{-2 pi i/n}
+    x = rand(n)
+    np.testing.assert_allclose(F @ x, np.fft.fft(x), atol=1e-12 * n)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_eq3_circulant_diagonalisation(n):
+    """Eq. (3): F circ(v) F^{-1} = Diag(F v)."""
+    v = rand(n)
+    F = O.dft_matrix(n)
+    lhs = F @ O.circ(v) @ np.linalg.inv(F)
+    np.testing.assert_allclose(lhs, np.diag(F @ v), atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", [(3, 4, 5), (2, 2, 6), (1, 3, 1), (4, 1, 7)])
+def test_dft_mode3_vs_numpy_fft_and_roundtrip(shape):
+    A = rand(*shape)
+    Ab = O.dft_mode3(A)
+    np.testing.assert_allclose(Ab, np.fft.fft(A, axis=2), atol=1e-12)
+    np.testing.assert_allclose(O.idft_mode3(Ab).real, A, atol=1e-13)
+    np.testing.assert_allclose(O.hermitian_half(A), np.fft.rfft(A, axis=2), atol=1e-12)
+
+
+@pytest.mark.parametrize("n3", [1, 2, 3, 4, 7, 8])
+def test_eq8_conjugate_symmetry_and_parseval(n3):
+    """Eq. (8) PAPER.md:L142-145 and Parseval (Eq. (1)) on the Hermitian half."""
+    A = rand(3, 4, n3)
+    Ab = O.dft_mode3(A)
+    np.testing.assert_allclose(Ab[:, :, 0].imag, 0, atol=1e-13)
+    for i in range(2, (n3 + 1) // 2 + 1):        # 1-based i as in Eq. (8)
+        np.testing.assert_allclose(np.conj(Ab[:, :, i - 1]), Ab[:, :, n3 - i + 2 - 1], atol=1e-13)
+    h = O.h_slices(n3)
+    w = np.full(h, 2.0)
+    w[0] = 1.0
+    if n3 % 2 == 0:
+        w[-1] = 1.0
+    half = sum(w[f] * np.sum(np.abs(Ab[:, :, f]) ** 2) for f in range(h))
+    assert half / n3 == pytest.approx(np.sum(A ** 2), rel=1e-12)
+
+
+def test_h_slices():
+    for n3 in range(1, 200):
+        assert O.h_slices(n3) == n3 // 2 + 1 == int(np.ceil((n3 + 1) / 2))
+
+
+# ---------------------------------------------------------------- t-product definition
+def _brute_force(A, B):
+    """Eq. (9) by explicit scalar loops: C[i,j,t] = sum_c sum_l bcirc-block(t,c)[i,l] B[l,j,c]."""
+    n1, n2, n3 = A.shape
+    n4 = B.shape[1]
+    C = np.zeros((n1, n4, n3))
+    for i, j, t in itertools.product(range(n1), range(n4), range(n3)):
+        s = 0.0
+        for c in range(n3):
+            for l in range(n2):
+                s += A[i, l, (t - c) % n3] * B[l, j, c]
+        C[i, j, t] = s
+    return C
+
+
+@pytest.mark.parametrize("dims", [(2, 3, 4, 2), (1, 1, 3, 1), (3, 2, 1, 2), (2, 2, 5, 3), (1, 4, 2, 1)])
+def test_bcirc_vs_brute_force(dims):
+    n1, n2, n3, n4 = dims
+    A, B = rand(n1, n2, n3), rand(n2, n4, n3)
+    ref = _brute_force(A, B)
+    np.testing.assert_allclose(O.tprod_bcirc(A, B), ref, atol=1e-12)
+    np.testing.assert_allclose(O.tprod_blockrow(A, B), ref, atol=1e-12)
+    np.testing.assert_allclose(O.tprod_columns(A, B, [n4 - 1])[:, 0, :], ref[:, n4 - 1, :], atol=1e-12)
+
+
+def test_fold_unfold():
+    A = rand(3, 2, 4)
+    U = O.unfold(A)
+    assert U.shape == (12, 2)
+    np.testing.assert_array_equal(U[3:6], A[:, :, 1])
+    np.testing.assert_array_equal(O.fold(U, 3, 2, 4), A)
+
+
+def test_alg1_equals_definition_sweep():
+    """SPEC.md:L183 acceptance shape: Alg. 1 vs Eq. (9) on >= 200 tiny instances."""
+    rng = np.random.default_rng(7)
+    worst = 0.0
+    for _ in range(200):
+        n1, n2, n4 = rng.integers(1, 6, size=3)
+        n3 = int(rng.integers(1, 7))
+        A, B = rng.standard_normal((n1, n2, n3)), rng.standard_normal((n2, n4, n3))
+        C = O.tprod_bcirc(A, B)
+        C1 = O.tprod_alg1(A, B)
+        worst = max(worst, O.rel_err(C1.real, C))
+        assert np.max(np.abs(C1.imag)) <= 1e-12 * max(1.0, np.max(np.abs(C)))
+    assert worst < 1e-12
+
+
+def test_library_fourier_path_equals_definition():
+    """Special case reducing to library routines: numpy rfft + per-slice matmul + irfft."""
+    A, B = rand(5, 6, 9), rand(6, 4, 9)
+    Ab, Bb = np.fft.rfft(A, axis=2), np.fft.rfft(B, axis=2)
+    Cb = np.einsum("ilf,ljf->ijf", Ab, Bb)
+    C = np.fft.irfft(Cb, n=9, axis=2)
+    assert O.rel_err(C, O.tprod_bcirc(A, B)) < 1e-13
+
+
+def _config1():
+    c = CONFIGS["c1"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"], np.float64)
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"], np.float64)
+    D = normal((c["n4"], 8, c["n3"]), c["seedD"], np.float64)
+    return A, B, D
+
+
+def test_identity_eq7_block_diagonalisation():
+    """Eq. (7) PAPER.md:L139 with literal Kronecker products, on config-1 dims."""
+    A, _, _ = _config1()
+    n1, n2, n3 = A.shape
+    F = O.dft_matrix(n3)
+    lhs = np.kron(F, np.eye(n1)) @ O.bcirc(A) @ np.kron(np.linalg.inv(F), np.eye(n2))
+    rhs = O.bdiag(O.dft_mode3(A))
+    assert np.linalg.norm(lhs - rhs) / np.linalg.norm(rhs) < 1e-13
+
+
+def test_identity_teye():
+    """A * I = A and I * A = A; I-bar slices are all I (same line)."""
+    A, _, _ = _config1()
+    n1, n2, n3 = A.shape
+    np.testing.assert_allclose(O.tprod_bcirc(A, O.teye(n2, n3)), A, atol=1e-15)
+    np.testing.assert_allclose(O.tprod_bcirc(O.teye(n1, n3), A), A, atol=1e-15)
+    Ib = O.dft_mode3(O.teye(4, n3))
+    for f in range(n3):
+        np.testing.assert_allclose(Ib[:, :, f], np.eye(4), atol=1e-14)
+    # bcirc(I) is the identity matrix
+    np.testing.assert_array_equal(O.bcirc(O.teye(3, 4)), np.eye(12))
+
+
+def test_identity_associativity_and_bilinearity():
+    A, B, D = _config1()
+    lhs = O.tprod_bcirc(O.tprod_bcirc(A, B), D)
+    rhs = O.tprod_bcirc(A, O.tprod_bcirc(B, D))
+    assert O.rel_err(lhs, rhs) < 1e-13
+    B2 = rand(*B.shape)
+    lin = O.tprod_bcirc(A, B + 2.5 * B2)
+    assert O.rel_err(lin, O.tprod_bcirc(A, B) + 2.5 * O.tprod_bcirc(A, B2)) < 1e-13
+
+
+def test_identity_transpose_antihomomorphism():
+    """(A*B)^* = B^* * A^* under Def. 2.2."""
+    A, B, _ = _config1()
+    lhs = O.tran(O.tprod_bcirc(A, B))
+    rhs = O.tprod_bcirc(O.tran(B), O.tran(A))
+    assert O.rel_err(lhs, rhs) < 1e-13
+    np.testing.assert_array_equal(O.tran(O.tran(A)), A)
+
+
+def test_real_in_real_out():
+    """Lemma 2.1 / Eq. (8): the full complex Fourier route (all n3 slices multiplied, no
+    conjugate fill) gives a real result equal to the definition."""
+    A, B, _ = _config1()
+    C = O.tprod_alg1(A, B, full=True)
+    assert np.max(np.abs(C.imag)) / np.max(np.abs(C.real)) < 1e-13
+    assert O.rel_err(C.real, O.tprod_bcirc(A, B)) < 1e-13
+
+
+def test_shift_equivariance():
+    """A * roll(B, s) = roll(A * B, s) along mode 3 (circular convolution of slice sequences)."""
+    A, B = rand(3, 4, 7), rand(4, 2, 7)
+    C = O.tprod_bcirc(A, B)
+    for s in (1, 3):
+        np.testing.assert_allclose(O.tprod_bcirc(A, np.roll(B, s, axis=2)), np.roll(C, s, axis=2), atol=1e-13)
+        np.testing.assert_allclose(O.tprod_bcirc(np.roll(A, s, axis=2), B), np.roll(C, s, axis=2), atol=1e-13)
+
+
+def test_tubal_rank_structure():
+    """Def. 2.7: U*V with U n1 x r x n3 has every Fourier slice of rank <= r."""
+    U, V = rand(9, 2, 5), rand(2, 8, 5)
+    P = O.tprod_bcirc(U, V)
+    Pb = O.dft_mode3(P)
+    for f in range(5):
+        s = np.linalg.svd(Pb[:, :, f], compute_uv=False)
+        assert s[2] / s[0] < 1e-12
+
+
+def test_shape_mismatch():
+    with pytest.raises(ValueError):
+        O.tprod_bcirc(rand(2, 3, 4), rand(2, 3, 4))
+
+
+def test_generator_recipe():
+    """synth.normal is Matlab-ordered default_rng(seed).standard_normal, rounded to the dtype."""
+    x = normal((3, 4, 5), 7, np.float32)
+    ref = np.random.default_rng(7).standard_normal(60).astype(np.float32)
+    np.testing.assert_array_equal(x.ravel(order="F"), ref)
+    assert x.flags.f_contiguous
