@@ -1,0 +1,143 @@
+/*
+ * tprod.h -- C ABI of the B200-native t-product library (libtprod.so).
+ *
+ * Operation (Definition 2.1, Eq. (9)):
+ *     C = A * B = fold( bcirc(A) . unfold(B) ),   A: n1 x n2 x n3,  B: n2 x n4 x n3,  C: n1 x n4 x n3
+ * computed the fast way of Algorithm 1: a mode-3 DFT of every tube
+ * (Eq. (2); fft(.,[],3), L120-122), one complex matrix product per frequency slice
+ * for the ceil((n3+1)/2) slices of the Hermitian half (Eq. (8); Alg. 1 step 2, L177),
+ * and an inverse DFT (L124-126, Alg. 1 step 3, L179) with the conjugate fill of the remaining
+ * slices fused into it (those slices are never materialised).
+ *
+ * Memory layout of every tensor argument (Matlab linearisation): element (i,j,k),
+ * 0-based, lives at offset i + n1*j + n1*n2*k (in elements of the tensor's dtype).  A torch
+ * tensor of shape (n1, n2, n3) with strides (1, n1, n1*n2) has exactly this layout.
+ *
+ * Ownership: all tensor pointers are caller-owned; the library never frees or retains them past
+ * the call.  The handle owns its plan cache, DFT tables and workspace (device memory, grown on
+ * demand, freed by tprod_destroy) and an optional NCCL communicator.
+ *
+ * Errors: every entry point returns an int status (0 = TPROD_OK).  Argument errors are detected
+ * synchronously, BEFORE anything is enqueued.  Device-side faults of enqueued kernels surface at
+ * the caller's next synchronisation of the stream.  tprod_strerror() maps a status to text.
+ *
+ * Threading: one handle must not be used concurrently from two host threads.  Calls are
+ * asynchronous with respect to the host (stream-ordered) unless stated otherwise.
+ *
+ * Precision: tprod_f32 takes and returns IEEE fp32; its result matches the fp64 definition
+ * within a relative Frobenius error of 1e-5 (BASELINE.json north_star).  Internally the
+ * per-frequency products run on tcgen05 tensor cores with operands split into two fp16 terms
+ * (hi + lo, three cross products, fp32 accumulation) after an exact power-of-two row/column
+ * scaling; see DESIGN.md.  tprod_f64 computes in fp64 throughout (<= 1e-12).
+ * Inputs must be finite; NaN/Inf inputs give unspecified output.
+ */
+#ifndef TPROD_H
+#define TPROD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tprod_ctx* tprod_handle;
+
+/* Status codes. */
+enum {
+  TPROD_OK = 0,
+  TPROD_EINVAL = 1,        /* a dimension < 1, a NULL pointer, element-count overflow, bad handle */
+  TPROD_EALIAS = 2,        /* C overlaps A or B (in-place is not supported) */
+  TPROD_ENOMEM = 3,        /* workspace or table allocation failed */
+  TPROD_ECUDA = 4,         /* a CUDA runtime / launch error */
+  TPROD_ENCCL = 5,         /* NCCL missing or an NCCL call failed */
+  TPROD_EUNSUPPORTED = 6,  /* no kernel for this shape / device (not sm_100) */
+  TPROD_ENOWORLD = 7       /* tprod_bcast_* called before tprod_set_world */
+};
+
+/* dtype selectors for tprod_workspace_bytes */
+enum { TPROD_DTYPE_F32 = 0, TPROD_DTYPE_F64 = 1 };
+
+/* Create a handle bound to CUDA device `device` (an ordinal as seen by the process).
+ * Fails with TPROD_EUNSUPPORTED if the device is not compute capability 10.0 (B200). */
+int tprod_create(int device, tprod_handle* out);
+
+/* Destroy a handle: synchronises its device, frees workspace/tables, destroys the NCCL comm. */
+int tprod_destroy(tprod_handle h);
+
+/* The t-product, fp32.  A: n1*n2*n3 floats, B: n2*n4*n3, C: n1*n4*n3, all DEVICE pointers on
+ * h's device, Matlab layout (see top).  A and B are read-only; C is written entirely.
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Enqueues the whole path on
+ * `stream` and returns; no host synchronisation.  Multi-GPU: n4 is the rank's LOCAL number of
+ * lateral slices and B / C are the rank's compact shard tensors; the call has
+ * no collective.  Deterministic: bitwise identical output for identical inputs, and column j of C
+ * does not depend on n4 (no split-K, fixed K order), so sharding is bitwise invariant. */
+int tprod_f32(const float* A, const float* B, float* C,
+              int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+              void* stream, tprod_handle h);
+
+/* Same in fp64 (all arithmetic fp64). */
+int tprod_f64(const double* A, const double* B, double* C,
+              int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+              void* stream, tprod_handle h);
+
+/* End-to-end variants with HOST pointers (pinned memory recommended): copies A and B to device
+ * buffers owned by the handle, runs tprod_*, copies C back, and synchronises `stream` before
+ * returning (so C_host is valid on return).  Same layout and errors as above. */
+int tprod_f32_host(const float* A_host, const float* B_host, float* C_host,
+                   int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+                   void* stream, tprod_handle h);
+int tprod_f64_host(const double* A_host, const double* B_host, double* C_host,
+                   int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+                   void* stream, tprod_handle h);
+
+/* Bytes of device workspace the handle needs for this shape (half-spectra of A, B, C plus
+ * scale vectors; DFT tables excluded).  Pure function, no device access. */
+int tprod_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t n4, int dtype, size_t* out);
+
+/* Human-readable text for a status code (static storage, never NULL). */
+const char* tprod_strerror(int status);
+
+/* Number of kernel launches enqueued by the most recent tprod_* call on this handle. */
+int tprod_last_launch_count(tprod_handle h, int64_t* out);
+
+/* ---------------------------------------------------------------- multi-GPU (one process/GPU)
+ * The NCCL library is the process's libnccl.so.2 (the one torch already loaded), opened with
+ * dlopen at first use.  tprod_nccl_unique_id writes the 128-byte ncclUniqueId on one rank; the
+ * caller exchanges it (e.g. through a torch.distributed process group) and every rank calls
+ * tprod_set_world with the same bytes.  tprod_bcast_* broadcasts a device buffer in place from
+ * `root` (ncclBroadcast over NVLink/NVSwitch): it is the one-time replication of A, a setup step
+ * that tprod_f32/tprod_f64 never call. */
+int tprod_nccl_unique_id(void* out_128_bytes);
+int tprod_set_world(tprod_handle h, int rank, int world, const void* unique_id_128_bytes);
+int tprod_bcast_f32(tprod_handle h, float* buf, int64_t count, int root, void* stream);
+int tprod_bcast_f64(tprod_handle h, double* buf, int64_t count, int root, void* stream);
+
+/* ---------------------------------------------------------------- stage entry points (tests)
+ * Forward mode-3 DFT of a real X (p x q x n3, Matlab layout, device) on the Hermitian half
+ * f = 0..h-1 (h = ceil((n3+1)/2)), written as fp32 planes Xre, Xim of layout [f][q][p]
+ * (h*p*q floats each, device).  `role` 0 runs the A-operand transform (row scale on p), role 1
+ * the B-operand transform (column scale on q); the production kernels run and their split fp16
+ * planes are decoded back to fp32, so the result carries the production rounding. */
+int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, int64_t n3,
+                  int role, void* stream, tprod_handle h);
+/* Inverse with the fused conjugate fill (Alg. 1 steps 2b-3): planes [f][q][p] -> real X. */
+int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int64_t q, int64_t n3,
+                   void* stream, tprod_handle h);
+
+/* Options (tests / benchmarking).  TPROD_OPT_ENGINE: 0 = auto (tcgen05), 1 = SIMT reference
+ * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
+ * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64/128/256). */
+enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3 };
+int tprod_set_option(tprod_handle h, int option, int64_t value);
+
+/* With TPROD_OPT_TIMING = 1, tprod_f32 records CUDA events on its stream between the stages of
+ * the path; this returns the durations (ms) of the most recent call's stages, in order
+ * [K0 scales, K1 forward DFTs, K2 per-frequency GEMMs, K3 inverse DFT], synchronising on the
+ * last event.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that call. */
+int tprod_last_stage_ms(tprod_handle h, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPROD_H */

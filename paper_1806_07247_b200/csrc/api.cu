@@ -1,0 +1,507 @@
+// C ABI of libtprod.so (include/tprod.h): handle, validation, plan/tables, workspace and the
+// launch sequence of the hot path (Algorithm 1):
+//
+//   fp32:  K0 absmax(A), K0 absmax(B)            exact power-of-two operand scales
+//          K1 fwd_split(A), K1 fwd_split(B)      Alg. 1 step 1 on the Hermitian half
+//          K2 gemm (tcgen05; SIMT reference)     Alg. 1 step 2, first branch (h slices)
+//          K3 inv                                Alg. 1 step 2 second branch + step 3, fused
+//   fp64:  K1 fwd_f64 x2, K2 gemm_simt_f64, K3 inv_f64
+#include "../../include/tprod.h"
+#include "internal.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+using namespace tprod;
+
+struct tprod_ctx {
+  int device = 0;
+  int num_sms = 148;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::map<int, float2*> tw32;
+  std::map<int, double2*> tw64;
+  void* hbuf[3] = {nullptr, nullptr, nullptr};   // device buffers of the *_host entry points
+  size_t hbuf_bytes[3] = {0, 0, 0};
+  int64_t last_launches = 0;
+  int engine = 0;
+  int force_bn = 0;
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, world = 1;
+  bool timing = false;
+  bool timed_last = false;
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t _e = (call);                       \
+    if (_e != cudaSuccess) {                       \
+      return TPROD_ECUDA;                          \
+    }                                              \
+  } while (0)
+
+bool checked_mul(int64_t a, int64_t b, int64_t* out) {
+  if (a < 0 || b < 0) return false;
+  if (a != 0 && b > INT64_MAX / a) return false;
+  *out = a * b;
+  return true;
+}
+
+int validate_dims(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
+  if (n1 < 1 || n2 < 1 || n3 < 1 || n4 < 1) return TPROD_EINVAL;
+  const int64_t lim = (int64_t)1 << 31;
+  if (n1 >= lim || n2 >= lim || n3 >= lim || n4 >= lim) return TPROD_EINVAL;
+  int64_t t;
+  if (!checked_mul(n1, n2, &t) || !checked_mul(t, n3, &t) || t > ((int64_t)1 << 40)) return TPROD_EINVAL;
+  if (!checked_mul(n2, n4, &t) || !checked_mul(t, n3, &t) || t > ((int64_t)1 << 40)) return TPROD_EINVAL;
+  if (!checked_mul(n1, n4, &t) || !checked_mul(t, n3, &t) || t > ((int64_t)1 << 40)) return TPROD_EINVAL;
+  if (h_slices(n3) > 65535) return TPROD_EUNSUPPORTED;   // grid.z of the SIMT engines
+  if ((n1 + 127) / 128 * n2 >= lim || (n2 + 127) / 128 * n4 >= lim) return TPROD_EUNSUPPORTED;
+  return TPROD_OK;
+}
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+  return a0 < b0 + bn && b0 < a0 + an;
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct Layout32 {
+  int64_t h, lda, ldb, ldc;
+  size_t off_maxA, off_maxB, off_Ab, off_Bb, off_Cb, total;
+};
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
+  Layout32 L;
+  L.h = h_slices(n3);
+  L.lda = round_up(n1, 8);   // 16-byte row pitch for TMA (fp16)
+  L.ldb = round_up(n2, 8);
+  L.ldc = round_up(n1, 4);
+  size_t o = 0;
+  L.off_maxA = o; o = align_up(o + 4 * (size_t)n1, 1024);
+  L.off_maxB = o; o = align_up(o + 4 * (size_t)n4, 1024);
+  L.off_Ab = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
+  L.off_Bb = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n4 * L.ldb), 1024);
+  L.off_Cb = o;   o = align_up(o + 4 * (size_t)(L.h * 2 * n4 * L.ldc), 1024);
+  L.total = o;
+  return L;
+}
+
+struct Layout64 {
+  int64_t h;
+  size_t off_Ab, off_Bb, off_Cb, total;
+};
+Layout64 layout64(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
+  Layout64 L;
+  L.h = h_slices(n3);
+  size_t o = 0;
+  L.off_Ab = o; o = align_up(o + 8 * (size_t)(L.h * 2 * n1 * n2), 1024);
+  L.off_Bb = o; o = align_up(o + 8 * (size_t)(L.h * 2 * n2 * n4), 1024);
+  L.off_Cb = o; o = align_up(o + 8 * (size_t)(L.h * 2 * n1 * n4), 1024);
+  L.total = o;
+  return L;
+}
+
+int ensure_ws(tprod_ctx* h, size_t bytes) {
+  if (h->ws_bytes >= bytes) return TPROD_OK;
+  if (h->ws) {
+    CK(cudaDeviceSynchronize());
+    cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+  }
+  if (cudaMalloc(&h->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return TPROD_ENOMEM;
+  }
+  h->ws_bytes = bytes;
+  return TPROD_OK;
+}
+
+int ensure_hbuf(tprod_ctx* h, int which, size_t bytes) {
+  if (h->hbuf_bytes[which] >= bytes) return TPROD_OK;
+  if (h->hbuf[which]) {
+    CK(cudaDeviceSynchronize());
+    cudaFree(h->hbuf[which]);
+    h->hbuf[which] = nullptr;
+    h->hbuf_bytes[which] = 0;
+  }
+  if (cudaMalloc(&h->hbuf[which], bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return TPROD_ENOMEM;
+  }
+  h->hbuf_bytes[which] = bytes;
+  return TPROD_OK;
+}
+
+int get_tw32(tprod_ctx* h, int n3, const float2** out) {
+  auto it = h->tw32.find(n3);
+  if (it != h->tw32.end()) { *out = it->second; return TPROD_OK; }
+  std::vector<double> cs(2 * (size_t)n3);
+  host_twiddles(n3, cs.data());
+  std::vector<float2> t(n3);
+  for (int m = 0; m < n3; ++m) t[m] = make_float2((float)cs[2 * m], (float)cs[2 * m + 1]);  // RN
+  float2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(float2) * n3) != cudaSuccess) { cudaGetLastError(); return TPROD_ENOMEM; }
+  CK(cudaMemcpy(d, t.data(), sizeof(float2) * n3, cudaMemcpyHostToDevice));
+  h->tw32[n3] = d;
+  *out = d;
+  return TPROD_OK;
+}
+
+int get_tw64(tprod_ctx* h, int n3, const double2** out) {
+  auto it = h->tw64.find(n3);
+  if (it != h->tw64.end()) { *out = it->second; return TPROD_OK; }
+  std::vector<double> cs(2 * (size_t)n3);
+  host_twiddles(n3, cs.data());
+  double2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double2) * n3) != cudaSuccess) { cudaGetLastError(); return TPROD_ENOMEM; }
+  CK(cudaMemcpy(d, cs.data(), sizeof(double2) * n3, cudaMemcpyHostToDevice));
+  h->tw64[n3] = d;
+  *out = d;
+  return TPROD_OK;
+}
+
+int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TPROD_OK : TPROD_ECUDA;
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Prefer the NCCL torch already loaded (matched by soname), else the system one.
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
+    api.Broadcast = (decltype(api.Broadcast))dlsym(lib, "ncclBroadcast");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.Broadcast && api.CommDestroy;
+  });
+  return api;
+}
+
+// ---------------------------------------------------------------- the hot path
+int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2,
+            int64_t n3, int64_t n4, cudaStream_t s) {
+  Layout32 L = layout32(n1, n2, n3, n4);
+  int st = ensure_ws(h, L.total);
+  if (st) return st;
+  const float2* tw = nullptr;
+  if ((st = get_tw32(h, (int)n3, &tw))) return st;
+  char* ws = (char*)h->ws;
+  unsigned* maxA = (unsigned*)(ws + L.off_maxA);
+  unsigned* maxB = (unsigned*)(ws + L.off_maxB);
+  __half* Ab = (__half*)(ws + L.off_Ab);
+  __half* Bb = (__half*)(ws + L.off_Bb);
+  float* Cb = (float*)(ws + L.off_Cb);
+  Twiddles32 T{tw, (int)n3};
+  int64_t launches = 0;
+
+  auto mark = [&](int i) { if (h->timing) cudaEventRecord(h->ev[i], s); };
+  h->timed_last = false;
+  mark(0);
+  CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_Ab - L.off_maxA, s));
+  launch_absmax(A, n1, n2, n3, 0, maxA, s); ++launches;          // row scales of A (i)
+  launch_absmax(B, n2, n4, n3, 1, maxB, s); ++launches;          // column scales of B (j)
+  mark(1);
+  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, s); ++launches;   // Alg.1 step 1 (A)
+  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, s); ++launches;   // Alg.1 step 1 (B)
+  mark(2);
+  if ((st = launch_status())) return st;
+  bool tc = h->engine == 0 && gemm_tc_supported();
+  if (tc) {
+    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3, maxA, maxB,
+                              h->force_bn, h->num_sms, s);
+    if (st) return st;
+  } else {
+    launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3, maxA, maxB, s);
+  }
+  ++launches;                                                     // Alg.1 step 2
+  mark(3);
+  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, C, s); ++launches;     // Alg.1 step 2b + 3
+  mark(4);
+  h->timed_last = h->timing;
+  h->last_launches = launches;
+  return launch_status();
+}
+
+int run_f64(tprod_ctx* h, const double* A, const double* B, double* C, int64_t n1, int64_t n2,
+            int64_t n3, int64_t n4, cudaStream_t s) {
+  Layout64 L = layout64(n1, n2, n3, n4);
+  int st = ensure_ws(h, L.total);
+  if (st) return st;
+  const double2* tw = nullptr;
+  if ((st = get_tw64(h, (int)n3, &tw))) return st;
+  char* ws = (char*)h->ws;
+  double* Ab = (double*)(ws + L.off_Ab);
+  double* Bb = (double*)(ws + L.off_Bb);
+  double* Cb = (double*)(ws + L.off_Cb);
+  Twiddles64 T{tw, (int)n3};
+  launch_fwd_f64(A, n1, n2, n3, T, Ab, n1, s);
+  launch_fwd_f64(B, n2, n4, n3, T, Bb, n2, s);
+  launch_gemm_simt_f64(Ab, n1, Bb, n2, Cb, n1, n1, n2, n4, L.h, s);
+  launch_inv_f64(Cb, n1, n1, n4, n3, T, C, s);
+  h->last_launches = 4;
+  return launch_status();
+}
+
+template <typename T>
+int check_call(tprod_ctx* h, const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3,
+               int64_t n4) {
+  if (!h || !A || !B || !C) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, n4);
+  if (st) return st;
+  size_t es = sizeof(T);
+  size_t bc = es * (size_t)(n1 * n4 * n3);
+  if (overlaps(C, bc, A, es * (size_t)(n1 * n2 * n3)) || overlaps(C, bc, B, es * (size_t)(n2 * n4 * n3)))
+    return TPROD_EALIAS;
+  return TPROD_OK;
+}
+
+template <typename T>
+int host_call(const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+                     void* stream, tprod_handle h) {
+  int st = check_call(h, A, B, C, n1, n2, n3, n4);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t bA = sizeof(T) * (size_t)(n1 * n2 * n3), bB = sizeof(T) * (size_t)(n2 * n4 * n3),
+         bC = sizeof(T) * (size_t)(n1 * n4 * n3);
+  if ((st = ensure_hbuf(h, 0, bA)) || (st = ensure_hbuf(h, 1, bB)) || (st = ensure_hbuf(h, 2, bC))) return st;
+  CK(cudaMemcpyAsync(h->hbuf[0], A, bA, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(h->hbuf[1], B, bB, cudaMemcpyHostToDevice, s));
+  if (sizeof(T) == 4)
+    st = run_f32(h, (const float*)h->hbuf[0], (const float*)h->hbuf[1], (float*)h->hbuf[2], n1, n2, n3, n4, s);
+  else
+    st = run_f64(h, (const double*)h->hbuf[0], (const double*)h->hbuf[1], (double*)h->hbuf[2], n1, n2, n3, n4, s);
+  if (st) return st;
+  CK(cudaMemcpyAsync(C, h->hbuf[2], bC, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return TPROD_OK;
+}
+
+}  // namespace
+
+// ====================================================================== exported C ABI
+extern "C" {
+
+int tprod_create(int device, tprod_handle* out) {
+  if (!out) return TPROD_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return TPROD_ECUDA; }
+  if (device < 0 || device >= n) return TPROD_EINVAL;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0) return TPROD_EUNSUPPORTED;   // sm_100a binary only
+  tprod_ctx* h = new tprod_ctx;
+  h->device = device;
+  h->num_sms = prop.multiProcessorCount;
+  *out = h;
+  return TPROD_OK;
+}
+
+int tprod_destroy(tprod_handle h) {
+  if (!h) return TPROD_EINVAL;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  if (h->comm && nccl().ok) nccl().CommDestroy((ncclComm_t)h->comm);
+  for (int i = 0; i < 5; ++i) if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  for (auto& kv : h->tw32) cudaFree(kv.second);
+  for (auto& kv : h->tw64) cudaFree(kv.second);
+  for (int i = 0; i < 3; ++i) if (h->hbuf[i]) cudaFree(h->hbuf[i]);
+  if (h->ws) cudaFree(h->ws);
+  delete h;
+  return TPROD_OK;
+}
+
+int tprod_f32(const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
+              int64_t n4, void* stream, tprod_handle h) {
+  int st = check_call(h, A, B, C, n1, n2, n3, n4);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  return run_f32(h, A, B, C, n1, n2, n3, n4, (cudaStream_t)stream);
+}
+
+int tprod_f64(const double* A, const double* B, double* C, int64_t n1, int64_t n2, int64_t n3,
+              int64_t n4, void* stream, tprod_handle h) {
+  int st = check_call(h, A, B, C, n1, n2, n3, n4);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  return run_f64(h, A, B, C, n1, n2, n3, n4, (cudaStream_t)stream);
+}
+
+int tprod_f32_host(const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
+                   int64_t n4, void* stream, tprod_handle h) {
+  return host_call(A, B, C, n1, n2, n3, n4, stream, h);
+}
+
+int tprod_f64_host(const double* A, const double* B, double* C, int64_t n1, int64_t n2, int64_t n3,
+                   int64_t n4, void* stream, tprod_handle h) {
+  return host_call(A, B, C, n1, n2, n3, n4, stream, h);
+}
+
+int tprod_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t n4, int dtype, size_t* out) {
+  if (!out) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, n4);
+  if (st) return st;
+  if (dtype == TPROD_DTYPE_F32) *out = layout32(n1, n2, n3, n4).total;
+  else if (dtype == TPROD_DTYPE_F64) *out = layout64(n1, n2, n3, n4).total;
+  else return TPROD_EINVAL;
+  return TPROD_OK;
+}
+
+const char* tprod_strerror(int status) {
+  switch (status) {
+    case TPROD_OK: return "ok";
+    case TPROD_EINVAL: return "invalid argument (dimension < 1, NULL pointer, size overflow or bad handle)";
+    case TPROD_EALIAS: return "output C overlaps input A or B (in-place t-product is not supported)";
+    case TPROD_ENOMEM: return "device memory allocation failed";
+    case TPROD_ECUDA: return "CUDA runtime or kernel launch error";
+    case TPROD_ENCCL: return "NCCL unavailable or an NCCL call failed";
+    case TPROD_EUNSUPPORTED: return "unsupported device or shape (requires sm_100 / B200)";
+    case TPROD_ENOWORLD: return "no NCCL world: call tprod_set_world first";
+    default: return "unknown tprod status";
+  }
+}
+
+int tprod_last_launch_count(tprod_handle h, int64_t* out) {
+  if (!h || !out) return TPROD_EINVAL;
+  *out = h->last_launches;
+  return TPROD_OK;
+}
+
+int tprod_nccl_unique_id(void* out) {
+  if (!out) return TPROD_EINVAL;
+  if (!nccl().ok) return TPROD_ENCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return TPROD_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  memcpy(out, &id, sizeof(id));
+  return TPROD_OK;
+}
+
+int tprod_set_world(tprod_handle h, int rank, int world, const void* uid) {
+  if (!h || !uid || world < 1 || rank < 0 || rank >= world) return TPROD_EINVAL;
+  if (!nccl().ok) return TPROD_ENCCL;
+  CK(cudaSetDevice(h->device));
+  if (h->comm) { nccl().CommDestroy((ncclComm_t)h->comm); h->comm = nullptr; }
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm;
+  if (nccl().CommInitRank(&comm, world, id, rank) != ncclSuccess) return TPROD_ENCCL;
+  h->comm = comm;
+  h->rank = rank;
+  h->world = world;
+  return TPROD_OK;
+}
+
+static int bcast(tprod_handle h, void* buf, int64_t count, ncclDataType_t dt, int root, void* stream) {
+  if (!h || !buf || count < 0) return TPROD_EINVAL;
+  if (!h->comm) return TPROD_ENOWORLD;
+  if (root < 0 || root >= h->world) return TPROD_EINVAL;
+  CK(cudaSetDevice(h->device));
+  if (nccl().Broadcast(buf, buf, (size_t)count, dt, root, (ncclComm_t)h->comm, (cudaStream_t)stream) != ncclSuccess)
+    return TPROD_ENCCL;
+  return TPROD_OK;
+}
+
+int tprod_bcast_f32(tprod_handle h, float* buf, int64_t count, int root, void* stream) {
+  return bcast(h, buf, count, ncclFloat32, root, stream);
+}
+int tprod_bcast_f64(tprod_handle h, double* buf, int64_t count, int root, void* stream) {
+  return bcast(h, buf, count, ncclFloat64, root, stream);
+}
+
+int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, int64_t n3,
+                  int role, void* stream, tprod_handle h) {
+  if (!h || !X || !Xre || !Xim || (role != 0 && role != 1)) return TPROD_EINVAL;
+  int st = validate_dims(p, q, n3, 1);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t hh = h_slices(n3), ld = round_up(p, 8);
+  int64_t nmax = role == 0 ? p : q;
+  size_t off_sp = align_up(4 * (size_t)nmax, 1024);
+  if ((st = ensure_ws(h, off_sp + 2 * (size_t)(hh * NPLANES * q * ld)))) return st;
+  const float2* tw = nullptr;
+  if ((st = get_tw32(h, (int)n3, &tw))) return st;
+  unsigned* mx = (unsigned*)h->ws;
+  __half* sp = (__half*)((char*)h->ws + off_sp);
+  CK(cudaMemsetAsync(mx, 0, 4 * (size_t)nmax, s));
+  launch_absmax(X, p, q, n3, role, mx, s);
+  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, s);
+  launch_decode_split(sp, ld, p, q, n3, role, mx, Xre, Xim, s);
+  h->last_launches = 3;
+  return launch_status();
+}
+
+int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int64_t q, int64_t n3,
+                   void* stream, tprod_handle h) {
+  if (!h || !Xre || !Xim || !X) return TPROD_EINVAL;
+  int st = validate_dims(p, q, n3, 1);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const float2* tw = nullptr;
+  if ((st = get_tw32(h, (int)n3, &tw))) return st;
+  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, Twiddles32{tw, (int)n3}, X, s);
+  h->last_launches = 1;
+  return launch_status();
+}
+
+int tprod_set_option(tprod_handle h, int option, int64_t value) {
+  if (!h) return TPROD_EINVAL;
+  switch (option) {
+    case TPROD_OPT_ENGINE:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->engine = (int)value;
+      return TPROD_OK;
+    case TPROD_OPT_TIMING:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      if (value && !h->ev[0]) {
+        CK(cudaSetDevice(h->device));
+        for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&h->ev[i]));
+      }
+      h->timing = value != 0;
+      return TPROD_OK;
+    case TPROD_OPT_GEMM_BN:
+      if (value != 0 && value != 64 && value != 128 && value != 256) return TPROD_EINVAL;
+      h->force_bn = (int)value;
+      return TPROD_OK;
+    default:
+      return TPROD_EINVAL;
+  }
+}
+
+int tprod_last_stage_ms(tprod_handle h, float* out) {
+  if (!h || !out || !h->timed_last) return TPROD_EINVAL;
+  CK(cudaEventSynchronize(h->ev[4]));
+  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
+  return TPROD_OK;
+}
+
+}  // extern "C"

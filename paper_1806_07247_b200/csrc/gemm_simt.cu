@@ -1,0 +1,135 @@
+// SIMT per-frequency complex GEMMs (Algorithm 1 step 2, first branch, PAPER.md:L177;
+// Eq. (10)):  C-bar_f = A-bar_f . B-bar_f  for f = 0..h-1.
+//
+//  * gemm_simt_split : fp32 path REFERENCE engine.  Reads the same split fp16 operand planes the
+//                      tcgen05 engine reads, decodes hi+lo to fp32 and accumulates in fp32.  It
+//                      exists to cross-check the tensor-core kernel on identical inputs
+//                      (TPROD_OPT_ENGINE = 1); the production fp32 path uses gemm_tc.cu.
+//  * gemm_simt_f64   : the fp64 path's GEMM (tcgen05 has no f64 kind; DFMA on CUDA cores).
+//
+// Operand layouts (internal.h): A-bar planes [f][s][l][lda] (i fastest), B-bar planes
+// [f][s][j][ldb] (l fastest), C-bar planes [f][re|im][j][ldc] (i fastest).
+#include "internal.h"
+#include "common.cuh"
+
+namespace tprod {
+
+constexpr int TS = 16;
+
+__global__ void gemm_simt_split_kernel(const __half* __restrict__ Ab, int64_t lda,
+                                       const __half* __restrict__ Bb, int64_t ldb,
+                                       float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4,
+                                       int n3, const unsigned* __restrict__ maxA,
+                                       const unsigned* __restrict__ maxB) {
+  __shared__ float sAr[TS][TS + 1], sAi[TS][TS + 1], sBr[TS][TS + 1], sBi[TS][TS + 1];
+  const int f = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i = blockIdx.x * TS + tx, j = blockIdx.y * TS + ty;
+  const int64_t pa = (int64_t)n2 * lda, pb = (int64_t)n4 * ldb;
+  const __half* A0 = Ab + (int64_t)(4 * f) * pa;
+  const __half* B0 = Bb + (int64_t)(4 * f) * pb;
+  float cr = 0.f, ci = 0.f;
+  for (int l0 = 0; l0 < n2; l0 += TS) {
+    {  // A tile: rows l = l0 + ty, cols i = blockIdx.x*TS + tx
+      int l = l0 + ty, ii = blockIdx.x * TS + tx;
+      float r = 0.f, im = 0.f;
+      if (l < n2 && ii < n1) {
+        int64_t o = (int64_t)l * lda + ii;
+        r = __half2float(A0[PL_RE_HI * pa + o]) + __half2float(A0[PL_RE_LO * pa + o]);
+        im = __half2float(A0[PL_IM_HI * pa + o]) + __half2float(A0[PL_IM_LO * pa + o]);
+      }
+      sAr[ty][tx] = r;
+      sAi[ty][tx] = im;
+    }
+    {  // B tile: rows j = blockIdx.y*TS + ty, cols l = l0 + tx
+      int l = l0 + tx, jj = blockIdx.y * TS + ty;
+      float r = 0.f, im = 0.f;
+      if (l < n2 && jj < n4) {
+        int64_t o = (int64_t)jj * ldb + l;
+        r = __half2float(B0[PL_RE_HI * pb + o]) + __half2float(B0[PL_RE_LO * pb + o]);
+        im = __half2float(B0[PL_IM_HI * pb + o]) + __half2float(B0[PL_IM_LO * pb + o]);
+      }
+      sBr[ty][tx] = r;
+      sBi[ty][tx] = im;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TS; ++kk) {
+      float ar = sAr[kk][tx], ai = sAi[kk][tx], br = sBr[ty][kk], bi = sBi[ty][kk];
+      cr = fmaf(ar, br, cr);
+      cr = fmaf(-ai, bi, cr);
+      ci = fmaf(ar, bi, ci);
+      ci = fmaf(ai, br, ci);
+    }
+    __syncthreads();
+  }
+  if (i < n1 && j < n4) {
+    int e = scale_exp(maxA[i], n3) + scale_exp(maxB[j], n3);
+    int64_t o = (int64_t)j * ldc + i;
+    int64_t pc = (int64_t)n4 * ldc;
+    Cb[(int64_t)(2 * f) * pc + o] = scalbnf(cr, -e);
+    Cb[(int64_t)(2 * f + 1) * pc + o] = scalbnf(ci, -e);
+  }
+}
+
+void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
+                            int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, int64_t n3,
+                            const unsigned* maxA, const unsigned* maxB, cudaStream_t s) {
+  dim3 grid((unsigned)((n1 + TS - 1) / TS), (unsigned)((n4 + TS - 1) / TS), (unsigned)h);
+  gemm_simt_split_kernel<<<grid, dim3(TS, TS), 0, s>>>(Ab, lda, Bb, ldb, Cb, ldc, (int)n1, (int)n2,
+                                                      (int)n4, (int)n3, maxA, maxB);
+}
+
+__global__ void gemm_simt_f64_kernel(const double* __restrict__ Ab, int64_t lda,
+                                     const double* __restrict__ Bb, int64_t ldb,
+                                     double* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4) {
+  __shared__ double sAr[TS][TS + 1], sAi[TS][TS + 1], sBr[TS][TS + 1], sBi[TS][TS + 1];
+  const int f = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i = blockIdx.x * TS + tx, j = blockIdx.y * TS + ty;
+  const int64_t pa = (int64_t)n2 * lda, pb = (int64_t)n4 * ldb;
+  const double* A0 = Ab + (int64_t)(2 * f) * pa;
+  const double* B0 = Bb + (int64_t)(2 * f) * pb;
+  double cr = 0.0, ci = 0.0;
+  for (int l0 = 0; l0 < n2; l0 += TS) {
+    {
+      int l = l0 + ty, ii = blockIdx.x * TS + tx;
+      bool ok = l < n2 && ii < n1;
+      int64_t o = (int64_t)l * lda + ii;
+      sAr[ty][tx] = ok ? A0[o] : 0.0;
+      sAi[ty][tx] = ok ? A0[pa + o] : 0.0;
+    }
+    {
+      int l = l0 + tx, jj = blockIdx.y * TS + ty;
+      bool ok = l < n2 && jj < n4;
+      int64_t o = (int64_t)jj * ldb + l;
+      sBr[ty][tx] = ok ? B0[o] : 0.0;
+      sBi[ty][tx] = ok ? B0[pb + o] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TS; ++kk) {
+      double ar = sAr[kk][tx], ai = sAi[kk][tx], br = sBr[ty][kk], bi = sBi[ty][kk];
+      cr = fma(ar, br, cr);
+      cr = fma(-ai, bi, cr);
+      ci = fma(ar, bi, ci);
+      ci = fma(ai, br, ci);
+    }
+    __syncthreads();
+  }
+  if (i < n1 && j < n4) {
+    int64_t o = (int64_t)j * ldc + i;
+    int64_t pc = (int64_t)n4 * ldc;
+    Cb[(int64_t)(2 * f) * pc + o] = cr;
+    Cb[(int64_t)(2 * f + 1) * pc + o] = ci;
+  }
+}
+
+void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64_t ldb, double* Cb,
+                          int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, cudaStream_t s) {
+  dim3 grid((unsigned)((n1 + TS - 1) / TS), (unsigned)((n4 + TS - 1) / TS), (unsigned)h);
+  gemm_simt_f64_kernel<<<grid, dim3(TS, TS), 0, s>>>(Ab, lda, Bb, ldb, Cb, ldc, (int)n1, (int)n2,
+                                                    (int)n4);
+}
+
+}  // namespace tprod

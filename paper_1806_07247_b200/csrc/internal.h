@@ -1,0 +1,68 @@
+// Internal declarations shared by the libtprod.so translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace tprod {
+
+// Number of frequency slices multiplied by Algorithm 1: ceil((n3+1)/2).
+inline int64_t h_slices(int64_t n3) { return n3 / 2 + 1; }
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------------ fp32 path data layout
+// Split spectrum of a real p x q x n3 tensor X (Matlab layout, p fastest):
+//   planes [f][s][q][ld] of __half, f < h, s in {Re_hi, Re_lo, Im_hi, Im_lo}, ld >= p, ld % 8 == 0
+// value(f,p,q) = (hi + lo) * 2^-e  where e = scale exponent of p (A role) or q (B role).
+// For A (p = i, q = l) this is an MN-major M x K operand; for B (p = l, q = j) a K-major N x K
+// operand of the per-frequency GEMM.  C-bar is fp32 planes [f][re|im][j][ldc] (i fastest).
+enum { PL_RE_HI = 0, PL_RE_LO = 1, PL_IM_HI = 2, PL_IM_LO = 3, NPLANES = 4 };
+
+struct Twiddles32 { const float2* tw; int n3; };   // tw[m] = (cos 2pi m/n3, sin 2pi m/n3)
+struct Twiddles64 { const double2* tw; int n3; };
+
+// K0: per-index max |x| as float bits (non-negative floats order like unsigned ints).
+// role 0: max over (q,k) for every p;  role 1: max over (p,k) for every q.
+void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
+                   unsigned* maxbits, cudaStream_t s);
+
+// K1: forward DFT (Hermitian half), exact power-of-two scaling, fp16 hi/lo split.
+void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
+                      const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
+                      cudaStream_t s);
+// decode split planes back to fp32 planes [f][q][p] (stage test entry only)
+void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
+                         const unsigned* maxbits, float* re, float* im, cudaStream_t s);
+
+// K2 (reference SIMT engine): C-bar_f = A-bar_f B-bar_f on split operands, unscaled in epilogue.
+void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
+                            float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
+                            int64_t n3, const unsigned* maxA, const unsigned* maxB, cudaStream_t s);
+
+// K2 (tcgen05 engine).  Returns false if the shape/device is not supported by the kernel.
+bool gemm_tc_supported();
+int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
+                         float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
+                         int64_t n3, const unsigned* maxA, const unsigned* maxB, int force_bn,
+                         int num_sms, cudaStream_t s);
+
+// K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
+// Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).
+void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
+                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, cudaStream_t s);
+
+// ------------------------------------------------------------------ fp64 path
+// spectra as fp64 planes [f][re|im][q][ld]
+void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
+                    double* out, int64_t ld, cudaStream_t s);
+void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64_t ldb,
+                          double* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
+                          cudaStream_t s);
+void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
+                    double* X, cudaStream_t s);
+
+// Host-side exact twiddle table: (cos, sin)(2 pi m / n), m = 0..n-1, computed in fp64 with exact
+// quadrant reduction so that m = 0, n/4, n/2, 3n/4 give exactly 0 / +-1.
+void host_twiddles(int n, double* cs /* 2n: cos,sin interleaved */);
+
+}  // namespace tprod

@@ -1,0 +1,264 @@
+// Mode-3 transforms of the t-product hot path (Algorithm 1 steps 1 and 3).
+//
+//   K0 absmax      : per-row / per-column max |x|  -> exact power-of-two operand scales
+//   K1 fwd_split   : X-bar_f(p,q) = sum_k X(p,q,k) w^{fk}, w = e^{-2 pi i/n3} (Eq. (2)),
+//                    f = 0..h-1 only (Hermitian half, Eq. (8)), scaled by 2^e and split
+//                    into fp16 hi/lo planes = the GEMM's operand format
+//   K3 inv         : C(p,q,t) = (1/n3) [Re C-bar_0 + sum_{f=1}^{h-1} w_f Re(C-bar_f e^{+2 pi i f t/n3})]
+//                    with w_f = 2, except w = 1 for f = n3/2 (even n3): the conjugate fill of
+//                    Alg. 1 step 2 (L177) fused into the inverse DFT (L126); slices h..n3-1 are
+//                    never materialised, the DC/Nyquist imaginary parts are discarded (C2R).
+//
+// Layout of X: element (p,q,k) at p + P*q + P*Q*k (Matlab layout); consecutive
+// threads take consecutive p, so every global access is coalesced along the contiguous dim.
+#include "internal.h"
+#include "common.cuh"
+
+#include <math.h>
+
+namespace tprod {
+
+// ------------------------------------------------------------------------------------ twiddles
+void host_twiddles(int n, double* cs) {
+  // angle = 2 pi m / n.  Reduce m to the first octant exactly with integer arithmetic so that
+  // the symmetric values are bit-identical and the axis values are exact.
+  for (int m = 0; m < n; ++m) {
+    // use 8m/n to find the octant without rounding: work with r = m (mod n) scaled by 8
+    long long num = 8LL * m;           // angle / (pi/4) = 8m/n
+    int oct = (int)(num / n);          // 0..7
+    long long rem = num - (long long)oct * n;  // remainder in [0, n): angle within octant = rem/n * pi/4
+    double a = (M_PI / 4.0) * ((double)rem / (double)n);
+    double c, s;
+    // base angle phi = oct*pi/4 + a
+    switch (oct) {
+      case 0: c = cos(a);                        s = sin(a); break;
+      case 1: c = sin(M_PI / 4.0 - a);           s = cos(M_PI / 4.0 - a); break;
+      case 2: c = -sin(a);                       s = cos(a); break;
+      case 3: c = -cos(M_PI / 4.0 - a);          s = sin(M_PI / 4.0 - a); break;
+      case 4: c = -cos(a);                       s = -sin(a); break;
+      case 5: c = -sin(M_PI / 4.0 - a);          s = -cos(M_PI / 4.0 - a); break;
+      case 6: c = sin(a);                        s = -cos(a); break;
+      default: c = cos(M_PI / 4.0 - a);          s = -sin(M_PI / 4.0 - a); break;
+    }
+    cs[2 * m] = c;
+    cs[2 * m + 1] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------ K0
+// role 0: max over (q,k) for each p  (A rows i);  role 1: max over (p,k) for each q (B cols j)
+__global__ void absmax_p_kernel(const float* __restrict__ X, int64_t P, int64_t ncols,
+                                unsigned* __restrict__ maxbits) {
+  // blockDim = (32, 8): x -> p within a 32-chunk, y -> columns (q,k) flattened
+  __shared__ float red[8][33];
+  int64_t p = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  float m = 0.f;
+  if (p < P) {
+    for (int64_t c = (int64_t)blockIdx.y * 8 + threadIdx.y; c < ncols; c += (int64_t)gridDim.y * 8)
+      m = fmaxf(m, fabsf(__ldg(X + p + P * c)));
+  }
+  red[threadIdx.y][threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.y == 0 && p < P) {
+    for (int r = 1; r < 8; ++r) m = fmaxf(m, red[r][threadIdx.x]);
+    atomicMax(maxbits + p, __float_as_uint(m));
+  }
+}
+
+__global__ void absmax_q_kernel(const float* __restrict__ X, int64_t P, int64_t Q, int64_t n3,
+                                unsigned* __restrict__ maxbits) {
+  // one warp per run (q,k): the contiguous P elements X(:, q, k)
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < Q * n3; r += nwarps) {
+    int64_t q = r % Q, k = r / Q;
+    const float* x = X + P * q + P * Q * k;
+    float m = 0.f;
+    for (int64_t p = lane; p < P; p += 32) m = fmaxf(m, fabsf(__ldg(x + p)));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) atomicMax(maxbits + q, __float_as_uint(m));
+  }
+}
+
+void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role, unsigned* maxbits,
+                   cudaStream_t s) {
+  if (role == 0) {
+    int64_t ncols = Q * n3;
+    int64_t gx = (P + 31) / 32;
+    int64_t gy = (ncols + 7) / 8;
+    int64_t target = 148 * 16;  // enough CTAs to saturate HBM
+    int64_t cap = (target + gx - 1) / gx;
+    if (gy > cap) gy = cap;
+    if (gy > 65535) gy = 65535;
+    if (gy < 1) gy = 1;
+    absmax_p_kernel<<<dim3((unsigned)gx, (unsigned)gy), dim3(32, 8), 0, s>>>(X, P, ncols, maxbits);
+  } else {
+    int64_t runs = Q * n3;
+    int64_t blocks = (runs * 32 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    absmax_q_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, P, Q, n3, maxbits);
+  }
+}
+
+// ------------------------------------------------------------------------------------ K1 (fp32)
+template <int ROLE>
+__global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t Q, int n3, int h,
+                                 const unsigned* __restrict__ maxbits,
+                                 const float2* __restrict__ tw, __half* __restrict__ out,
+                                 int64_t ld) {
+  extern __shared__ float2 stw[];
+  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw[m] = tw[m];
+  __syncthreads();
+  int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
+  int64_t q = blockIdx.x / pblocks;
+  int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int64_t PQ = P * Q;
+  const float* x = X + p + P * q;
+  const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), n3);
+  const int64_t plane = Q * ld;
+  __half* o = out + q * ld + p;
+  for (int f = 0; f < h; ++f) {
+    float re = 0.f, im = 0.f;
+    int m = 0;
+    for (int k = 0; k < n3; ++k) {
+      float v = __ldg(x + PQ * k);
+      float2 w = stw[m];
+      re = fmaf(v, w.x, re);
+      im = fmaf(-v, w.y, im);       // w^{fk} = cos - i sin
+      m += f;
+      if (m >= n3) m -= n3;
+    }
+    __half hi, lo;
+    split_f16(scalbnf(re, e), hi, lo);
+    o[(int64_t)(4 * f + PL_RE_HI) * plane] = hi;
+    o[(int64_t)(4 * f + PL_RE_LO) * plane] = lo;
+    split_f16(scalbnf(im, e), hi, lo);
+    o[(int64_t)(4 * f + PL_IM_HI) * plane] = hi;
+    o[(int64_t)(4 * f + PL_IM_LO) * plane] = lo;
+  }
+}
+
+void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
+                      const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
+                      cudaStream_t s) {
+  const int threads = 128;
+  int64_t blocks = (P + threads - 1) / threads * Q;
+  size_t smem = sizeof(float2) * (size_t)n3;
+  int h = (int)h_slices(n3);
+  if (role == 0)
+    fwd_split_kernel<0><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld);
+  else
+    fwd_split_kernel<1><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld);
+}
+
+__global__ void decode_split_kernel(const __half* __restrict__ in, int64_t ld, int64_t P, int64_t Q,
+                                    int n3, int h, int role, const unsigned* __restrict__ maxbits,
+                                    float* __restrict__ re, float* __restrict__ im) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)h * P * Q;
+  if (idx >= total) return;
+  int64_t p = idx % P, q = (idx / P) % Q, f = idx / (P * Q);
+  int e = scale_exp(maxbits[role == 0 ? p : q], n3);
+  const int64_t plane = Q * ld;
+  const __half* b = in + q * ld + p;
+  float r = __half2float(b[(4 * f + PL_RE_HI) * plane]) + __half2float(b[(4 * f + PL_RE_LO) * plane]);
+  float i = __half2float(b[(4 * f + PL_IM_HI) * plane]) + __half2float(b[(4 * f + PL_IM_LO) * plane]);
+  re[idx] = scalbnf(r, -e);
+  im[idx] = scalbnf(i, -e);
+}
+
+void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
+                         const unsigned* maxbits, float* re, float* im, cudaStream_t s) {
+  int64_t total = h_slices(n3) * P * Q;
+  decode_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+      in, ld, P, Q, (int)n3, (int)h_slices(n3), role, maxbits, re, im);
+}
+
+// ------------------------------------------------------------------------------------ K3 (fp32)
+template <typename T, typename T2>
+__global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim, int64_t ld,
+                           int64_t fstride, int64_t P, int64_t Q, int n3, int h,
+                           const T2* __restrict__ tw, T* __restrict__ X) {
+  extern __shared__ unsigned char smem_raw[];
+  T2* stw = reinterpret_cast<T2*>(smem_raw);
+  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw[m] = tw[m];
+  __syncthreads();
+  int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
+  int64_t q = blockIdx.x / pblocks;
+  int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const T* cr = Cre + q * ld + p;
+  const T* ci = Cim + q * ld + p;
+  const T inv_n = T(1) / T(n3);
+  for (int t = 0; t < n3; ++t) {
+    T acc = cr[0];                      // Re C-bar_0 (Im of DC discarded)
+    int m = 0;
+    for (int f = 1; f < h; ++f) {
+      m += t;
+      if (m >= n3) m -= n3;             // m = f t mod n3
+      T2 w = stw[m];
+      T r = cr[(int64_t)f * fstride], i = ci[(int64_t)f * fstride];
+      T v = r * w.x - i * w.y;          // Re(C-bar_f e^{+i theta})
+      acc += (2 * f == n3) ? v : T(2) * v;
+    }
+    X[p + P * q + P * Q * (int64_t)t] = acc * inv_n;
+  }
+}
+
+void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
+                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, cudaStream_t s) {
+  const int threads = 128;
+  int64_t blocks = (P + threads - 1) / threads * Q;
+  inv_kernel<float, float2><<<(unsigned)blocks, threads, sizeof(float2) * n3, s>>>(
+      Cre, Cim, ld, fstride, P, Q, (int)n3, (int)h_slices(n3), tw.tw, X);
+}
+
+// ------------------------------------------------------------------------------------ fp64 path
+__global__ void fwd_f64_kernel(const double* __restrict__ X, int64_t P, int64_t Q, int n3, int h,
+                               const double2* __restrict__ tw, double* __restrict__ out, int64_t ld) {
+  extern __shared__ double2 stw64[];
+  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw64[m] = tw[m];
+  __syncthreads();
+  int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
+  int64_t q = blockIdx.x / pblocks;
+  int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const int64_t PQ = P * Q;
+  const double* x = X + p + P * q;
+  const int64_t plane = Q * ld;
+  double* o = out + q * ld + p;
+  for (int f = 0; f < h; ++f) {
+    double re = 0.0, im = 0.0;
+    int m = 0;
+    for (int k = 0; k < n3; ++k) {
+      double v = x[PQ * k];
+      double2 w = stw64[m];
+      re = fma(v, w.x, re);
+      im = fma(-v, w.y, im);
+      m += f;
+      if (m >= n3) m -= n3;
+    }
+    o[(int64_t)(2 * f) * plane] = re;
+    o[(int64_t)(2 * f + 1) * plane] = im;
+  }
+}
+
+void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw, double* out,
+                    int64_t ld, cudaStream_t s) {
+  const int threads = 128;
+  int64_t blocks = (P + threads - 1) / threads * Q;
+  fwd_f64_kernel<<<(unsigned)blocks, threads, sizeof(double2) * n3, s>>>(
+      X, P, Q, (int)n3, (int)h_slices(n3), tw.tw, out, ld);
+}
+
+void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
+                    double* X, cudaStream_t s) {
+  const int threads = 128;
+  int64_t blocks = (P + threads - 1) / threads * Q;
+  inv_kernel<double, double2><<<(unsigned)blocks, threads, sizeof(double2) * n3, s>>>(
+      Cb, Cb + Q * ld, ld, 2 * Q * ld, P, Q, (int)n3, (int)h_slices(n3), tw.tw, X);
+}
+
+}  // namespace tprod

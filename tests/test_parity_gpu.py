@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by element.
+
+Bar (BASELINE.json north_star): relative Frobenius error <= 1e-5 on the fp32 path and <= 1e-12
+on the fp64 path, the oracle always evaluated on the exact (rounded) values the GPU saw."""
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import CONFIGS, lateral_shard, normal, sample_columns
+
+pytestmark = pytest.mark.gpu
+
+TOL32, TOL64 = 1e-5, 1e-12
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1806_07247_b200 import build
+    build.build()
+    import paper_1806_07247_b200 as tp
+    return tp
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.asfortranarray(x)).cuda()
+
+
+def host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def gpu_tprod(T, A, B, handle=None):
+    return host(T.tprod(dev(A), dev(B), handle=handle))
+
+
+# ------------------------------------------------------------------------------- config 1
+def test_config1_fp64(T):
+    c = CONFIGS["c1"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"], np.float64)
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"], np.float64)
+    D = normal((c["n4"], 8, c["n3"]), c["seedD"], np.float64)
+    ref = O.tprod_bcirc(A, B)
+    C = gpu_tprod(T, A, B)
+    assert O.rel_err(C, ref) <= TOL64
+    # A * teye = A and associativity, through the GPU path
+    I = O.teye(c["n2"], c["n3"])
+    assert O.rel_err(gpu_tprod(T, A, I), A) <= TOL64
+    lhs = gpu_tprod(T, C, D)
+    rhs = gpu_tprod(T, A, gpu_tprod(T, B, D))
+    assert O.rel_err(lhs, O.tprod_bcirc(ref, D)) <= TOL64
+    assert O.rel_err(lhs, rhs) <= 10 * TOL64
+
+
+def test_config1_dims_fp32(T):
+    """Unaligned dims (n1*n2 % 8 != 0, n2 = 30) on the fp32 path."""
+    c = CONFIGS["c1"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"], np.float32)
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"], np.float32)
+    assert O.rel_err(gpu_tprod(T, A, B), O.tprod_bcirc(A, B)) <= TOL32
+
+
+# ------------------------------------------------------------------------------- config 2
+def test_config2_full(T):
+    c = CONFIGS["c2"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"])
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"])
+    err = O.rel_err(gpu_tprod(T, A, B), O.tprod_bcirc(A, B))
+    print("config2 rel_err", err)
+    assert err <= TOL32
+
+
+# ------------------------------------------------------------------------------- shape sweep
+SWEEP = [
+    (1, 1, 1, 1), (1, 1, 2, 1), (2, 3, 1, 4), (3, 2, 2, 5), (5, 4, 3, 2), (7, 9, 4, 6),
+    (16, 8, 5, 24), (33, 17, 6, 31), (64, 64, 7, 64), (129, 65, 8, 130), (130, 200, 9, 70),
+    (255, 129, 31, 257), (128, 256, 32, 128), (300, 260, 31, 200), (40, 50, 64, 30),
+    (200, 136, 3, 264), (8, 1000, 2, 8), (1000, 8, 2, 3),
+]
+
+
+@pytest.mark.parametrize("dims", SWEEP, ids=lambda d: "x".join(map(str, d)))
+def test_sweep_fp32(T, dims):
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 100 + n1 + n3)
+    B = normal((n2, n4, n3), 200 + n4 + n3)
+    err = O.rel_err(gpu_tprod(T, A, B), O.tprod_bcirc(A, B))
+    assert err <= TOL32, err
+
+
+@pytest.mark.parametrize("dims", SWEEP[:12], ids=lambda d: "x".join(map(str, d)))
+def test_sweep_fp64(T, dims):
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 300 + n1 + n3, np.float64)
+    B = normal((n2, n4, n3), 400 + n4 + n3, np.float64)
+    assert O.rel_err(gpu_tprod(T, A, B), O.tprod_bcirc(A, B)) <= TOL64
+
+
+def test_simt_engine_cross_check(T):
+    """The SIMT reference engine and the tcgen05 engine on identical split operands."""
+    h = T.Handle()
+    A = normal((300, 260, 31), 5)
+    B = normal((260, 200, 31), 6)
+    ref = O.tprod_bcirc(A, B)
+    C_tc = gpu_tprod(T, A, B, handle=h)
+    h.set_option(T._lib.TPROD_OPT_ENGINE, 1)
+    C_simt = gpu_tprod(T, A, B, handle=h)
+    assert O.rel_err(C_tc, ref) <= TOL32
+    assert O.rel_err(C_simt, ref) <= TOL32
+    assert O.rel_err(C_tc, C_simt) <= TOL32
+
+
+# ------------------------------------------------------------------------------- stages
+@pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 100, 4096])
+def test_stage_forward_dft(T, n3):
+    """S1/S2 vs numpy.fft.rfft (library special case), both operand roles."""
+    p, q = (37, 5) if n3 > 64 else (133, 9)
+    X = normal((p, q, n3), 7 + n3)
+    ref = np.fft.rfft(X.astype(np.float64), axis=2)
+    for role in (0, 1):
+        got = host(T.dft_f32(dev(X), role=role))
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err < 2e-6, (role, err)
+
+
+@pytest.mark.parametrize("n3", [1, 2, 7, 31, 32, 64, 4096])
+def test_stage_inverse_roundtrip(T, n3):
+    """S4(S1(X)) = X and the 1x1xn3 circular-convolution worked example."""
+    import torch
+    X = normal((45, 3, n3), 17 + n3)
+    Xb = torch.from_numpy(np.fft.rfft(X.astype(np.float64), axis=2).astype(np.complex64)).cuda()
+    back = host(T.idft_f32(Xb, n3))
+    assert np.linalg.norm(back - X) / np.linalg.norm(X) < 2e-6
+
+
+def test_worked_examples_on_gpu(T, golden):
+    for dt in (np.float32, np.float64):
+        g = golden["tprod_tubes_1x1x3"]
+        a = np.array(g["a"], dt).reshape(1, 1, -1)
+        b = np.array(g["b"], dt).reshape(1, 1, -1)
+        np.testing.assert_allclose(gpu_tprod(T, a, b)[0, 0], g["c"], rtol=1e-6)
+        g = golden["tprod_n3_1"]
+        A = np.array(g["A"], dt)[:, :, None]
+        B = np.array(g["B"], dt)[:, :, None]
+        np.testing.assert_allclose(gpu_tprod(T, A, B)[:, :, 0], g["C"], rtol=1e-6)
+
+
+# ------------------------------------------------------------------------------- invariants
+def test_identity_shift_transpose_fp32(T):
+    A = normal((70, 50, 12), 1)
+    B = normal((50, 40, 12), 2)
+    I = O.teye(50, 12).astype(np.float32)
+    assert O.rel_err(gpu_tprod(T, A, I), A) <= TOL32
+    C = gpu_tprod(T, A, B)
+    Cs = gpu_tprod(T, A, np.roll(B, 5, axis=2))
+    assert O.rel_err(Cs, np.roll(C, 5, axis=2)) <= TOL32
+    Ct = gpu_tprod(T, np.ascontiguousarray(O.tran(B)), np.ascontiguousarray(O.tran(A)))
+    assert O.rel_err(Ct, O.tran(C)) <= TOL32
+
+
+def test_determinism_and_w_invariance(T):
+    """Bitwise-repeatable, and lateral-slice shards equal the matching columns of the full
+    result bitwise (no split-K; K order independent of n4) -- the multi-GPU partition run
+    sequentially on one GPU."""
+    A = normal((256, 192, 31), 3)
+    B = normal((192, 300, 31), 4)
+    C1 = gpu_tprod(T, A, B)
+    C2 = gpu_tprod(T, A, B)
+    assert np.array_equal(C1, C2)
+    for W in (2, 3, 4):
+        for r in range(W):
+            s, e = lateral_shard(300, W, r)
+            Cr = gpu_tprod(T, A, np.asfortranarray(B[:, s:e, :]))
+            assert np.array_equal(Cr, C1[:, s:e, :]), (W, r)
+
+
+def test_errors(T):
+    import torch
+    A = T.to_matlab(torch.randn(4, 5, 6, device="cuda"))
+    B = T.to_matlab(torch.randn(5, 3, 6, device="cuda"))
+    with pytest.raises(ValueError, match="shape mismatch"):
+        T.tprod(A, T.to_matlab(torch.randn(4, 3, 6, device="cuda")))
+    with pytest.raises(ValueError, match="Matlab layout"):
+        T.tprod(torch.randn(4, 5, 6, device="cuda"), B)
+    # aliasing output with an input -> TPROD_EALIAS from the C ABI
+    X = T.to_matlab(torch.randn(4, 4, 6, device="cuda"))
+    with pytest.raises(T.TprodError) as e:
+        T.tprod(X, T.to_matlab(torch.randn(4, 4, 6, device="cuda")), out=X)
+    assert e.value.status == T._lib.TPROD_EALIAS
+
+
+# ------------------------------------------------------------------------------- full sizes
+def _c3_inputs(rank5=False):
+    c = CONFIGS["c3"]
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"])
+    if rank5:
+        U = normal((c["n1"], c["rank"], c["n3"]), c["seedU"], np.float64)
+        V = normal((c["rank"], c["n2"], c["n3"]), c["seedV"], np.float64)
+        A = O.tprod_bcirc(U, V).astype(np.float32)     # A' = U*V by the oracle, rounded to fp32
+    else:
+        A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"])
+    return A, B
+
+
+@pytest.mark.parametrize("rank5", [False, True], ids=["iid", "rank5"])
+def test_config3_sampled(T, rank5):
+    A, B = _c3_inputs(rank5)
+    C = gpu_tprod(T, A, B)
+    J = sample_columns(B.shape[1], 48)
+    ref = O.tprod_columns(A, B, J)
+    err = O.rel_err(C[:, J, :], ref)
+    print("config3", "rank5" if rank5 else "iid", "sampled rel_err", err)
+    assert err <= TOL32
+    if rank5:
+        # tubal rank <= 5 (Def. 2.7): every Fourier slice of C has sigma_6 / sigma_1 at fp32 noise
+        Cb = np.fft.rfft(C[:, :64, :].astype(np.float64), axis=2)
+        for f in range(0, Cb.shape[2], 5):
+            s = np.linalg.svd(Cb[:, :, f], compute_uv=False)
+            assert s[5] / s[0] < 1e-4
+
+
+def test_config4_sampled(T):
+    c = CONFIGS["c4"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"])
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"])
+    C = gpu_tprod(T, A, B)
+    J = np.array([0, 17, 63])
+    tl = np.array([0, 1, 2, 1000, 2048, 4095])
+    ref = O.tprod_blockrow(A, B, tl, J)
+    err = O.rel_err(C[:, J][:, :, tl], ref)
+    print("config4 sampled rel_err", err)
+    assert err <= TOL32
+
+
+@pytest.mark.slow
+def test_config5_sampled(T):
+    import torch
+    c = CONFIGS["c5"]
+    A = normal((c["n1"], c["n2"], c["n3"]), c["seedA"])
+    B = normal((c["n2"], c["n4"], c["n3"]), c["seedB"])
+    J = sample_columns(c["n4"], 32)
+    ref = O.tprod_columns(A, B, J)
+    Ad, Bd = dev(A), dev(B)
+    C = T.tprod(Ad, Bd)
+    Cj = host(C[:, torch.from_numpy(J).cuda(), :])
+    err = O.rel_err(Cj, ref)
+    print("config5 sampled rel_err", err)
+    assert err <= TOL32
