@@ -1,11 +1,365 @@
-// tcgen05 per-frequency complex GEMM -- placeholder until the tensor-core kernel lands.
+// K2: per-frequency complex GEMM on 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+//   C-bar_f = A-bar_f . B-bar_f,  f = 0..h-1       (Algorithm 1 step 2, first branch, PAPER.md:L177;
+//                                                   Eq. (10))
+// Operands are the split fp16 planes written by K1 (internal.h):
+//   A-bar_f ~ 2^-e_i (Arh + Arl + i(Aih + Ail)),  B-bar_f ~ 2^-e_j (Brh + Brl + i(Bih + Bil))
+// and each real product X.Y is evaluated as Xh.Yh + Xh.Yl + Xl.Yh (the lo.lo term is below fp32
+// rounding), with the complex product in the 4M form
+//   Cr = Ar.Br - Ai.Bi,   Ci = Ar.Bi + Ai.Br        (-Ai via the instruction descriptor's negate-A bit)
+// i.e. 12 tcgen05.mma.kind::f16 per K step, all accumulating in fp32 in TMEM (Cr in columns
+// [0, BN), Ci in [BN, 2 BN)).  The epilogue multiplies by 2^-(e_i + e_j) (exact) and stores fp32
+// planes [f][re|im][j][i] coalesced along i.
+//
+// Kernel structure (one 128 x BN output tile of one frequency per CTA, 128 threads):
+//   warp 0 / lane 0 : TMA producer -- per K block of BK=32: 8 boxes of A (4 planes x 2 M-halves,
+//                     MN-major, 128B swizzle) + 4 boxes of B (4 planes, K-major, 64B swizzle)
+//                     into a STAGES-deep ring guarded by full/empty mbarriers
+//   warp 1 / lane 0 : MMA issuer -- waits full[s], issues 24 MMAs (M=128, N=BN, K=16), commits
+//                     empty[s]; after the last K block commits tmem_full
+//   all 4 warps     : epilogue -- tcgen05.ld 32x32b.x16 from TMEM lanes 32w..32w+31, scale, store
+// Deterministic: fixed K order, no split-K, no atomics (C column j independent of n4).
 #include "internal.h"
+#include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 
 namespace tprod {
-bool gemm_tc_supported() { return false; }
-int launch_gemm_tc_split(const __half*, int64_t, const __half*, int64_t, float*, int64_t, int64_t,
-                         int64_t, int64_t, int64_t, int64_t, const unsigned*, const unsigned*, int,
-                         int, cudaStream_t) {
-  return 6;
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;            // K elements per stage (64 B rows for the K-major B operand)
+constexpr int NTHREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"): start, leading/stride byte offsets,
+// swizzle mode in bits 61-63 (2 = 128B, 4 = 64B, 6 = 32B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t swz) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)swz << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D f32, A/B f16, A MN-major, B K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int negA) {
+  return (1u << 4)                      // c_format = F32
+         | (0u << 7) | (0u << 10)       // a_format = b_format = F16
+         | ((uint32_t)negA << 13)       // negate A
+         | (1u << 15)                   // A MN-major
+         | (0u << 16)                   // B K-major
+         | ((uint32_t)(N >> 3) << 17)   // N / 8
+         | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_PLANE = BK * BM * 2;                  // bytes: BK rows x 128 i x fp16
+  static constexpr int B_PLANE = BN * BK * 2;                  // bytes: BN rows x BK l x fp16
+  static constexpr int STAGE = NPLANES * (A_PLANE + B_PLANE);
+  static constexpr int STAGES = (BN == 256) ? 2 : (BN == 128 ? 3 : 4);
+  static constexpr int TMEM_COLS = 2 * BN;                     // Cr | Ci  (power of two)
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + 4 * BN;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int n3,
+                   const unsigned* __restrict__ maxA, const unsigned* __restrict__ maxB) {
+  using G = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + G::STAGES * G::STAGE);
+  uint64_t* empty = full + G::STAGES;
+  uint64_t* tmem_full = empty + G::STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+  int* sExpB = (int*)(smem + G::STAGES * G::STAGE + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, f = blockIdx.z;
+  const int nk = (n2 + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < G::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // whole warp allocates TMEM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(G::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int x = threadIdx.x; x < BN; x += NTHREADS)
+    sExpB[x] = (n0 + x < n4) ? scale_exp(maxB[n0 + x], n3) : 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % G::STAGES;
+      const uint32_t ph = (kb / G::STAGES) & 1;
+      mbar_wait(empty + s, ph ^ 1);
+      uint8_t* st = smem + s * G::STAGE;
+      mbar_expect_tx(full + s, G::STAGE);
+      const int k0 = kb * BK;
+#pragma unroll
+      for (int p = 0; p < NPLANES; ++p) {
+        uint8_t* a = st + p * G::A_PLANE;
+        tma_load_3d(a, &tmA, full + s, m0, k0, 4 * f + p);
+        tma_load_3d(a + BK * 128, &tmA, full + s, m0 + 64, k0, 4 * f + p);
+        uint8_t* b = st + NPLANES * G::A_PLANE + p * G::B_PLANE;
+        tma_load_3d(b, &tmB, full + s, k0, n0, 4 * f + p);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t ID_POS = idesc_f16(BM, BN, 0);
+    constexpr uint32_t ID_NEG = idesc_f16(BM, BN, 1);
+    const uint32_t tCr = tmem, tCi = tmem + BN;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % G::STAGES;
+      const uint32_t ph = (kb / G::STAGES) & 1;
+      mbar_wait(full + s, ph);
+      tc_fence_after();
+      const uint32_t base = smem_u32(smem + s * G::STAGE);
+      const uint32_t bbase = base + NPLANES * G::A_PLANE;
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        // A (MN-major, SW128): LBO = distance between the two 64-row halves, SBO = 8 K-rows
+        uint64_t a[NPLANES], b[NPLANES];
+#pragma unroll
+        for (int p = 0; p < NPLANES; ++p) {
+          a[p] = sdesc(base + p * G::A_PLANE + ks * 2048, BK * 128, 1024, 2);
+          b[p] = sdesc(bbase + p * G::B_PLANE + ks * 32, 16, 512, 4);
+        }
+        const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+        // Cr = Ar.Br - Ai.Bi
+        mma_f16(tCr, a[PL_RE_HI], b[PL_RE_HI], ID_POS, acc0);
+        mma_f16(tCr, a[PL_RE_HI], b[PL_RE_LO], ID_POS, 1);
+        mma_f16(tCr, a[PL_RE_LO], b[PL_RE_HI], ID_POS, 1);
+        mma_f16(tCr, a[PL_IM_HI], b[PL_IM_HI], ID_NEG, 1);
+        mma_f16(tCr, a[PL_IM_HI], b[PL_IM_LO], ID_NEG, 1);
+        mma_f16(tCr, a[PL_IM_LO], b[PL_IM_HI], ID_NEG, 1);
+        // Ci = Ar.Bi + Ai.Br
+        mma_f16(tCi, a[PL_RE_HI], b[PL_IM_HI], ID_POS, acc0);
+        mma_f16(tCi, a[PL_RE_HI], b[PL_IM_LO], ID_POS, 1);
+        mma_f16(tCi, a[PL_RE_LO], b[PL_IM_HI], ID_POS, 1);
+        mma_f16(tCi, a[PL_IM_HI], b[PL_RE_HI], ID_POS, 1);
+        mma_f16(tCi, a[PL_IM_HI], b[PL_RE_LO], ID_POS, 1);
+        mma_f16(tCi, a[PL_IM_LO], b[PL_RE_HI], ID_POS, 1);
+      }
+      mma_commit(empty + s);               // frees the smem slot when these MMAs have read it
+    }
+    mma_commit(tmem_full);                 // accumulators complete
+  }
+
+  // ------------------------------------------------------------ epilogue (all 4 warps)
+  __syncwarp();
+  mbar_wait(tmem_full, 0);
+  tc_fence_after();
+  const int i = m0 + warp * 32 + lane;
+  const int eA = (i < n1) ? scale_exp(maxA[i], n3) : 0;
+  const int64_t plane = (int64_t)n4 * ldc;
+  float* Cr = Cb + (int64_t)(2 * f) * plane + i;
+  float* Ci = Cr + plane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    if (n0 + c >= n4) break;
+    float vr[16], vi[16];
+    tmem_ld16(trow + c, vr);
+    tmem_ld16(trow + BN + c, vi);
+    if (i < n1) {
+#pragma unroll
+      for (int x = 0; x < 16; ++x) {
+        const int j = n0 + c + x;
+        if (j < n4) {
+          const int e = eA + sExpB[c + x];
+          Cr[(int64_t)j * ldc] = scalbnf(vr[x], -e);
+          Ci[(int64_t)j * ldc] = scalbnf(vi[x], -e);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(G::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// 3-D fp16 tensor map: dims {d0, d1, d2}, row pitch ld0 elements (d0 contiguous), plane pitch
+// d1*ld0 elements; box {b0, b1, 1}.
+bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld0,
+              uint32_t b0, uint32_t b1, CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {ld0 * 2, d1 * ld0 * 2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN>
+int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
+              int64_t n2, int64_t n4, int64_t h, int64_t n3, const unsigned* maxA,
+              const unsigned* maxB, cudaStream_t s) {
+  using G = Cfg<BN>;
+  CUtensorMap mb;
+  if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN,
+                CU_TENSOR_MAP_SWIZZLE_64B))
+    return 4;
+  if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) !=
+      cudaSuccess)
+    return 4;
+  dim3 grid((unsigned)((n1 + BM - 1) / BM), (unsigned)((n4 + BN - 1) / BN), (unsigned)h);
+  gemm_tc_kernel<BN><<<grid, NTHREADS, G::SMEM, s>>>(ma, mb, Cb, ldc, (int)n1, (int)n2, (int)n4, (int)n3,
+                                                     maxA, maxB);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+}  // namespace tc
+
+bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
+
+int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
+                         int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, int64_t n3,
+                         const unsigned* maxA, const unsigned* maxB, int force_bn, int num_sms,
+                         cudaStream_t s) {
+  CUtensorMap ma;
+  if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
+                    tc::BK, CU_TENSOR_MAP_SWIZZLE_128B))
+    return 4;
+  int bn = force_bn;
+  if (bn == 0) {
+    // largest N tile that still gives every SM at least one tile
+    const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
+    bn = 64;
+    for (int cand : {256, 128}) {
+      if (mt * ((n4 + cand - 1) / cand) * h >= num_sms) { bn = cand; break; }
+    }
+  }
+  switch (bn) {
+    case 256: return tc::launch_bn<256>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
+    case 128: return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
+    default: return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
+  }
+}
+
 }  // namespace tprod
