@@ -127,7 +127,7 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
 
 /* Options (tests / benchmarking).  TPROD_OPT_ENGINE: 0 = auto (tcgen05), 1 = SIMT reference
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
- * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64/128/256). */
+ * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3 };
 int tprod_set_option(tprod_handle h, int option, int64_t value);
 

@@ -489,7 +489,7 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       h->timing = value != 0;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:
-      if (value != 0 && value != 64 && value != 128 && value != 256) return TPROD_EINVAL;
+      if (value != 0 && value != 64 && value != 128) return TPROD_EINVAL;
       h->force_bn = (int)value;
       return TPROD_OK;
     default:

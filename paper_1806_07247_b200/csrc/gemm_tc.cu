@@ -136,33 +136,67 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---------------------------------------------------------------------------------- kernel
+// Persistent warp-specialised kernel, 1 CTA per SM, (2 + 8) warps:
+//   warp 0          TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1          MMA issuer (one lane) + TMEM allocator; accumulates K segment g of the
+//                   current tile into TMEM buffer g&1 (Cr | Ci, 2*BN columns each buffer)
+//   warps 2..9      epilogue: per segment, tcgen05.ld the buffer and add it into fp32 REGISTER
+//                   accumulators (round-to-nearest), then release the buffer; after the last
+//                   segment of a tile, scale by 2^-(e_i+e_j) and store.
+// Promotion: tensor-core accumulation rounds the fp32 accumulator toward zero at every MMA, so
+// the error of one TMEM accumulator grows linearly with the number of MMAs it absorbs (measured:
+// 7e-6 at K=1024, 3e-5 at K=4096 without promotion).  Restarting the TMEM accumulator every
+// SEG_KB K-blocks and summing the segments in fp32 registers keeps the error flat in K.
+constexpr int SEG_KB = 4;                  // K-blocks per promoted segment (K = 128)
+constexpr int EPI_WARPS = 8;
+constexpr int NTHREADS2 = 32 * (2 + EPI_WARPS);
+
 template <int BN>
 struct Cfg {
   static constexpr int A_PLANE = BK * BM * 2;                  // bytes: BK rows x 128 i x fp16
   static constexpr int B_PLANE = BN * BK * 2;                  // bytes: BN rows x BK l x fp16
   static constexpr int STAGE = NPLANES * (A_PLANE + B_PLANE);
-  static constexpr int STAGES = (BN == 256) ? 2 : (BN == 128 ? 3 : 4);
-  static constexpr int TMEM_COLS = 2 * BN;                     // Cr | Ci  (power of two)
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/ + 4 * BN;
+  static constexpr int STAGES = (BN == 128) ? 3 : 4;
+  static constexpr int BUF_COLS = 2 * BN;                      // Cr | Ci of one segment buffer
+  static constexpr int TMEM_COLS = 2 * BUF_COLS;               // double-buffered
+  static constexpr int COLS_PER_THREAD = BN / 2;               // each epilogue warp: half of N
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+struct TileInfo {
+  int f, m0, n0;
+};
+
+__device__ __forceinline__ TileInfo tile_of(int64_t t, int mt, int nt) {
+  // n fastest, then m, then f: concurrently running CTAs share the A_f / B_f panels in L2
+  TileInfo ti;
+  ti.n0 = (int)(t % nt);
+  int64_t r = t / nt;
+  ti.m0 = (int)(r % mt) * BM;
+  ti.f = (int)(r / mt);
+  return ti;
+}
+
 template <int BN>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int n3,
+                   float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int n3, int h,
                    const unsigned* __restrict__ maxA, const unsigned* __restrict__ maxB) {
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + G::STAGES * G::STAGE);
   uint64_t* empty = full + G::STAGES;
-  uint64_t* tmem_full = empty + G::STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
-  int* sExpB = (int*)(smem + G::STAGES * G::STAGE + 256);
+  uint64_t* seg_full = empty + G::STAGES;     // [2]
+  uint64_t* seg_empty = seg_full + 2;         // [2]
+  uint32_t* tmem_slot = (uint32_t*)(seg_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, f = blockIdx.z;
   const int nk = (n2 + BK - 1) / BK;
+  const int nseg = (nk + SEG_KB - 1) / SEG_KB;
+  const int mt = (n1 + BM - 1) / BM, nt = (n4 + BN - 1) / BN;
+  const int64_t ntiles = (int64_t)mt * nt * h;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -171,110 +205,151 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(seg_full + b, 1);
+      mbar_init(seg_empty + b, EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // whole warp allocates TMEM
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(G::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int x = threadIdx.x; x < BN; x += NTHREADS)
-    sExpB[x] = (n0 + x < n4) ? scale_exp(maxB[n0 + x], n3) : 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % G::STAGES;
-      const uint32_t ph = (kb / G::STAGES) & 1;
-      mbar_wait(empty + s, ph ^ 1);
-      uint8_t* st = smem + s * G::STAGE;
-      mbar_expect_tx(full + s, G::STAGE);
-      const int k0 = kb * BK;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- TMA producer
+      uint32_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileInfo ti = tile_of(t, mt, nt);
+        const int n0 = ti.n0 * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % G::STAGES;
+          const uint32_t ph = (it / G::STAGES) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          uint8_t* st = smem + s * G::STAGE;
+          mbar_expect_tx(full + s, G::STAGE);
+          const int k0 = kb * BK;
 #pragma unroll
-      for (int p = 0; p < NPLANES; ++p) {
-        uint8_t* a = st + p * G::A_PLANE;
-        tma_load_3d(a, &tmA, full + s, m0, k0, 4 * f + p);
-        tma_load_3d(a + BK * 128, &tmA, full + s, m0 + 64, k0, 4 * f + p);
-        uint8_t* b = st + NPLANES * G::A_PLANE + p * G::B_PLANE;
-        tma_load_3d(b, &tmB, full + s, k0, n0, 4 * f + p);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t ID_POS = idesc_f16(BM, BN, 0);
-    constexpr uint32_t ID_NEG = idesc_f16(BM, BN, 1);
-    const uint32_t tCr = tmem, tCi = tmem + BN;
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % G::STAGES;
-      const uint32_t ph = (kb / G::STAGES) & 1;
-      mbar_wait(full + s, ph);
-      tc_fence_after();
-      const uint32_t base = smem_u32(smem + s * G::STAGE);
-      const uint32_t bbase = base + NPLANES * G::A_PLANE;
-#pragma unroll
-      for (int ks = 0; ks < BK / 16; ++ks) {
-        // A (MN-major, SW128): LBO = distance between the two 64-row halves, SBO = 8 K-rows
-        uint64_t a[NPLANES], b[NPLANES];
-#pragma unroll
-        for (int p = 0; p < NPLANES; ++p) {
-          a[p] = sdesc(base + p * G::A_PLANE + ks * 2048, BK * 128, 1024, 2);
-          b[p] = sdesc(bbase + p * G::B_PLANE + ks * 32, 16, 512, 4);
+          for (int p = 0; p < NPLANES; ++p) {
+            uint8_t* a = st + p * G::A_PLANE;
+            tma_load_3d(a, &tmA, full + s, ti.m0, k0, 4 * ti.f + p);
+            tma_load_3d(a + BK * 128, &tmA, full + s, ti.m0 + 64, k0, 4 * ti.f + p);
+            uint8_t* b = st + NPLANES * G::A_PLANE + p * G::B_PLANE;
+            tma_load_3d(b, &tmB, full + s, k0, n0, 4 * ti.f + p);
+          }
         }
-        const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
-        // Cr = Ar.Br - Ai.Bi
-        mma_f16(tCr, a[PL_RE_HI], b[PL_RE_HI], ID_POS, acc0);
-        mma_f16(tCr, a[PL_RE_HI], b[PL_RE_LO], ID_POS, 1);
-        mma_f16(tCr, a[PL_RE_LO], b[PL_RE_HI], ID_POS, 1);
-        mma_f16(tCr, a[PL_IM_HI], b[PL_IM_HI], ID_NEG, 1);
-        mma_f16(tCr, a[PL_IM_HI], b[PL_IM_LO], ID_NEG, 1);
-        mma_f16(tCr, a[PL_IM_LO], b[PL_IM_HI], ID_NEG, 1);
-        // Ci = Ar.Bi + Ai.Br
-        mma_f16(tCi, a[PL_RE_HI], b[PL_IM_HI], ID_POS, acc0);
-        mma_f16(tCi, a[PL_RE_HI], b[PL_IM_LO], ID_POS, 1);
-        mma_f16(tCi, a[PL_RE_LO], b[PL_IM_HI], ID_POS, 1);
-        mma_f16(tCi, a[PL_IM_HI], b[PL_RE_HI], ID_POS, 1);
-        mma_f16(tCi, a[PL_IM_HI], b[PL_RE_LO], ID_POS, 1);
-        mma_f16(tCi, a[PL_IM_LO], b[PL_RE_HI], ID_POS, 1);
       }
-      mma_commit(empty + s);               // frees the smem slot when these MMAs have read it
     }
-    mma_commit(tmem_full);                 // accumulators complete
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t ID_POS = idesc_f16(BM, BN, 0);
+      constexpr uint32_t ID_NEG = idesc_f16(BM, BN, 1);
+      uint32_t it = 0, g = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int sg = 0; sg < nseg; ++sg, ++g) {
+          const uint32_t b = g & 1, use = g >> 1;
+          mbar_wait(seg_empty + b, (use & 1) ^ 1);     // epilogue drained this buffer
+          tc_fence_after();
+          const uint32_t tCr = tmem + b * G::BUF_COLS, tCi = tCr + BN;
+          const int kb_end = min(nk, (sg + 1) * SEG_KB);
+          for (int kb = sg * SEG_KB; kb < kb_end; ++kb, ++it) {
+            const int s = it % G::STAGES;
+            const uint32_t ph = (it / G::STAGES) & 1;
+            mbar_wait(full + s, ph);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * G::STAGE);
+            const uint32_t bbase = base + NPLANES * G::A_PLANE;
+#pragma unroll
+            for (int ks = 0; ks < BK / 16; ++ks) {
+              uint64_t a[NPLANES], bd[NPLANES];
+#pragma unroll
+              for (int p = 0; p < NPLANES; ++p) {
+                // A: MN-major, 128B swizzle; LBO = second 64-row half, SBO = 8 K-rows
+                a[p] = sdesc(base + p * G::A_PLANE + ks * 2048, BK * 128, 1024, 2);
+                // B: K-major, 64B swizzle; SBO = 8 rows of 64 B
+                bd[p] = sdesc(bbase + p * G::B_PLANE + ks * 32, 16, 512, 4);
+              }
+              const uint32_t acc0 = (kb > sg * SEG_KB || ks > 0) ? 1u : 0u;
+              // Cr = Ar.Br - Ai.Bi   (hi.hi + hi.lo + lo.hi each)
+              mma_f16(tCr, a[PL_RE_HI], bd[PL_RE_HI], ID_POS, acc0);
+              mma_f16(tCr, a[PL_RE_HI], bd[PL_RE_LO], ID_POS, 1);
+              mma_f16(tCr, a[PL_RE_LO], bd[PL_RE_HI], ID_POS, 1);
+              mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
+              mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
+              mma_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
+              // Ci = Ar.Bi + Ai.Br
+              mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
+              mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
+              mma_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
+              mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
+              mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
+              mma_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+            }
+            mma_commit(empty + s);       // smem slot free once these MMAs have read it
+          }
+          mma_commit(seg_full + b);      // segment accumulators complete
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue warps
+    const int q = warp & 3;                      // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;            // which half of the N columns
+    constexpr int CPT = G::COLS_PER_THREAD;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const int64_t plane = (int64_t)n4 * ldc;
+    uint32_t g = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TileInfo ti = tile_of(t, mt, nt);
+      const int n0 = ti.n0 * BN + half * CPT;
+      float accr[CPT], acci[CPT];
+#pragma unroll
+      for (int x = 0; x < CPT; ++x) accr[x] = acci[x] = 0.f;
+      for (int sg = 0; sg < nseg; ++sg, ++g) {
+        const uint32_t b = g & 1, use = g >> 1;
+        mbar_wait(seg_full + b, use & 1);
+        tc_fence_after();
+        const uint32_t base = tmem + lane_addr + b * G::BUF_COLS + half * CPT;
+#pragma unroll
+        for (int c = 0; c < CPT; c += 16) {
+          float v[16];
+          tmem_ld16(base + c, v);
+#pragma unroll
+          for (int x = 0; x < 16; ++x) accr[c + x] += v[x];
+          tmem_ld16(base + BN + c, v);
+#pragma unroll
+          for (int x = 0; x < 16; ++x) acci[c + x] += v[x];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(seg_empty + b)) : "memory");
+      }
+      const int i = ti.m0 + q * 32 + lane;
+      if (i < n1) {
+        const int eA = scale_exp(maxA[i], n3);
+        float* Cr = Cb + (int64_t)(2 * ti.f) * plane + i;
+        float* Ci = Cr + plane;
+#pragma unroll
+        for (int x = 0; x < CPT; ++x) {
+          const int j = n0 + x;
+          if (j < n4) {
+            const int e = eA + scale_exp(__ldg(maxB + j), n3);
+            Cr[(int64_t)j * ldc] = scalbnf(accr[x], -e);
+            Ci[(int64_t)j * ldc] = scalbnf(acci[x], -e);
+          }
+        }
+      }
+    }
   }
 
-  // ------------------------------------------------------------ epilogue (all 4 warps)
-  __syncwarp();
-  mbar_wait(tmem_full, 0);
-  tc_fence_after();
-  const int i = m0 + warp * 32 + lane;
-  const int eA = (i < n1) ? scale_exp(maxA[i], n3) : 0;
-  const int64_t plane = (int64_t)n4 * ldc;
-  float* Cr = Cb + (int64_t)(2 * f) * plane + i;
-  float* Ci = Cr + plane;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    if (n0 + c >= n4) break;
-    float vr[16], vi[16];
-    tmem_ld16(trow + c, vr);
-    tmem_ld16(trow + BN + c, vi);
-    if (i < n1) {
-#pragma unroll
-      for (int x = 0; x < 16; ++x) {
-        const int j = n0 + c + x;
-        if (j < n4) {
-          const int e = eA + sExpB[c + x];
-          Cr[(int64_t)j * ldc] = scalbnf(vr[x], -e);
-          Ci[(int64_t)j * ldc] = scalbnf(vi[x], -e);
-        }
-      }
-    }
-  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -319,7 +394,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 template <int BN>
 int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
               int64_t n2, int64_t n4, int64_t h, int64_t n3, const unsigned* maxA,
-              const unsigned* maxB, cudaStream_t s) {
+              const unsigned* maxB, int num_sms, cudaStream_t s) {
   using G = Cfg<BN>;
   CUtensorMap mb;
   if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN,
@@ -328,9 +403,10 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
   if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) !=
       cudaSuccess)
     return 4;
-  dim3 grid((unsigned)((n1 + BM - 1) / BM), (unsigned)((n4 + BN - 1) / BN), (unsigned)h);
-  gemm_tc_kernel<BN><<<grid, NTHREADS, G::SMEM, s>>>(ma, mb, Cb, ldc, (int)n1, (int)n2, (int)n4, (int)n3,
-                                                     maxA, maxB);
+  const int64_t ntiles = ((n1 + BM - 1) / BM) * ((n4 + BN - 1) / BN) * h;
+  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  gemm_tc_kernel<BN><<<grid, NTHREADS2, G::SMEM, s>>>(ma, mb, Cb, ldc, (int)n1, (int)n2, (int)n4,
+                                                      (int)n3, (int)h, maxA, maxB);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -348,18 +424,12 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
     return 4;
   int bn = force_bn;
   if (bn == 0) {
-    // largest N tile that still gives every SM at least one tile
+    // N = 128 unless that leaves SMs idle (small problems), then N = 64
     const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
-    bn = 64;
-    for (int cand : {256, 128}) {
-      if (mt * ((n4 + cand - 1) / cand) * h >= num_sms) { bn = cand; break; }
-    }
+    bn = (mt * ((n4 + 127) / 128) * h >= num_sms) ? 128 : 64;
   }
-  switch (bn) {
-    case 256: return tc::launch_bn<256>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
-    case 128: return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
-    default: return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, s);
-  }
+  if (bn == 128) return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, num_sms, s);
+  return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, num_sms, s);
 }
 
 }  // namespace tprod
