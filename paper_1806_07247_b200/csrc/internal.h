@@ -61,6 +61,13 @@ void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64
 void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
                     double* X, cudaStream_t s);
 
+// Register-resident dense transforms for n3 <= 64 (transforms_dense.cu); false = not handled.
+bool dense_supported(int64_t n3);
+bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
+                      const unsigned* maxbits, __half* out, int64_t ld, cudaStream_t s);
+bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
+                      int64_t Q, int64_t n3, float* X, cudaStream_t s);
+
 // Host-side exact twiddle table: (cos, sin)(2 pi m / n), m = 0..n-1, computed in fp64 with exact
 // quadrant reduction so that m = 0, n/4, n/2, 3n/4 give exactly 0 / +-1.
 void host_twiddles(int n, double* cs /* 2n: cos,sin interleaved */);

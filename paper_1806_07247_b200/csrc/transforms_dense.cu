@@ -1,0 +1,183 @@
+// Register-resident dense mode-3 DFT kernels for n3 <= 64 (the "small n3" path of the north star).
+//
+// K1 (forward, Alg. 1 step 1; Eq. (2)): one thread per tube x(0..N-1).
+// For a real tube the Hermitian half X_f = sum_k x_k w^{fk}, w = e^{-2 pi i/N}, f < H = N/2+1
+// (Eq. (8)), is evaluated with the conjugate-pair folding
+//     u_k = x_k + x_{N-k},  v_k = x_k - x_{N-k}   (k = 1..(N-1)/2)
+//     Re X_f = x_0 + sum_k u_k cos(2 pi f k/N) [+ (-1)^f x_{N/2}],   Im X_f = -sum_k v_k sin(2 pi f k/N)
+// which halves the multiply-adds.  N is a template parameter, so every twiddle index (f k mod N)
+// is a compile-time constant and the twiddles are read as constant-bank FFMA operands (no shared
+// or global loads in the inner loop).  The output is scaled by 2^e (exact) and split into the
+// fp16 hi/lo planes the tcgen05 GEMM consumes.
+//
+// K3 (inverse + fused conjugate fill, Alg. 1 step 2 second branch and step 3, L177-179):
+//     C_t = (1/N) [R_0 + sum_{f=1}^{H-1} w_f (R_f cos(2 pi f t/N) - I_f sin(2 pi f t/N))],
+//     w_f = 2 (f != N/2), 1 (f = N/2)
+// with the pair folding C_t = a_t + b_t, C_{N-t} = a_t - b_t.
+//
+// Memory: every load/store is warp-coalesced along the contiguous dimension p (Matlab layout).
+#include "internal.h"
+#include "common.cuh"
+
+#include <mutex>
+#include <vector>
+
+namespace tprod {
+
+constexpr int DENSE_MAX = 64;
+// c_tw[off(N) + m] = (cos, sin)(2 pi m / N), off(N) = N(N-1)/2
+__constant__ float2 c_tw[DENSE_MAX * (DENSE_MAX + 1) / 2];
+
+__host__ __device__ constexpr int tw_off(int N) { return N * (N - 1) / 2; }
+
+template <int N, int ROLE>
+__global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict__ X, int64_t P, int64_t Q,
+                                                        const unsigned* __restrict__ maxbits,
+                                                        __half* __restrict__ out, int64_t ld) {
+  constexpr int H = N / 2 + 1;
+  constexpr int K2 = (N - 1) / 2;
+  const int64_t pblocks = (P + 127) >> 7;
+  const int64_t q = blockIdx.x / pblocks;
+  const int64_t p = (blockIdx.x - q * pblocks) * 128 + threadIdx.x;
+  if (p >= P) return;
+  const int64_t PQ = P * Q;
+  const float* x = X + p + P * q;
+  float v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = __ldg(x + PQ * k);
+  float u[K2 + 1], w[K2 + 1];
+#pragma unroll
+  for (int k = 1; k <= K2; ++k) {
+    u[k] = v[k] + v[N - k];
+    w[k] = v[k] - v[N - k];
+  }
+  const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), N);
+  const int64_t plane = Q * ld;
+  __half* o = out + q * ld + p;
+#pragma unroll
+  for (int f = 0; f < H; ++f) {
+    float re = v[0], im = 0.f;
+#pragma unroll
+    for (int k = 1; k <= K2; ++k) {
+      const float2 t = c_tw[tw_off(N) + (f * k) % N];
+      re = fmaf(u[k], t.x, re);
+      im = fmaf(-w[k], t.y, im);
+    }
+    if (N % 2 == 0) re += (f & 1) ? -v[N / 2] : v[N / 2];
+    __half hi, lo;
+    split_f16(scalbnf(re, e), hi, lo);
+    o[(int64_t)(4 * f + PL_RE_HI) * plane] = hi;
+    o[(int64_t)(4 * f + PL_RE_LO) * plane] = lo;
+    split_f16(scalbnf(im, e), hi, lo);
+    o[(int64_t)(4 * f + PL_IM_HI) * plane] = hi;
+    o[(int64_t)(4 * f + PL_IM_LO) * plane] = lo;
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict__ Cre,
+                                                        const float* __restrict__ Cim, int64_t ld,
+                                                        int64_t fstride, int64_t P, int64_t Q,
+                                                        float* __restrict__ X) {
+  constexpr int H = N / 2 + 1;
+  const int64_t pblocks = (P + 127) >> 7;
+  const int64_t q = blockIdx.x / pblocks;
+  const int64_t p = (blockIdx.x - q * pblocks) * 128 + threadIdx.x;
+  if (p >= P) return;
+  const float* cr = Cre + q * ld + p;
+  const float* ci = Cim + q * ld + p;
+  float R[H], I[H];
+#pragma unroll
+  for (int f = 0; f < H; ++f) {
+    const float wf = (f == 0 || 2 * f == N) ? 1.f : 2.f;     // conjugate fill weight
+    R[f] = wf * __ldg(cr + fstride * f);
+    I[f] = (f == 0 || 2 * f == N) ? 0.f : wf * __ldg(ci + fstride * f);  // Im of DC/Nyquist dropped
+  }
+  const float inv_n = 1.f / (float)N;
+  const int64_t PQ = P * Q;
+  float* xo = X + p + P * q;
+#pragma unroll
+  for (int t = 0; t <= N / 2; ++t) {
+    float a = R[0], b = 0.f;
+#pragma unroll
+    for (int f = 1; f < H; ++f) {
+      const float2 tw = c_tw[tw_off(N) + (f * t) % N];
+      a = fmaf(R[f], tw.x, a);
+      b = fmaf(-I[f], tw.y, b);
+    }
+    xo[PQ * t] = (a + b) * inv_n;
+    if (t > 0 && 2 * t != N) xo[PQ * (N - t)] = (a - b) * inv_n;
+  }
+}
+
+// ------------------------------------------------------------------------------ dispatch tables
+using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t);
+using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, float*);
+
+template <int N>
+struct DenseTable {
+  static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
+    f0[N] = fwd_dense_kernel<N, 0>;
+    f1[N] = fwd_dense_kernel<N, 1>;
+    inv[N] = inv_dense_kernel<N>;
+    DenseTable<N - 1>::fill(f0, f1, inv);
+  }
+};
+template <>
+struct DenseTable<0> {
+  static void fill(FwdFn*, FwdFn*, InvFn*) {}
+};
+
+struct DenseFns {
+  FwdFn fwd0[DENSE_MAX + 1] = {};
+  FwdFn fwd1[DENSE_MAX + 1] = {};
+  InvFn inv[DENSE_MAX + 1] = {};
+  DenseFns() { DenseTable<DENSE_MAX>::fill(fwd0, fwd1, inv); }
+};
+
+static const DenseFns& dense_fns() {
+  static DenseFns t;
+  return t;
+}
+
+static bool ensure_dense_twiddles() {
+  static std::mutex mu;
+  static uint64_t done_mask = 0;  // per device ordinal (< 64)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && (done_mask >> dev) & 1) return true;
+  std::vector<float2> tab(DENSE_MAX * (DENSE_MAX + 1) / 2);
+  std::vector<double> cs;
+  for (int N = 1; N <= DENSE_MAX; ++N) {
+    cs.assign(2 * N, 0.0);
+    host_twiddles(N, cs.data());
+    for (int m = 0; m < N; ++m) tab[tw_off(N) + m] = make_float2((float)cs[2 * m], (float)cs[2 * m + 1]);
+  }
+  if (cudaMemcpyToSymbol(c_tw, tab.data(), sizeof(float2) * tab.size()) != cudaSuccess) return false;
+  if (dev < 64) done_mask |= 1ull << dev;
+  return true;
+}
+
+bool dense_supported(int64_t n3) { return n3 >= 1 && n3 <= DENSE_MAX; }
+
+bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
+                      const unsigned* maxbits, __half* out, int64_t ld, cudaStream_t s) {
+  if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
+  const DenseFns& t = dense_fns();
+  FwdFn fn = role == 0 ? t.fwd0[n3] : t.fwd1[n3];
+  int64_t blocks = (P + 127) / 128 * Q;
+  void* args[] = {(void*)&X, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld};
+  return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
+}
+
+bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
+                      int64_t Q, int64_t n3, float* X, cudaStream_t s) {
+  if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
+  InvFn fn = dense_fns().inv[n3];
+  int64_t blocks = (P + 127) / 128 * Q;
+  void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&X};
+  return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
+}
+
+}  // namespace tprod
