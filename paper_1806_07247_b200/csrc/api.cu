@@ -78,7 +78,7 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 // ---------------------------------------------------------------- workspace layout
 struct Layout32 {
   int64_t h, lda, ldb, ldc;
-  size_t off_maxA, off_maxB, off_Ab, off_Bb, off_Cb, total;
+  size_t off_maxA, off_maxB, off_uA, off_uB, off_Ab, off_Bb, off_Cb, total;
 };
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -91,7 +91,9 @@ Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
   size_t o = 0;
   L.off_maxA = o; o = align_up(o + 4 * (size_t)n1, 1024);
   L.off_maxB = o; o = align_up(o + 4 * (size_t)n4, 1024);
-  L.off_Ab = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
+  L.off_uA = o;   o = align_up(o + 4 * (size_t)n1, 1024);
+  L.off_uB = o;   o = align_up(o + 4 * (size_t)n4, 1024);
+  L.off_Ab = o;  o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
   L.off_Bb = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n4 * L.ldb), 1024);
   L.off_Cb = o;   o = align_up(o + 4 * (size_t)(L.h * 2 * n4 * L.ldc), 1024);
   L.total = o;
@@ -214,6 +216,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   char* ws = (char*)h->ws;
   unsigned* maxA = (unsigned*)(ws + L.off_maxA);
   unsigned* maxB = (unsigned*)(ws + L.off_maxB);
+  float* uA = (float*)(ws + L.off_uA);
+  float* uB = (float*)(ws + L.off_uB);
   __half* Ab = (__half*)(ws + L.off_Ab);
   __half* Bb = (__half*)(ws + L.off_Bb);
   float* Cb = (float*)(ws + L.off_Cb);
@@ -223,21 +227,22 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   auto mark = [&](int i) { if (h->timing) cudaEventRecord(h->ev[i], s); };
   h->timed_last = false;
   mark(0);
-  CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_Ab - L.off_maxA, s));
+  CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_uA - L.off_maxA, s));
   launch_absmax(A, n1, n2, n3, 0, maxA, s); ++launches;          // row scales of A (i)
   launch_absmax(B, n2, n4, n3, 1, maxB, s); ++launches;          // column scales of B (j)
   mark(1);
-  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, s); ++launches;   // Alg.1 step 1 (A)
-  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, s); ++launches;   // Alg.1 step 1 (B)
+  // B first: the tail of B just streamed by K0 is still resident in L2
+  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, s); ++launches;   // Alg.1 step 1 (B)
+  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, s); ++launches;   // Alg.1 step 1 (A)
   mark(2);
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
   if (tc) {
-    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3, maxA, maxB,
+    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB,
                               h->force_bn, h->num_sms, s);
     if (st) return st;
   } else {
-    launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3, maxA, maxB, s);
+    launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB, s);
   }
   ++launches;                                                     // Alg.1 step 2
   mark(3);
@@ -445,16 +450,18 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   cudaStream_t s = (cudaStream_t)stream;
   int64_t hh = h_slices(n3), ld = round_up(p, 8);
   int64_t nmax = role == 0 ? p : q;
-  size_t off_sp = align_up(4 * (size_t)nmax, 1024);
+  size_t off_u = align_up(4 * (size_t)nmax, 1024);
+  size_t off_sp = off_u + align_up(4 * (size_t)nmax, 1024);
   if ((st = ensure_ws(h, off_sp + 2 * (size_t)(hh * NPLANES * q * ld)))) return st;
   const float2* tw = nullptr;
   if ((st = get_tw32(h, (int)n3, &tw))) return st;
   unsigned* mx = (unsigned*)h->ws;
+  float* u = (float*)((char*)h->ws + off_u);
   __half* sp = (__half*)((char*)h->ws + off_sp);
   CK(cudaMemsetAsync(mx, 0, 4 * (size_t)nmax, s));
   launch_absmax(X, p, q, n3, role, mx, s);
-  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, s);
-  launch_decode_split(sp, ld, p, q, n3, role, mx, Xre, Xim, s);
+  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, u, s);
+  launch_decode_split(sp, ld, p, q, n3, role, u, Xre, Xim, s);
   h->last_launches = 3;
   return launch_status();
 }

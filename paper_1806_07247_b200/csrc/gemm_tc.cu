@@ -122,8 +122,8 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// 16 consecutive fp32 columns of this thread's TMEM lane; caller issues tmem_wait() before use.
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
       "%12, %13, %14, %15}, [%16];"
@@ -131,10 +131,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------- kernel
 // Persistent warp-specialised kernel, 1 CTA per SM, (2 + 8) warps:
@@ -181,8 +179,8 @@ __device__ __forceinline__ TileInfo tile_of(int64_t t, int mt, int nt) {
 template <int BN>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int n3, int h,
-                   const unsigned* __restrict__ maxA, const unsigned* __restrict__ maxB) {
+                   float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
+                   const float* __restrict__ uA, const float* __restrict__ uB) {
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -320,13 +318,15 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         const uint32_t base = tmem + lane_addr + b * G::BUF_COLS + half * CPT;
 #pragma unroll
         for (int c = 0; c < CPT; c += 16) {
-          float v[16];
-          tmem_ld16(base + c, v);
+          uint32_t vr[16], vi[16];
+          tmem_ld16_nowait(base + c, vr);
+          tmem_ld16_nowait(base + BN + c, vi);
+          tmem_wait();
 #pragma unroll
-          for (int x = 0; x < 16; ++x) accr[c + x] += v[x];
-          tmem_ld16(base + BN + c, v);
-#pragma unroll
-          for (int x = 0; x < 16; ++x) acci[c + x] += v[x];
+          for (int x = 0; x < 16; ++x) {
+            accr[c + x] += __uint_as_float(vr[x]);
+            acci[c + x] += __uint_as_float(vi[x]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -334,16 +334,15 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       }
       const int i = ti.m0 + q * 32 + lane;
       if (i < n1) {
-        const int eA = scale_exp(maxA[i], n3);
-        float* Cr = Cb + (int64_t)(2 * ti.f) * plane + i;
+        const float ua = __ldg(uA + i);
+        float* Cr = Cb + (int64_t)(2 * ti.f) * plane + (int64_t)n0 * ldc + i;
         float* Ci = Cr + plane;
 #pragma unroll
         for (int x = 0; x < CPT; ++x) {
-          const int j = n0 + x;
-          if (j < n4) {
-            const int e = eA + scale_exp(__ldg(maxB + j), n3);
-            Cr[(int64_t)j * ldc] = scalbnf(accr[x], -e);
-            Ci[(int64_t)j * ldc] = scalbnf(acci[x], -e);
+          if (n0 + x < n4) {
+            const float ub = __ldg(uB + n0 + x);      // exact 2^-(e_i + e_j) unscaling
+            Cr[(int64_t)x * ldc] = (accr[x] * ua) * ub;
+            Ci[(int64_t)x * ldc] = (acci[x] * ua) * ub;
           }
         }
       }
@@ -393,8 +392,8 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 
 template <int BN>
 int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
-              int64_t n2, int64_t n4, int64_t h, int64_t n3, const unsigned* maxA,
-              const unsigned* maxB, int num_sms, cudaStream_t s) {
+              int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int num_sms,
+              cudaStream_t s) {
   using G = Cfg<BN>;
   CUtensorMap mb;
   if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN,
@@ -406,7 +405,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
   const int64_t ntiles = ((n1 + BM - 1) / BM) * ((n4 + BN - 1) / BN) * h;
   const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
   gemm_tc_kernel<BN><<<grid, NTHREADS2, G::SMEM, s>>>(ma, mb, Cb, ldc, (int)n1, (int)n2, (int)n4,
-                                                      (int)n3, (int)h, maxA, maxB);
+                                                      (int)h, uA, uB);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -415,8 +414,8 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
 bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
 
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
-                         int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, int64_t n3,
-                         const unsigned* maxA, const unsigned* maxB, int force_bn, int num_sms,
+                         int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
+                         const float* uA, const float* uB, int force_bn, int num_sms,
                          cudaStream_t s) {
   CUtensorMap ma;
   if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
@@ -428,8 +427,8 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
     const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
     bn = (mt * ((n4 + 127) / 128) * h >= num_sms) ? 128 : 64;
   }
-  if (bn == 128) return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, num_sms, s);
-  return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, n3, maxA, maxB, num_sms, s);
+  if (bn == 128) return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+  return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
 }
 
 }  // namespace tprod

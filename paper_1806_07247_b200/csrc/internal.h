@@ -26,25 +26,28 @@ struct Twiddles64 { const double2* tw; int n3; };
 void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                    unsigned* maxbits, cudaStream_t s);
 
-// K1: forward DFT (Hermitian half), exact power-of-two scaling, fp16 hi/lo split.
+// K1: forward DFT (Hermitian half), exact power-of-two scaling 2^e, fp16 hi/lo split.  Also
+// writes unscale[p] (role 0) or unscale[q] (role 1) = 2^-e, the exact factor the GEMM epilogue
+// applies (one writer per index).
 void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
-                      cudaStream_t s);
+                      float* unscale, cudaStream_t s);
 // decode split planes back to fp32 planes [f][q][p] (stage test entry only)
 void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
-                         const unsigned* maxbits, float* re, float* im, cudaStream_t s);
+                         const float* unscale, float* re, float* im, cudaStream_t s);
 
-// K2 (reference SIMT engine): C-bar_f = A-bar_f B-bar_f on split operands, unscaled in epilogue.
+// K2 (reference SIMT engine): C-bar_f = A-bar_f B-bar_f on split operands; epilogue multiplies
+// by uA[i] * uB[j] (exact powers of two).
 void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                             float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                            int64_t n3, const unsigned* maxA, const unsigned* maxB, cudaStream_t s);
+                            const float* uA, const float* uB, cudaStream_t s);
 
 // K2 (tcgen05 engine).  Returns false if the shape/device is not supported by the kernel.
 bool gemm_tc_supported();
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         int64_t n3, const unsigned* maxA, const unsigned* maxB, int force_bn,
-                         int num_sms, cudaStream_t s);
+                         const float* uA, const float* uB, int force_bn, int num_sms,
+                         cudaStream_t s);
 
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
 // Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).
@@ -64,7 +67,8 @@ void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t 
 // Register-resident dense transforms for n3 <= 64 (transforms_dense.cu); false = not handled.
 bool dense_supported(int64_t n3);
 bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
-                      const unsigned* maxbits, __half* out, int64_t ld, cudaStream_t s);
+                      const unsigned* maxbits, __half* out, int64_t ld, float* unscale,
+                      cudaStream_t s);
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, float* X, cudaStream_t s);
 

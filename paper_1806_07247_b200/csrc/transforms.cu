@@ -102,11 +102,12 @@ void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role, u
 }
 
 // ------------------------------------------------------------------------------------ K1 (fp32)
+// Generic fallback (any n3; O(n3^2) per tube).  n3 <= 64 runs transforms_dense.cu instead.
 template <int ROLE>
 __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t Q, int n3, int h,
                                  const unsigned* __restrict__ maxbits,
                                  const float2* __restrict__ tw, __half* __restrict__ out,
-                                 int64_t ld) {
+                                 int64_t ld, float* __restrict__ unscale) {
   extern __shared__ float2 stw[];
   for (int m = threadIdx.x; m < n3; m += blockDim.x) stw[m] = tw[m];
   __syncthreads();
@@ -117,6 +118,8 @@ __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t
   const int64_t PQ = P * Q;
   const float* x = X + p + P * q;
   const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), n3);
+  const float sc = pow2f(e);
+  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = pow2f(-e);
   const int64_t plane = Q * ld;
   __half* o = out + q * ld + p;
   for (int f = 0; f < h; ++f) {
@@ -131,10 +134,10 @@ __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t
       if (m >= n3) m -= n3;
     }
     __half hi, lo;
-    split_f16(scalbnf(re, e), hi, lo);
+    split_f16(re * sc, hi, lo);
     o[(int64_t)(4 * f + PL_RE_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_RE_LO) * plane] = lo;
-    split_f16(scalbnf(im, e), hi, lo);
+    split_f16(im * sc, hi, lo);
     o[(int64_t)(4 * f + PL_IM_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_IM_LO) * plane] = lo;
   }
@@ -142,39 +145,39 @@ __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t
 
 void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
-                      cudaStream_t s) {
-  if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, s)) return;
+                      float* unscale, cudaStream_t s) {
+  if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   size_t smem = sizeof(float2) * (size_t)n3;
   int h = (int)h_slices(n3);
   if (role == 0)
-    fwd_split_kernel<0><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld);
+    fwd_split_kernel<0><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld, unscale);
   else
-    fwd_split_kernel<1><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld);
+    fwd_split_kernel<1><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld, unscale);
 }
 
 __global__ void decode_split_kernel(const __half* __restrict__ in, int64_t ld, int64_t P, int64_t Q,
-                                    int n3, int h, int role, const unsigned* __restrict__ maxbits,
+                                    int h, int role, const float* __restrict__ unscale,
                                     float* __restrict__ re, float* __restrict__ im) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)h * P * Q;
   if (idx >= total) return;
   int64_t p = idx % P, q = (idx / P) % Q, f = idx / (P * Q);
-  int e = scale_exp(maxbits[role == 0 ? p : q], n3);
+  const float u = unscale[role == 0 ? p : q];
   const int64_t plane = Q * ld;
   const __half* b = in + q * ld + p;
   float r = __half2float(b[(4 * f + PL_RE_HI) * plane]) + __half2float(b[(4 * f + PL_RE_LO) * plane]);
   float i = __half2float(b[(4 * f + PL_IM_HI) * plane]) + __half2float(b[(4 * f + PL_IM_LO) * plane]);
-  re[idx] = scalbnf(r, -e);
-  im[idx] = scalbnf(i, -e);
+  re[idx] = r * u;
+  im[idx] = i * u;
 }
 
 void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
-                         const unsigned* maxbits, float* re, float* im, cudaStream_t s) {
+                         const float* unscale, float* re, float* im, cudaStream_t s) {
   int64_t total = h_slices(n3) * P * Q;
   decode_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
-      in, ld, P, Q, (int)n3, (int)h_slices(n3), role, maxbits, re, im);
+      in, ld, P, Q, (int)h_slices(n3), role, unscale, re, im);
 }
 
 // ------------------------------------------------------------------------------------ K3 (fp32)

@@ -33,7 +33,8 @@ __host__ __device__ constexpr int tw_off(int N) { return N * (N - 1) / 2; }
 template <int N, int ROLE>
 __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict__ X, int64_t P, int64_t Q,
                                                         const unsigned* __restrict__ maxbits,
-                                                        __half* __restrict__ out, int64_t ld) {
+                                                        __half* __restrict__ out, int64_t ld,
+                                                        float* __restrict__ unscale) {
   constexpr int H = N / 2 + 1;
   constexpr int K2 = (N - 1) / 2;
   const int64_t pblocks = (P + 127) >> 7;
@@ -52,6 +53,8 @@ __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict_
     w[k] = v[k] - v[N - k];
   }
   const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), N);
+  const float sc = pow2f(e);
+  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = pow2f(-e);
   const int64_t plane = Q * ld;
   __half* o = out + q * ld + p;
 #pragma unroll
@@ -65,10 +68,10 @@ __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict_
     }
     if (N % 2 == 0) re += (f & 1) ? -v[N / 2] : v[N / 2];
     __half hi, lo;
-    split_f16(scalbnf(re, e), hi, lo);
+    split_f16(re * sc, hi, lo);
     o[(int64_t)(4 * f + PL_RE_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_RE_LO) * plane] = lo;
-    split_f16(scalbnf(im, e), hi, lo);
+    split_f16(im * sc, hi, lo);
     o[(int64_t)(4 * f + PL_IM_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_IM_LO) * plane] = lo;
   }
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
 }
 
 // ------------------------------------------------------------------------------ dispatch tables
-using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t);
+using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
 using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, float*);
 
 template <int N>
@@ -162,12 +165,13 @@ static bool ensure_dense_twiddles() {
 bool dense_supported(int64_t n3) { return n3 >= 1 && n3 <= DENSE_MAX; }
 
 bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
-                      const unsigned* maxbits, __half* out, int64_t ld, cudaStream_t s) {
+                      const unsigned* maxbits, __half* out, int64_t ld, float* unscale,
+                      cudaStream_t s) {
   if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
   const DenseFns& t = dense_fns();
   FwdFn fn = role == 0 ? t.fwd0[n3] : t.fwd1[n3];
   int64_t blocks = (P + 127) / 128 * Q;
-  void* args[] = {(void*)&X, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld};
+  void* args[] = {(void*)&X, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld, (void*)&unscale};
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
 }
 
