@@ -213,14 +213,12 @@ def main():
     B_host = torch.from_numpy(normal((n2, n4, n3), wl["seedB"] + 1000 * rank))
     B = B_host.to(dev)
     if world > 1:
-        uid = [tp.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        handle.set_world(rank, world, uid[0])
+        from paper_1806_07247_b200 import dist as tpdist
+        handle.set_world(rank, world, tpdist.exchange_uid(tp.nccl_unique_id))
         A = tp.matlab_empty(n1, n2, n3, torch.float32, dev)
         if rank == 0:
             A.copy_(A_host)
-        flat = A.permute(2, 1, 0)  # contiguous view of the same storage
-        handle.bcast_(flat, root=0)
+        tpdist.replicate(A, root=0, handle=handle)       # one ncclBroadcast, setup only
         torch.cuda.synchronize()
         if rank != 0:
             A_host = A.cpu()

@@ -228,8 +228,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   h->timed_last = false;
   mark(0);
   CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_uA - L.off_maxA, s));
-  launch_absmax(A, n1, n2, n3, 0, maxA, s); ++launches;          // row scales of A (i)
-  launch_absmax(B, n2, n4, n3, 1, maxB, s); ++launches;          // column scales of B (j)
+  launch_absmax2(A, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
+  launches += (n1 % 4 == 0 && n2 % 4 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 2;
   mark(1);
   // B first: the tail of B just streamed by K0 is still resident in L2
   launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, s); ++launches;   // Alg.1 step 1 (B)

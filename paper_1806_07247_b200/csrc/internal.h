@@ -25,6 +25,9 @@ struct Twiddles64 { const double2* tw; int n3; };
 // role 0: max over (q,k) for every p;  role 1: max over (p,k) for every q.
 void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                    unsigned* maxbits, cudaStream_t s);
+// Both operands in one vectorised launch (falls back to two launch_absmax calls if unaligned).
+void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+                    unsigned* maxA, unsigned* maxB, int num_sms, cudaStream_t s);
 
 // K1: forward DFT (Hermitian half), exact power-of-two scaling 2^e, fp16 hi/lo split.  Also
 // writes unscale[p] (role 0) or unscale[q] (role 1) = 2^-e, the exact factor the GEMM epilogue

@@ -81,6 +81,95 @@ __global__ void absmax_q_kernel(const float* __restrict__ X, int64_t P, int64_t 
   }
 }
 
+// Fused, vectorised K0 for both operands in one launch (requires 16-byte aligned bases and
+// n1 % 4 == 0, n2 % 4 == 0).  Blocks [0, nbA) reduce A's rows: a 256-float strip of p times a
+// strided set of columns (q,k), float4 loads, smem reduction over the 4 column lanes, one atomic
+// per p per block.  Blocks [nbA, nbA+nbB) reduce B's columns: one warp per contiguous run
+// B(:, j, k) (float4 loads), one atomic per run.
+__global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ A, int64_t n1,
+                                                      int64_t colsA, int gyA, int gxA,
+                                                      const float* __restrict__ B, int64_t n2,
+                                                      int64_t n4, int64_t n3,
+                                                      unsigned* __restrict__ maxA,
+                                                      unsigned* __restrict__ maxB) {
+  const int nbA = gxA * gyA;
+  if ((int)blockIdx.x < nbA) {
+    __shared__ float red[4][257];
+    const int bx = blockIdx.x % gxA, by = blockIdx.x / gxA;
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    const int64_t p = (int64_t)bx * 256 + 4 * tx;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p < n1) {
+      const float4* base = reinterpret_cast<const float4*>(A + p);
+      const int64_t step = (int64_t)gyA * 4;
+      int64_t c = (int64_t)by * 4 + ty;
+#pragma unroll 4
+      for (; c < colsA; c += step) {
+        float4 v = __ldg(base + (c * n1 >> 2));
+        m.x = fmaxf(m.x, fabsf(v.x));
+        m.y = fmaxf(m.y, fabsf(v.y));
+        m.z = fmaxf(m.z, fabsf(v.z));
+        m.w = fmaxf(m.w, fabsf(v.w));
+      }
+    }
+    red[ty][4 * tx] = m.x;
+    red[ty][4 * tx + 1] = m.y;
+    red[ty][4 * tx + 2] = m.z;
+    red[ty][4 * tx + 3] = m.w;
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int64_t pt = (int64_t)bx * 256 + t;
+    if (pt < n1) {
+      float r = fmaxf(fmaxf(red[0][t], red[1][t]), fmaxf(red[2][t], red[3][t]));
+      atomicMax(maxA + pt, __float_as_uint(r));
+    }
+  } else {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)(blockIdx.x - nbA) * 256 + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)(gridDim.x - nbA) * 256) >> 5;
+    const int64_t runs = n4 * n3;
+    for (int64_t r = warp; r < runs; r += nwarps) {
+      const int64_t j = r % n4;
+      const float4* x = reinterpret_cast<const float4*>(B + n2 * r);   // run (j,k): offset n2*(j + n4 k)
+      float m = 0.f;
+#pragma unroll 4
+      for (int64_t l4 = lane; l4 < (n2 >> 2); l4 += 32) {
+        float4 v = __ldg(x + l4);
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) atomicMax(maxB + j, __float_as_uint(m));
+    }
+  }
+}
+
+void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int64_t n3, int64_t n4,
+                    unsigned* maxA, unsigned* maxB, int num_sms, cudaStream_t s) {
+  const bool vec = n1 % 4 == 0 && n2 % 4 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0;
+  if (!vec) {
+    launch_absmax(A, n1, n2, n3, 0, maxA, s);
+    launch_absmax(B, n2, n4, n3, 1, maxB, s);
+    return;
+  }
+  // split ~8 CTAs per SM between the two tensors in proportion to their sizes
+  const double szA = (double)n1 * n2 * n3, szB = (double)n2 * n4 * n3;
+  const int64_t total = (int64_t)num_sms * 8;
+  int64_t nbA_target = (int64_t)(total * szA / (szA + szB));
+  if (nbA_target < 1) nbA_target = 1;
+  const int64_t gxA = (n1 + 255) / 256;
+  const int64_t colsA = n2 * n3;
+  int64_t gyA = (nbA_target + gxA - 1) / gxA;
+  const int64_t maxgy = (colsA + 3) / 4;
+  if (gyA > maxgy) gyA = maxgy;
+  if (gyA < 1) gyA = 1;
+  int64_t nbB = total - gxA * gyA;
+  const int64_t runsB = n4 * n3;
+  if (nbB > (runsB + 7) / 8) nbB = (runsB + 7) / 8;
+  if (nbB < 1) nbB = 1;
+  absmax2_kernel<<<(unsigned)(gxA * gyA + nbB), 256, 0, s>>>(A, n1, colsA, (int)gyA, (int)gxA, B, n2,
+                                                             n4, n3, maxA, maxB);
+}
+
 void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role, unsigned* maxbits,
                    cudaStream_t s) {
   if (role == 0) {

@@ -113,6 +113,122 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
   }
 }
 
+// Two adjacent tubes (p, p+1) per thread for N <= PAIR_MAX: float2 loads, half2 stores and paired
+// fp16 conversions halve the per-tube instruction count of the memory-bound transforms.
+// Requires P even (then every column start and every plane row stays 8-/4-byte aligned).
+constexpr int PAIR_MAX = 32;
+
+template <int N, int ROLE>
+__global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict__ X, int64_t P,
+                                                         int64_t Q, const unsigned* __restrict__ maxbits,
+                                                         __half* __restrict__ out, int64_t ld,
+                                                         float* __restrict__ unscale) {
+  constexpr int H = N / 2 + 1;
+  constexpr int K2 = (N - 1) / 2;
+  const int64_t pblocks = (P + 255) >> 8;
+  const int64_t q = blockIdx.x / pblocks;
+  const int64_t p = ((blockIdx.x - q * pblocks) * 128 + threadIdx.x) * 2;
+  if (p >= P) return;
+  const int64_t PQh = (P * Q) >> 1;
+  const float2* x = reinterpret_cast<const float2*>(X + p + P * q);
+  float2 v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = __ldg(x + PQh * k);
+  float2 u[K2 + 1], w[K2 + 1];
+#pragma unroll
+  for (int k = 1; k <= K2; ++k) {
+    u[k] = make_float2(v[k].x + v[N - k].x, v[k].y + v[N - k].y);
+    w[k] = make_float2(v[k].x - v[N - k].x, v[k].y - v[N - k].y);
+  }
+  int e0, e1;
+  if (ROLE == 0) {
+    e0 = scale_exp(__ldg(maxbits + p), N);
+    e1 = scale_exp(__ldg(maxbits + p + 1), N);
+    if (q == 0) {
+      unscale[p] = pow2f(-e0);
+      unscale[p + 1] = pow2f(-e1);
+    }
+  } else {
+    e0 = e1 = scale_exp(__ldg(maxbits + q), N);
+    if (p == 0) unscale[q] = pow2f(-e0);
+  }
+  const float s0 = pow2f(e0), s1 = pow2f(e1);
+  const int64_t plane = Q * ld;
+  __half* o = out + q * ld + p;
+#pragma unroll
+  for (int f = 0; f < H; ++f) {
+    float2 re = v[0], im = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 1; k <= K2; ++k) {
+      const float2 t = c_tw[tw_off(N) + (f * k) % N];
+      re.x = fmaf(u[k].x, t.x, re.x);
+      re.y = fmaf(u[k].y, t.x, re.y);
+      im.x = fmaf(-w[k].x, t.y, im.x);
+      im.y = fmaf(-w[k].y, t.y, im.y);
+    }
+    if (N % 2 == 0) {
+      const float sg = (f & 1) ? -1.f : 1.f;
+      re.x = fmaf(sg, v[N / 2].x, re.x);
+      re.y = fmaf(sg, v[N / 2].y, re.y);
+    }
+    const float2 rs = make_float2(re.x * s0, re.y * s1), is = make_float2(im.x * s0, im.y * s1);
+    const __half2 rh = __float22half2_rn(rs), ih = __float22half2_rn(is);
+    const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
+    const __half2 rl = __float22half2_rn(make_float2(rs.x - rhf.x, rs.y - rhf.y));
+    const __half2 il = __float22half2_rn(make_float2(is.x - ihf.x, is.y - ihf.y));
+    *reinterpret_cast<__half2*>(o + (int64_t)(4 * f + PL_RE_HI) * plane) = rh;
+    *reinterpret_cast<__half2*>(o + (int64_t)(4 * f + PL_RE_LO) * plane) = rl;
+    *reinterpret_cast<__half2*>(o + (int64_t)(4 * f + PL_IM_HI) * plane) = ih;
+    *reinterpret_cast<__half2*>(o + (int64_t)(4 * f + PL_IM_LO) * plane) = il;
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict__ Cre,
+                                                         const float* __restrict__ Cim, int64_t ld,
+                                                         int64_t fstride, int64_t P, int64_t Q,
+                                                         float* __restrict__ X) {
+  constexpr int H = N / 2 + 1;
+  const int64_t pblocks = (P + 255) >> 8;
+  const int64_t q = blockIdx.x / pblocks;
+  const int64_t p = ((blockIdx.x - q * pblocks) * 128 + threadIdx.x) * 2;
+  if (p >= P) return;
+  const float2* cr = reinterpret_cast<const float2*>(Cre + q * ld + p);
+  const float2* ci = reinterpret_cast<const float2*>(Cim + q * ld + p);
+  const int64_t fs = fstride >> 1;
+  float2 R[H], I[H];
+#pragma unroll
+  for (int f = 0; f < H; ++f) {
+    const bool self = (f == 0 || 2 * f == N);
+    const float wf = self ? 1.f : 2.f;     // conjugate fill weight
+    const float2 r = __ldg(cr + fs * f);
+    R[f] = make_float2(wf * r.x, wf * r.y);
+    if (self) {
+      I[f] = make_float2(0.f, 0.f);         // Im of DC/Nyquist dropped (C2R)
+    } else {
+      const float2 i = __ldg(ci + fs * f);
+      I[f] = make_float2(wf * i.x, wf * i.y);
+    }
+  }
+  const float inv_n = 1.f / (float)N;
+  const int64_t PQh = (P * Q) >> 1;
+  float2* xo = reinterpret_cast<float2*>(X + p + P * q);
+#pragma unroll
+  for (int t = 0; t <= N / 2; ++t) {
+    float2 a = R[0], b = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int f = 1; f < H; ++f) {
+      const float2 tw = c_tw[tw_off(N) + (f * t) % N];
+      a.x = fmaf(R[f].x, tw.x, a.x);
+      a.y = fmaf(R[f].y, tw.x, a.y);
+      b.x = fmaf(-I[f].x, tw.y, b.x);
+      b.y = fmaf(-I[f].y, tw.y, b.y);
+    }
+    xo[PQh * t] = make_float2((a.x + b.x) * inv_n, (a.y + b.y) * inv_n);
+    if (t > 0 && 2 * t != N) xo[PQh * (N - t)] = make_float2((a.x - b.x) * inv_n, (a.y - b.y) * inv_n);
+  }
+}
+
 // ------------------------------------------------------------------------------ dispatch tables
 using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
 using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, float*);
@@ -131,11 +247,31 @@ struct DenseTable<0> {
   static void fill(FwdFn*, FwdFn*, InvFn*) {}
 };
 
+template <int N>
+struct PairTable {
+  static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
+    f0[N] = fwd_dense2_kernel<N, 0>;
+    f1[N] = fwd_dense2_kernel<N, 1>;
+    inv[N] = inv_dense2_kernel<N>;
+    PairTable<N - 1>::fill(f0, f1, inv);
+  }
+};
+template <>
+struct PairTable<0> {
+  static void fill(FwdFn*, FwdFn*, InvFn*) {}
+};
+
 struct DenseFns {
   FwdFn fwd0[DENSE_MAX + 1] = {};
   FwdFn fwd1[DENSE_MAX + 1] = {};
   InvFn inv[DENSE_MAX + 1] = {};
-  DenseFns() { DenseTable<DENSE_MAX>::fill(fwd0, fwd1, inv); }
+  FwdFn fwd0p[PAIR_MAX + 1] = {};
+  FwdFn fwd1p[PAIR_MAX + 1] = {};
+  InvFn invp[PAIR_MAX + 1] = {};
+  DenseFns() {
+    DenseTable<DENSE_MAX>::fill(fwd0, fwd1, inv);
+    PairTable<PAIR_MAX>::fill(fwd0p, fwd1p, invp);
+  }
 };
 
 static const DenseFns& dense_fns() {
@@ -169,8 +305,9 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
                       cudaStream_t s) {
   if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
   const DenseFns& t = dense_fns();
-  FwdFn fn = role == 0 ? t.fwd0[n3] : t.fwd1[n3];
-  int64_t blocks = (P + 127) / 128 * Q;
+  const bool pair = n3 <= PAIR_MAX && P % 2 == 0 && ((uintptr_t)X & 7) == 0;
+  FwdFn fn = pair ? (role == 0 ? t.fwd0p[n3] : t.fwd1p[n3]) : (role == 0 ? t.fwd0[n3] : t.fwd1[n3]);
+  int64_t blocks = (P + (pair ? 255 : 127)) / (pair ? 256 : 128) * Q;
   void* args[] = {(void*)&X, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld, (void*)&unscale};
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
 }
@@ -178,8 +315,10 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, float* X, cudaStream_t s) {
   if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
-  InvFn fn = dense_fns().inv[n3];
-  int64_t blocks = (P + 127) / 128 * Q;
+  const bool pair = n3 <= PAIR_MAX && P % 2 == 0 && ld % 2 == 0 && fstride % 2 == 0 &&
+                    ((uintptr_t)X & 7) == 0 && ((uintptr_t)Cre & 7) == 0 && ((uintptr_t)Cim & 7) == 0;
+  InvFn fn = pair ? dense_fns().invp[n3] : dense_fns().inv[n3];
+  int64_t blocks = (P + (pair ? 255 : 127)) / (pair ? 256 : 128) * Q;
   void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&X};
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
 }
