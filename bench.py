@@ -178,6 +178,8 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="0 tcgen05 (default), 1 SIMT reference")
+    ap.add_argument("--bn", type=int, default=0, help="force the GEMM N tile (0 = library heuristic)")
+    ap.add_argument("--cn", type=int, default=0, help="force GEMM cluster width 1/2 (0 = heuristic)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -207,6 +209,10 @@ def main():
     n1, n2, n3, n4 = wl["n1"], wl["n2"], wl["n3"], wl["n4"]
     handle = tp.Handle(local)
     handle.set_option(tp._lib.TPROD_OPT_ENGINE, args.engine)
+    if args.bn:
+        handle.set_option(tp._lib.TPROD_OPT_GEMM_BN, args.bn)
+    if args.cn:
+        handle.set_option(tp._lib.TPROD_OPT_GEMM_CLUSTER, args.cn)
 
     # ---- inputs: A on rank 0 then one NCCL broadcast (setup, untimed); B = this rank's shard
     A_host = torch.from_numpy(normal((n1, n2, n3), wl["seedA"])) if rank == 0 else None
@@ -227,9 +233,17 @@ def main():
     C = tp.matlab_empty(n1, n4, n3, torch.float32, dev)
     stream = torch.cuda.current_stream(dev)
 
-    # L2 flush buffer (> 126 MB L2), written between timed steps outside the events
+    # L2 flush between timed steps, outside the events: write a buffer of 2x L2 (evicts every
+    # line of the previous step), then read a second one so the write-backs of those dirty lines
+    # also complete before the next step starts (cold, clean L2).
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev)
+    flush_rd = torch.ones_like(flush)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def l2_flush():
+        flush.zero_()
+        torch.sum(flush_rd, dim=(0,), out=flush_sink)
 
     def step():
         tp.tprod_f32(A, B, out=C, handle=handle, stream=stream)
@@ -249,7 +263,7 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            flush.zero_()
+            l2_flush()
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -314,7 +328,7 @@ def main():
             "config": {"workload": args.workload, "n1": n1, "n2": n2, "n3": n3, "n4_per_gpu": n4,
                        "h": h_slices(n3), "global_n4": n4 * world,
                        "parallelism": f"lateral-slice shards x{world}, A broadcast once (NCCL)",
-                       "l2": "flushed between timed steps (memset 2x L2, outside the step events)",
+                       "l2": "flushed between timed steps (write 2x L2 then read 2x L2, outside the step events)",
                        "engine": "tcgen05" if args.engine == 0 else "simt-reference"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_alg,
                          "unit": "TFLOP/s", "frac": achieved / peak_alg, "traffic": None,

@@ -128,7 +128,10 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
 /* Options (tests / benchmarking).  TPROD_OPT_ENGINE: 0 = auto (tcgen05), 1 = SIMT reference
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
-enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3 };
+enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4 };
+/* TPROD_OPT_GEMM_CLUSTER: 0 = auto, 1 = independent CTAs, 2 = 2-CTA clusters along N sharing the
+ * A tile by TMA multicast.  None of the options changes the arithmetic (results are bitwise
+ * identical for every option value except TPROD_OPT_ENGINE). */
 int tprod_set_option(tprod_handle h, int option, int64_t value);
 
 /* With TPROD_OPT_TIMING = 1, tprod_f32 records CUDA events on its stream between the stages of

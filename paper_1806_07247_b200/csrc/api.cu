@@ -33,6 +33,7 @@ struct tprod_ctx {
   int64_t last_launches = 0;
   int engine = 0;
   int force_bn = 0;
+  int force_cn = 0;
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
   bool timing = false;
@@ -239,7 +240,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   bool tc = h->engine == 0 && gemm_tc_supported();
   if (tc) {
     st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB,
-                              h->force_bn, h->num_sms, s);
+                              h->force_bn, h->force_cn, h->num_sms, s);
     if (st) return st;
   } else {
     launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB, s);
@@ -494,6 +495,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
         for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&h->ev[i]));
       }
       h->timing = value != 0;
+      return TPROD_OK;
+    case TPROD_OPT_GEMM_CLUSTER:
+      if (value != 0 && value != 1 && value != 2) return TPROD_EINVAL;
+      h->force_cn = (int)value;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:
       if (value != 0 && value != 64 && value != 128) return TPROD_EINVAL;

@@ -25,13 +25,18 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tprod {
 
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;            // K elements per stage (64 B rows for the K-major B operand)
+constexpr int BK = 32;            // K elements per stage (two MMA K-steps; 64 B rows of B)
+constexpr int B_ROW = BK * 2;     // bytes per K-major B row in smem
+constexpr uint32_t B_SWZ = (BK == 32) ? 4u : 6u;   // smem-descriptor swizzle code: 64B / 32B
+constexpr CUtensorMapSwizzle B_TMA_SWZ = (BK == 32) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
 constexpr int NTHREADS = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,6 +74,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// Same box, written to the same smem offset of every CTA in `mask` (and completing the mbarrier
+// at the same offset in each of them).
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                               int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -115,6 +141,16 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Arrive (on completion of this thread's prior MMAs) on the mbarrier at the same offset in every
+// CTA of `mask`.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+      "%1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -146,7 +182,7 @@ __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.syn
 // the error of one TMEM accumulator grows linearly with the number of MMAs it absorbs (measured:
 // 7e-6 at K=1024, 3e-5 at K=4096 without promotion).  Restarting the TMEM accumulator every
 // SEG_KB K-blocks and summing the segments in fp32 registers keeps the error flat in K.
-constexpr int SEG_KB = 4;                  // K-blocks per promoted segment (K = 128)
+constexpr int SEG_KB = 128 / BK;           // K-blocks per promoted segment (K = 128)
 constexpr int EPI_WARPS = 8;
 constexpr int NTHREADS2 = 32 * (2 + EPI_WARPS);
 
@@ -155,7 +191,8 @@ struct Cfg {
   static constexpr int A_PLANE = BK * BM * 2;                  // bytes: BK rows x 128 i x fp16
   static constexpr int B_PLANE = BN * BK * 2;                  // bytes: BN rows x BK l x fp16
   static constexpr int STAGE = NPLANES * (A_PLANE + B_PLANE);
-  static constexpr int STAGES = (BN == 128) ? 3 : 4;
+  static constexpr int STAGES_FIT = (227 * 1024 - 2048) / STAGE;          // deepest ring that fits
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int BUF_COLS = 2 * BN;                      // Cr | Ci of one segment buffer
   static constexpr int TMEM_COLS = 2 * BUF_COLS;               // double-buffered
   static constexpr int COLS_PER_THREAD = BN / 2;               // each epilogue warp: half of N
@@ -163,25 +200,34 @@ struct Cfg {
 };
 
 struct TileInfo {
-  int f, m0, n0;
+  int f, m0, n0;   // n0: index of this CTA's N tile (in tiles)
 };
 
-__device__ __forceinline__ TileInfo tile_of(int64_t t, int mt, int nt) {
-  // n fastest, then m, then f: concurrently running CTAs share the A_f / B_f panels in L2
+// Cluster tile ct -> (f, m, n-group); CTA `rank` of a CN-wide cluster takes N tile n-group*CN+rank.
+// n fastest, then m, then f: concurrently running clusters share the A_f / B_f panels in L2.
+__device__ __forceinline__ TileInfo tile_of(int64_t ct, int mt, int ntg, int CN, int rank) {
   TileInfo ti;
-  ti.n0 = (int)(t % nt);
-  int64_t r = t / nt;
+  ti.n0 = (int)(ct % ntg) * CN + rank;
+  int64_t r = ct / ntg;
   ti.m0 = (int)(r % mt) * BM;
   ti.f = (int)(r / mt);
   return ti;
 }
 
-template <int BN>
+// CN = 1: independent CTAs.  CN = 2: a cluster of two CTAs along N computes two adjacent N
+// tiles of the same (f, m); both need the same A tile, so each CTA TMA-loads one 64-row half of A
+// and multicasts it to both (per-SM L2->smem traffic 64 KB -> 48 KB per K block), and each MMA
+// commit arrives on the `empty` barriers of both CTAs (a slot is refilled only after both
+// consumers are done with it).
+template <int BN, int CN>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
-                   const float* __restrict__ uA, const float* __restrict__ uB) {
+                   const float* __restrict__ uA, const float* __restrict__ uB,
+                   long long* __restrict__ dbg) {
   using G = Cfg<BN>;
+  const long long t_start = clock64();
+  long long w0 = 0, w1 = 0;   // per-role wait cycles (diagnostics, dbg != nullptr)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + G::STAGES * G::STAGE);
@@ -194,14 +240,17 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   const int nk = (n2 + BK - 1) / BK;
   const int nseg = (nk + SEG_KB - 1) / SEG_KB;
   const int mt = (n1 + BM - 1) / BM, nt = (n4 + BN - 1) / BN;
-  const int64_t ntiles = (int64_t)mt * nt * h;
+  const int ntg = (nt + CN - 1) / CN;
+  const int64_t nctiles = (int64_t)mt * ntg * h;
+  const int rank = CN > 1 ? (int)cluster_ctarank() : 0;
+  const int64_t cid = blockIdx.x / CN, ncl = gridDim.x / CN;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < G::STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CN);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(seg_full + b, 1);
@@ -217,6 +266,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CN > 1) cluster_sync();      // peers' barriers are initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -224,21 +274,26 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     if (lane == 0) {
       // ---------------------------------------------------------- TMA producer
       uint32_t it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const TileInfo ti = tile_of(t, mt, nt);
+      for (int64_t t = cid; t < nctiles; t += ncl) {
+        const TileInfo ti = tile_of(t, mt, ntg, CN, rank);
         const int n0 = ti.n0 * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % G::STAGES;
           const uint32_t ph = (it / G::STAGES) & 1;
-          mbar_wait(empty + s, ph ^ 1);
+          { long long t0 = dbg ? clock64() : 0; mbar_wait(empty + s, ph ^ 1); if (dbg) w0 += clock64() - t0; }
           uint8_t* st = smem + s * G::STAGE;
           mbar_expect_tx(full + s, G::STAGE);
           const int k0 = kb * BK;
 #pragma unroll
           for (int p = 0; p < NPLANES; ++p) {
             uint8_t* a = st + p * G::A_PLANE;
-            tma_load_3d(a, &tmA, full + s, ti.m0, k0, 4 * ti.f + p);
-            tma_load_3d(a + BK * 128, &tmA, full + s, ti.m0 + 64, k0, 4 * ti.f + p);
+            if (CN == 1) {
+              tma_load_3d(a, &tmA, full + s, ti.m0, k0, 4 * ti.f + p);
+              tma_load_3d(a + BK * 128, &tmA, full + s, ti.m0 + 64, k0, 4 * ti.f + p);
+            } else {
+              tma_load_3d_mc(a + rank * BK * 128, &tmA, full + s, ti.m0 + 64 * rank, k0, 4 * ti.f + p,
+                             (uint16_t)((1u << CN) - 1));
+            }
             uint8_t* b = st + NPLANES * G::A_PLANE + p * G::B_PLANE;
             tma_load_3d(b, &tmB, full + s, k0, n0, 4 * ti.f + p);
           }
@@ -251,17 +306,17 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       constexpr uint32_t ID_POS = idesc_f16(BM, BN, 0);
       constexpr uint32_t ID_NEG = idesc_f16(BM, BN, 1);
       uint32_t it = 0, g = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int64_t t = cid; t < nctiles; t += ncl) {
         for (int sg = 0; sg < nseg; ++sg, ++g) {
           const uint32_t b = g & 1, use = g >> 1;
-          mbar_wait(seg_empty + b, (use & 1) ^ 1);     // epilogue drained this buffer
+          { long long t0 = dbg ? clock64() : 0; mbar_wait(seg_empty + b, (use & 1) ^ 1); if (dbg) w0 += clock64() - t0; }  // epilogue drained this buffer
           tc_fence_after();
           const uint32_t tCr = tmem + b * G::BUF_COLS, tCi = tCr + BN;
           const int kb_end = min(nk, (sg + 1) * SEG_KB);
           for (int kb = sg * SEG_KB; kb < kb_end; ++kb, ++it) {
             const int s = it % G::STAGES;
             const uint32_t ph = (it / G::STAGES) & 1;
-            mbar_wait(full + s, ph);
+            { long long t0 = dbg ? clock64() : 0; mbar_wait(full + s, ph); if (dbg) w1 += clock64() - t0; }
             tc_fence_after();
             const uint32_t base = smem_u32(smem + s * G::STAGE);
             const uint32_t bbase = base + NPLANES * G::A_PLANE;
@@ -272,8 +327,8 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
               for (int p = 0; p < NPLANES; ++p) {
                 // A: MN-major, 128B swizzle; LBO = second 64-row half, SBO = 8 K-rows
                 a[p] = sdesc(base + p * G::A_PLANE + ks * 2048, BK * 128, 1024, 2);
-                // B: K-major, 64B swizzle; SBO = 8 rows of 64 B
-                bd[p] = sdesc(bbase + p * G::B_PLANE + ks * 32, 16, 512, 4);
+                // B: K-major, BK*2-byte rows swizzled; SBO = 8 rows
+                bd[p] = sdesc(bbase + p * G::B_PLANE + ks * 32, 16, 8 * B_ROW, B_SWZ);
               }
               const uint32_t acc0 = (kb > sg * SEG_KB || ks > 0) ? 1u : 0u;
               // Cr = Ar.Br - Ai.Bi   (hi.hi + hi.lo + lo.hi each)
@@ -291,7 +346,9 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
               mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
               mma_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
             }
-            mma_commit(empty + s);       // smem slot free once these MMAs have read it
+            // smem slot free once these MMAs have read it (in every CTA that wrote into it)
+            if (CN == 1) mma_commit(empty + s);
+            else mma_commit_mc(empty + s, (uint16_t)((1u << CN) - 1));
           }
           mma_commit(seg_full + b);      // segment accumulators complete
         }
@@ -305,15 +362,15 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const int64_t plane = (int64_t)n4 * ldc;
     uint32_t g = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const TileInfo ti = tile_of(t, mt, nt);
+    for (int64_t t = cid; t < nctiles; t += ncl) {
+      const TileInfo ti = tile_of(t, mt, ntg, CN, rank);
       const int n0 = ti.n0 * BN + half * CPT;
       float accr[CPT], acci[CPT];
 #pragma unroll
       for (int x = 0; x < CPT; ++x) accr[x] = acci[x] = 0.f;
       for (int sg = 0; sg < nseg; ++sg, ++g) {
         const uint32_t b = g & 1, use = g >> 1;
-        mbar_wait(seg_full + b, use & 1);
+        { long long t0 = dbg ? clock64() : 0; mbar_wait(seg_full + b, use & 1); if (dbg) w0 += clock64() - t0; }
         tc_fence_after();
         const uint32_t base = tmem + lane_addr + b * G::BUF_COLS + half * CPT;
 #pragma unroll
@@ -332,6 +389,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(seg_empty + b)) : "memory");
       }
+      const long long ts0 = dbg ? clock64() : 0;
       const int i = ti.m0 + q * 32 + lane;
       if (i < n1) {
         const float ua = __ldg(uA + i);
@@ -346,11 +404,24 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
           }
         }
       }
+      if (dbg) w1 += clock64() - ts0;
     }
   }
 
+  if (dbg && lane == 0 && warp <= 2) {
+    // [0] total cycles  [1] producer: wait empty  [2] MMA: wait seg_empty  [3] MMA: wait full
+    // [4] epilogue(warp 2): wait seg_full  [5] epilogue(warp 2): store phase  [6] CTAs
+    if (warp == 0) { atomicAdd((unsigned long long*)dbg + 0, (unsigned long long)(clock64() - t_start));
+                     atomicAdd((unsigned long long*)dbg + 1, (unsigned long long)w0);
+                     atomicAdd((unsigned long long*)dbg + 6, 1ull); }
+    if (warp == 1) { atomicAdd((unsigned long long*)dbg + 2, (unsigned long long)w0);
+                     atomicAdd((unsigned long long*)dbg + 3, (unsigned long long)w1); }
+    if (warp == 2) { atomicAdd((unsigned long long*)dbg + 4, (unsigned long long)w0);
+                     atomicAdd((unsigned long long*)dbg + 5, (unsigned long long)w1); }
+  }
   tc_fence_before();
   __syncthreads();
+  if (CN > 1) cluster_sync();      // no CTA leaves while its peer may still signal its barriers
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -390,22 +461,55 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int CN>
 int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
               int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int num_sms,
               cudaStream_t s) {
   using G = Cfg<BN>;
   CUtensorMap mb;
   if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN,
-                CU_TENSOR_MAP_SWIZZLE_64B))
+                B_TMA_SWZ))
     return 4;
-  if (cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) !=
-      cudaSuccess)
+  auto kern = gemm_tc_kernel<BN, CN>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
     return 4;
-  const int64_t ntiles = ((n1 + BM - 1) / BM) * ((n4 + BN - 1) / BN) * h;
-  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
-  gemm_tc_kernel<BN><<<grid, NTHREADS2, G::SMEM, s>>>(ma, mb, Cb, ldc, (int)n1, (int)n2, (int)n4,
-                                                      (int)h, uA, uB);
+  const int64_t ntg = ((n4 + BN - 1) / BN + CN - 1) / CN;
+  const int64_t nct = ((n1 + BM - 1) / BM) * ntg * h;       // cluster tiles
+  const int64_t max_cl = num_sms / CN;
+  const int grid = (int)((nct < max_cl ? nct : max_cl) * CN);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS2);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CN;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
+  // Diagnostics (env TPROD_GEMM_DEBUG=1): per-role barrier-wait cycles, printed after a sync.
+  static long long* dbg_buf = nullptr;
+  static const bool want_dbg = getenv("TPROD_GEMM_DEBUG") != nullptr;
+  long long* dbg = nullptr;
+  if (want_dbg) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, 8 * sizeof(long long));
+    cudaMemsetAsync(dbg_buf, 0, 8 * sizeof(long long), s);
+    dbg = dbg_buf;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, dbg) != cudaSuccess)
+    return 4;
+  if (dbg) {
+    long long hv[8];
+    cudaMemcpyAsync(hv, dbg, sizeof(hv), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double c = hv[6] ? (double)hv[6] : 1.0;
+    fprintf(stderr, "[tprod gemm BN=%d CN=%d] per CTA (cycles): total %.0f | producer wait empty %.0f | "
+            "mma wait seg_empty %.0f, wait full %.0f | epi wait seg_full %.0f, store %.0f\n", BN, CN,
+            hv[0] / c, hv[1] / c, hv[2] / c, hv[3] / c, hv[4] / c, hv[5] / c);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -415,20 +519,26 @@ bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
 
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
                          int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int force_bn, int num_sms,
-                         cudaStream_t s) {
+                         const float* uA, const float* uB, int force_bn, int force_cn,
+                         int num_sms, cudaStream_t s) {
   CUtensorMap ma;
   if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
                     tc::BK, CU_TENSOR_MAP_SWIZZLE_128B))
     return 4;
   int bn = force_bn;
+  const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
   if (bn == 0) {
     // N = 128 unless that leaves SMs idle (small problems), then N = 64
-    const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
     bn = (mt * ((n4 + 127) / 128) * h >= num_sms) ? 128 : 64;
   }
-  if (bn == 128) return tc::launch_bn<128>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
-  return tc::launch_bn<64>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+  const int64_t nt = (n4 + bn - 1) / bn;
+  int cn = force_cn;
+  if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
+  if (bn == 128)
+    return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s)
+                   : tc::launch_bn<128, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+  return cn == 2 ? tc::launch_bn<64, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s)
+                 : tc::launch_bn<64, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
 }
 
 }  // namespace tprod

@@ -49,8 +49,8 @@ void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int
 bool gemm_tc_supported();
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int force_bn, int num_sms,
-                         cudaStream_t s);
+                         const float* uA, const float* uB, int force_bn, int force_cn,
+                         int num_sms, cudaStream_t s);
 
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
 // Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).

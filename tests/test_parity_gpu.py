@@ -115,6 +115,27 @@ def test_simt_engine_cross_check(T):
     assert O.rel_err(C_tc, C_simt) <= TOL32
 
 
+@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (1000, 136, 3, 700), (129, 64, 7, 129)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
+    """GEMM N tile (64/128) and 2-CTA A-multicast clusters change scheduling only: the K order of
+    every output is fixed, so all variants are bitwise identical (odd N-tile counts included)."""
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 11)
+    B = normal((n2, n4, n3), 12)
+    ref = O.tprod_bcirc(A, B)
+    outs = []
+    for bn in (64, 128):
+        for cn in (1, 2):
+            h = T.Handle()
+            h.set_option(T._lib.TPROD_OPT_GEMM_BN, bn)
+            h.set_option(T._lib.TPROD_OPT_GEMM_CLUSTER, cn)
+            outs.append(gpu_tprod(T, A, B, handle=h))
+    assert O.rel_err(outs[0], ref) <= TOL32
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
 # ------------------------------------------------------------------------------- stages
 @pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 100, 4096])
 def test_stage_forward_dft(T, n3):
