@@ -75,6 +75,13 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, float* X, cudaStream_t s);
 
+// In-smem radix-4 FFT transforms for power-of-two 64 < n3 <= 16384 (transforms_fft.cu).
+bool fft_supported(int64_t n3);
+bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                    const float2* tw, __half* out, int64_t ld, float* unscale, cudaStream_t s);
+bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
+                    int64_t n3, const float2* tw, float* X, cudaStream_t s);
+
 // Host-side exact twiddle table: (cos, sin)(2 pi m / n), m = 0..n-1, computed in fp64 with exact
 // quadrant reduction so that m = 0, n/4, n/2, 3n/4 give exactly 0 / +-1.
 void host_twiddles(int n, double* cs /* 2n: cos,sin interleaved */);

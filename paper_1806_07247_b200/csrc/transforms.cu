@@ -236,6 +236,7 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
                       float* unscale, cudaStream_t s) {
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
+  if (launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.tw, out, ld, unscale, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   size_t smem = sizeof(float2) * (size_t)n3;
@@ -303,6 +304,7 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                     int64_t Q, int64_t n3, Twiddles32 tw, float* X, cudaStream_t s) {
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, X, s)) return;
+  if (launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.tw, X, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   inv_kernel<float, float2><<<(unsigned)blocks, threads, sizeof(float2) * n3, s>>>(
