@@ -201,6 +201,43 @@ def test_determinism_and_w_invariance(T):
             assert np.array_equal(Cr, C1[:, s:e, :]), (W, r)
 
 
+def test_nccl_world_of_one(T):
+    """The multi-GPU plumbing through the C ABI on one GPU: NCCL unique id, communicator init
+    (world size 1) and the in-place broadcast used to replicate A; then a t-product on the
+    broadcast tensor.  (World sizes > 1 need more GPUs than gpurun provides; the host logic is
+    covered by tests/test_dist_gloo.py.)"""
+    import torch
+    uid = T.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    h = T.Handle()
+    h.set_world(0, 1, uid)
+    A = normal((40, 30, 9), 8)
+    Ad = dev(A)
+    before = host(Ad).copy()
+    h.bcast_(Ad.permute(2, 1, 0), root=0)
+    assert np.array_equal(host(Ad), before)
+    B = normal((30, 20, 9), 9)
+    assert O.rel_err(gpu_tprod(T, host(Ad), B, handle=h), O.tprod_bcirc(A, B)) <= TOL32
+    with pytest.raises(T.TprodError):
+        h.bcast_(Ad.permute(2, 1, 0), root=1)     # root out of range
+    h2 = T.Handle()
+    with pytest.raises(T.TprodError) as e:
+        h2.bcast_(torch.zeros(4, device="cuda"))  # no world
+    assert e.value.status == T._lib.TPROD_ENOWORLD
+
+
+def test_host_entry_e2e(T):
+    """tprod_f32_host / tprod_f64_host: host buffers in, host result out."""
+    import torch
+    for dt, tol in ((np.float32, TOL32), (np.float64, TOL64)):
+        A = normal((50, 40, 7), 21, dt)
+        B = normal((40, 30, 7), 22, dt)
+        At, Bt = torch.from_numpy(A), torch.from_numpy(B)      # Fortran order = Matlab layout
+        fn = T.tprod_f32_host if dt == np.float32 else T.tprod_f64_host
+        C = fn(At, Bt).numpy()
+        assert O.rel_err(C, O.tprod_bcirc(A, B)) <= tol
+
+
 def test_errors(T):
     import torch
     A = T.to_matlab(torch.randn(4, 5, 6, device="cuda"))
