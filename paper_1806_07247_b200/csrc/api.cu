@@ -233,8 +233,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   launches += (n1 % 4 == 0 && n2 % 4 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 2;
   mark(1);
   // B first: the tail of B just streamed by K0 is still resident in L2
-  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, s); ++launches;   // Alg.1 step 1 (B)
-  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, s); ++launches;   // Alg.1 step 1 (A)
+  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
+  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
   mark(2);
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
@@ -247,7 +247,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   }
   ++launches;                                                     // Alg.1 step 2
   mark(3);
-  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, C, s); ++launches;     // Alg.1 step 2b + 3
+  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, C, h->num_sms, s); ++launches;     // Alg.1 step 2b + 3
   mark(4);
   h->timed_last = h->timing;
   h->last_launches = launches;
@@ -461,7 +461,7 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   __half* sp = (__half*)((char*)h->ws + off_sp);
   CK(cudaMemsetAsync(mx, 0, 4 * (size_t)nmax, s));
   launch_absmax(X, p, q, n3, role, mx, s);
-  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, u, s);
+  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, u, h->num_sms, s);
   launch_decode_split(sp, ld, p, q, n3, role, u, Xre, Xim, s);
   h->last_launches = 3;
   return launch_status();
@@ -476,7 +476,7 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
   cudaStream_t s = (cudaStream_t)stream;
   const float2* tw = nullptr;
   if ((st = get_tw32(h, (int)n3, &tw))) return st;
-  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, Twiddles32{tw, (int)n3}, X, s);
+  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, Twiddles32{tw, (int)n3}, X, h->num_sms, s);
   h->last_launches = 1;
   return launch_status();
 }

@@ -34,7 +34,7 @@ void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int6
 // applies (one writer per index).
 void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
-                      float* unscale, cudaStream_t s);
+                      float* unscale, int num_sms, cudaStream_t s);
 // decode split planes back to fp32 planes [f][q][p] (stage test entry only)
 void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
                          const float* unscale, float* re, float* im, cudaStream_t s);
@@ -55,7 +55,15 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
 // Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, cudaStream_t s);
+                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, int num_sms, cudaStream_t s);
+
+// TMA-staged persistent dense transforms for n3 <= 64 (transforms_tma.cu); false = not handled
+// (unaligned shapes fall back to the register kernels of transforms_dense.cu).  The inverse
+// requires C-bar in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld).
+bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                    __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
+bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
+                    cudaStream_t s);
 
 // ------------------------------------------------------------------ fp64 path
 // spectra as fp64 planes [f][re|im][q][ld]

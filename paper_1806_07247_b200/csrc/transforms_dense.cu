@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
 // Two adjacent tubes (p, p+1) per thread for N <= PAIR_MAX: float2 loads, half2 stores and paired
 // fp16 conversions halve the per-tube instruction count of the memory-bound transforms.
 // Requires P even (then every column start and every plane row stays 8-/4-byte aligned).
-constexpr int PAIR_MAX = 32;
+// Superseded by the TMA-staged kernels (transforms_tma.cu) for every shape the pair path could
+// take (even P, aligned); kept compiled out.
+constexpr int PAIR_MAX = 0;
 
 template <int N, int ROLE>
 __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict__ X, int64_t P,

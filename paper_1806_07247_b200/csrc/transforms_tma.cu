@@ -1,0 +1,393 @@
+// TMA-staged, persistent dense mode-3 transforms for n3 <= 64 (the production K1/K3 of configs
+// 2, 3, 5).  Same arithmetic as transforms_dense.cu (conjugate-pair folding, compile-time twiddle
+// indices into a constant-bank table), different data movement:
+//
+//   * a work item is 256 consecutive tubes p0..p0+255 of one q;
+//   * one thread TMA-loads the item's whole tile  X(p0:p0+256, q, 0:n3)  (a 3-D box, the
+//     out-of-range tail zero-filled) into a shared-memory buffer, double-buffered across the
+//     persistent loop, so HBM latency overlaps the arithmetic of the previous item without
+//     holding the tile in registers;
+//   * each thread reads its TPT adjacent tubes from smem (conflict-free) and writes half2/__half
+//     (K1) or float2/float (K3) results, warp-coalesced along p.  TPT = 2 for n3 <= 32, else 1
+//     (register budget).
+//
+// K1: Alg. 1 step 1, Eq. (2), Hermitian half (Eq. (8)).
+// K3: Alg. 1 step 2 second branch + step 3 (L177-179): fused conjugate fill + inverse DFT.
+#include "internal.h"
+#include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include <vector>
+
+namespace tprod {
+
+namespace {
+
+constexpr int TMAX = 64;
+constexpr int TP = 256;          // tubes per work item
+__constant__ float2 c_tw2[TMAX * (TMAX + 1) / 2];
+__host__ __device__ constexpr int toff(int N) { return N * (N - 1) / 2; }
+__host__ __device__ constexpr int tpt_of(int N) { return N <= 32 ? 2 : 1; }
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nLAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\nbra LAB_WAIT;\nDONE:\n}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(su32(dst)), "l"(m), "r"(su32(b)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+struct Item {
+  int64_t q, p0;
+};
+__device__ __forceinline__ Item item_of(int64_t it, int64_t pblocks) {
+  Item r;
+  r.q = it / pblocks;
+  r.p0 = (it - r.q * pblocks) * TP;
+  return r;
+}
+
+// Persistent double-buffered TMA pipeline shared by K1 and K3: calls body(item, smem buffer) for
+// every work item of this CTA.  BUF = floats per buffer; box = {TP, 1, rows}.
+template <int BUF, typename Body>
+__device__ __forceinline__ void tma_pipeline(const CUtensorMap* m, int64_t P, int64_t Q, float* smem,
+                                             uint64_t* full, Body&& body) {
+  const int tid = threadIdx.x;
+  const int64_t pblocks = (P + TP - 1) / TP;
+  const int64_t items = pblocks * Q;
+  if (tid == 0) {
+    bar_init(&full[0], 1);
+    bar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t it0 = blockIdx.x;
+  if (tid == 0 && it0 < items) {
+    const Item nx = item_of(it0, pblocks);
+    bar_expect(&full[0], BUF * 4);
+    tma3d(smem, m, &full[0], (int)nx.p0, (int)nx.q, 0);
+  }
+  int n = 0;
+  for (int64_t it = it0; it < items; it += gridDim.x, ++n) {
+    const int b = n & 1;
+    if (tid == 0 && it + gridDim.x < items) {       // prefetch the next item into the other buffer
+      const Item nx = item_of(it + gridDim.x, pblocks);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_expect(&full[b ^ 1], BUF * 4);
+      tma3d(smem + (b ^ 1) * BUF, m, &full[b ^ 1], (int)nx.p0, (int)nx.q, 0);
+    }
+    bar_wait(&full[b], (n >> 1) & 1);
+    body(item_of(it, pblocks), smem + b * BUF);
+    __syncthreads();      // buffer b fully consumed before it is refilled (two iterations on)
+  }
+}
+
+// load TPT adjacent floats of row r of a [rows][TP] smem tile
+template <int TPT>
+__device__ __forceinline__ void lds(const float* s, int r, int tid, float (&o)[TPT]) {
+  if constexpr (TPT == 2) {
+    const float2 v = reinterpret_cast<const float2*>(s + r * TP)[tid];
+    o[0] = v.x;
+    o[1] = v.y;
+  } else {
+    o[0] = s[r * TP + tid];
+  }
+}
+
+template <int TPT>
+__device__ __forceinline__ void store_split(__half* dst_hi, __half* dst_lo, const float (&v)[TPT], bool full_pair) {
+  if constexpr (TPT == 2) {
+    const float2 x = make_float2(v[0], v[1]);
+    const __half2 h = __float22half2_rn(x);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __float22half2_rn(make_float2(x.x - hf.x, x.y - hf.y));
+    if (full_pair) {
+      *reinterpret_cast<__half2*>(dst_hi) = h;
+      *reinterpret_cast<__half2*>(dst_lo) = l;
+    } else {
+      *dst_hi = __low2half(h);
+      *dst_lo = __low2half(l);
+    }
+  } else {
+    __half h, l;
+    split_f16(v[0], h, l);
+    *dst_hi = h;
+    *dst_lo = l;
+  }
+}
+
+template <int N, int ROLE>
+__global__ void __launch_bounds__(TP / tpt_of(N)) fwd_tma_kernel(const __grid_constant__ CUtensorMap mX,
+                                                                int64_t P, int64_t Q,
+                                                                const unsigned* __restrict__ maxbits,
+                                                                __half* __restrict__ out, int64_t ld,
+                                                                float* __restrict__ unscale) {
+  constexpr int H = N / 2 + 1;
+  constexpr int K2 = (N - 1) / 2;
+  constexpr int TPT = tpt_of(N);
+  constexpr int BUF = TP * N;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full[2];
+  const int tid = threadIdx.x;
+  const int64_t plane = Q * ld;
+  tma_pipeline<BUF>(&mX, P, Q, smem, full, [&](const Item& cur, const float* s) {
+    const int64_t p = cur.p0 + TPT * tid;
+    if (p >= P) return;
+    const bool pair = (TPT == 2) && (p + 1 < P);
+    float v[N][TPT];
+#pragma unroll
+    for (int k = 0; k < N; ++k) lds<TPT>(s, k, tid, v[k]);
+    float u[K2 + 1][TPT], w[K2 + 1][TPT];
+#pragma unroll
+    for (int k = 1; k <= K2; ++k)
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        u[k][t] = v[k][t] + v[N - k][t];
+        w[k][t] = v[k][t] - v[N - k][t];
+      }
+    const int64_t q = cur.q;
+    float sc[TPT];
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+      int e = 0;
+      if (ROLE == 0) {
+        if (p + t < P) e = scale_exp(__ldg(maxbits + p + t), N);
+        if (q == 0 && p + t < P) unscale[p + t] = pow2f(-e);
+      } else {
+        e = scale_exp(__ldg(maxbits + q), N);
+        if (p == 0 && t == 0) unscale[q] = pow2f(-e);
+      }
+      sc[t] = pow2f(e);
+    }
+    __half* o = out + q * ld + p;
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      float re[TPT], im[TPT];
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        re[t] = v[0][t];
+        im[t] = 0.f;
+      }
+#pragma unroll
+      for (int k = 1; k <= K2; ++k) {
+        const float2 tw = c_tw2[toff(N) + (f * k) % N];
+#pragma unroll
+        for (int t = 0; t < TPT; ++t) {
+          re[t] = fmaf(u[k][t], tw.x, re[t]);
+          im[t] = fmaf(-w[k][t], tw.y, im[t]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        if (N % 2 == 0) re[t] += (f & 1) ? -v[N / 2][t] : v[N / 2][t];
+        re[t] *= sc[t];
+        im[t] *= sc[t];
+      }
+      __half* of = o + (int64_t)(4 * f) * plane;
+      store_split<TPT>(of + PL_RE_HI * plane, of + PL_RE_LO * plane, re, pair);
+      store_split<TPT>(of + PL_IM_HI * plane, of + PL_IM_LO * plane, im, pair);
+    }
+  });
+}
+
+template <int N>
+__global__ void __launch_bounds__(TP / tpt_of(N)) inv_tma_kernel(const __grid_constant__ CUtensorMap mC,
+                                                                int64_t P, int64_t Q, float* __restrict__ X) {
+  constexpr int H = N / 2 + 1;
+  constexpr int TPT = tpt_of(N);
+  constexpr int BUF = TP * 2 * H;                  // floats per buffer: [f][re|im][256]
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full[2];
+  const int tid = threadIdx.x;
+  const float inv_n = 1.f / (float)N;
+  const int64_t PQ = P * Q;
+  tma_pipeline<BUF>(&mC, P, Q, smem, full, [&](const Item& cur, const float* s) {
+    const int64_t p = cur.p0 + TPT * tid;
+    if (p >= P) return;
+    float R[H][TPT], I[H][TPT];
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      const bool self = (f == 0 || 2 * f == N);
+      const float wf = self ? 1.f : 2.f;             // conjugate fill weight
+      lds<TPT>(s, 2 * f, tid, R[f]);
+      lds<TPT>(s, 2 * f + 1, tid, I[f]);
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        R[f][t] *= wf;
+        I[f][t] = self ? 0.f : I[f][t] * wf;       // Im of DC/Nyquist dropped (C2R)
+      }
+    }
+    float* xo = X + p + P * cur.q;
+#pragma unroll
+    for (int tt = 0; tt <= N / 2; ++tt) {
+      float a[TPT], bb[TPT];
+#pragma unroll
+      for (int t = 0; t < TPT; ++t) {
+        a[t] = R[0][t];
+        bb[t] = 0.f;
+      }
+#pragma unroll
+      for (int f = 1; f < H; ++f) {
+        const float2 tw = c_tw2[toff(N) + (f * tt) % N];
+#pragma unroll
+        for (int t = 0; t < TPT; ++t) {
+          a[t] = fmaf(R[f][t], tw.x, a[t]);
+          bb[t] = fmaf(-I[f][t], tw.y, bb[t]);
+        }
+      }
+      if constexpr (TPT == 2) {
+        *reinterpret_cast<float2*>(xo + PQ * tt) = make_float2((a[0] + bb[0]) * inv_n, (a[1] + bb[1]) * inv_n);
+        if (tt > 0 && 2 * tt != N)
+          *reinterpret_cast<float2*>(xo + PQ * (N - tt)) =
+              make_float2((a[0] - bb[0]) * inv_n, (a[1] - bb[1]) * inv_n);
+      } else {
+        xo[PQ * tt] = (a[0] + bb[0]) * inv_n;
+        if (tt > 0 && 2 * tt != N) xo[PQ * (N - tt)] = (a[0] - bb[0]) * inv_n;
+      }
+    }
+  });
+}
+
+// ------------------------------------------------------------------------------ tables / launch
+using FwdFn = void (*)(CUtensorMap, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
+using InvFn = void (*)(CUtensorMap, int64_t, int64_t, float*);
+
+template <int N>
+struct Tab {
+  static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
+    f0[N] = fwd_tma_kernel<N, 0>;
+    f1[N] = fwd_tma_kernel<N, 1>;
+    inv[N] = inv_tma_kernel<N>;
+    Tab<N - 1>::fill(f0, f1, inv);
+  }
+};
+template <>
+struct Tab<0> {
+  static void fill(FwdFn*, FwdFn*, InvFn*) {}
+};
+
+struct Fns {
+  FwdFn f0[TMAX + 1] = {}, f1[TMAX + 1] = {};
+  InvFn inv[TMAX + 1] = {};
+  Fns() { Tab<TMAX>::fill(f0, f1, inv); }
+};
+const Fns& fns() {
+  static Fns t;
+  return t;
+}
+
+bool ensure_tw() {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && (done >> dev) & 1) return true;
+  std::vector<float2> tab(TMAX * (TMAX + 1) / 2);
+  std::vector<double> cs;
+  for (int N = 1; N <= TMAX; ++N) {
+    cs.assign(2 * N, 0.0);
+    host_twiddles(N, cs.data());
+    for (int m = 0; m < N; ++m) tab[toff(N) + m] = make_float2((float)cs[2 * m], (float)cs[2 * m + 1]);
+  }
+  if (cudaMemcpyToSymbol(c_tw2, tab.data(), sizeof(float2) * tab.size()) != cudaSuccess) return false;
+  if (dev < 64) done |= 1ull << dev;
+  return true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// fp32 3-D map {d0 (contiguous, pitch ld0), d1, d2 (pitch ld0*d1)}, box {TP, 1, b2}
+bool map_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t ld0, uint64_t d1, uint64_t d2,
+             uint32_t b2) {
+  auto fn = encode();
+  if (!fn || (ld0 * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0 || b2 > 256) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {ld0 * 4, ld0 * d1 * 4};
+  cuuint32_t box[3] = {(cuuint32_t)TP, 1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int grid_for(int64_t items, size_t smem_bytes, int threads, int num_sms) {
+  int per_sm = (int)((220 * 1024) / (smem_bytes + 1024));
+  const int per_sm_thr = 2048 / threads;
+  if (per_sm > per_sm_thr) per_sm = per_sm_thr;
+  if (per_sm > 8) per_sm = 8;
+  if (per_sm < 1) per_sm = 1;
+  int64_t g = (int64_t)num_sms * per_sm;
+  return (int)(items < g ? items : g);
+}
+
+int threads_of(int64_t n3) { return TP / (n3 <= 32 ? 2 : 1); }
+
+}  // namespace
+
+bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                    __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
+  if (n3 < 1 || n3 > TMAX || ld % 2 != 0 || !ensure_tw()) return false;
+  CUtensorMap m;
+  if (!map_f32(&m, X, (uint64_t)P, (uint64_t)P, (uint64_t)Q, (uint64_t)n3, (uint32_t)n3)) return false;
+  FwdFn fn = role == 0 ? fns().f0[n3] : fns().f1[n3];
+  const size_t smem = 2 * sizeof(float) * TP * (size_t)n3;
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return false;
+  const int64_t items = (P + TP - 1) / TP * Q;
+  const int thr = threads_of(n3);
+  const int grid = grid_for(items, smem, thr, num_sms);
+  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld, (void*)&unscale};
+  return cudaLaunchKernel((const void*)fn, dim3(grid), dim3(thr), args, smem, s) == cudaSuccess;
+}
+
+bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
+                    cudaStream_t s) {
+  // C-bar planes [f][re|im][q][ld] as a 3-D map {P (pitch ld), Q, 2h}
+  if (n3 < 1 || n3 > TMAX || !ensure_tw() || ((uintptr_t)X & 7) != 0 || P % 2 != 0) return false;
+  const int64_t h = n3 / 2 + 1;
+  CUtensorMap m;
+  if (!map_f32(&m, Cre, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(2 * h), (uint32_t)(2 * h)))
+    return false;
+  InvFn fn = fns().inv[n3];
+  const size_t smem = 2 * sizeof(float) * TP * 2 * (size_t)h;
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return false;
+  const int64_t items = (P + TP - 1) / TP * Q;
+  const int thr = threads_of(n3);
+  const int grid = grid_for(items, smem, thr, num_sms);
+  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&X};
+  return cudaLaunchKernel((const void*)fn, dim3(grid), dim3(thr), args, smem, s) == cudaSuccess;
+}
+
+}  // namespace tprod
