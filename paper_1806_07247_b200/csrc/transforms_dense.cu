@@ -30,6 +30,101 @@ __constant__ float2 c_tw[DENSE_MAX * (DENSE_MAX + 1) / 2];
 
 __host__ __device__ constexpr int tw_off(int N) { return N * (N - 1) / 2; }
 
+// ---------------------------------------------------------------- register real FFT (N = 2^m >= 8)
+// For power-of-two N the Hermitian half is computed in O(N log N) instead of the O(N^2/2) pair
+// folding: pack z[n] = x[2n] + i x[2n+1] (n < M = N/2), Z = FFT_M(z) (radix-2 DIT
+// in registers, twiddle indices compile-time), then
+//   E_k = (Z_k + conj Z_{M-k})/2,  O_k = (Z_k - conj Z_{M-k})/(2i),  X_k = E_k + w^k O_k,  k = 0..M
+// with w = e^{-2 pi i/N}.  The inverse reverses it: E_k = (X_k + conj X_{M-k})/2,
+// O_k = w^{-k} (X_k - conj X_{M-k})/2, z = IFFT_M(E + i O), x[2n] = Re z, x[2n+1] = Im z.
+__host__ __device__ constexpr bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+__host__ __device__ constexpr int bitrev(int v, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((v >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
+
+// in-place forward DFT of a[0..M) (natural order in, natural order out), twiddles from table N
+template <int N, int M>
+__device__ __forceinline__ void cfft_reg(float2 (&a)[M]) {
+  constexpr int LB = ilog2c(M);
+  float2 b[M];
+#pragma unroll
+  for (int n = 0; n < M; ++n) b[bitrev(n, LB)] = a[n];
+#pragma unroll
+  for (int st = 0; st < LB; ++st) {
+    const int len = 2 << st;
+#pragma unroll
+    for (int i = 0; i < M; i += len) {
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        const float2 u = b[i + j];
+        float2 v = b[i + j + len / 2];
+        if (j != 0) {
+          const float2 t = c_tw[tw_off(N) + j * (N / len)];     // w_len^j = (c, -s)
+          v = make_float2(v.x * t.x + v.y * t.y, v.y * t.x - v.x * t.y);
+        }
+        b[i + j] = make_float2(u.x + v.x, u.y + v.y);
+        b[i + j + len / 2] = make_float2(u.x - v.x, u.y - v.y);
+      }
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < M; ++n) a[n] = b[n];
+}
+
+template <int N>
+__device__ __forceinline__ void rfft_half(const float (&x)[N], float2 (&X)[N / 2 + 1]) {
+  constexpr int M = N / 2;
+  float2 z[M];
+#pragma unroll
+  for (int n = 0; n < M; ++n) z[n] = make_float2(x[2 * n], x[2 * n + 1]);
+  cfft_reg<N, M>(z);
+#pragma unroll
+  for (int k = 0; k <= M; ++k) {
+    const float2 zk = z[k % M], zm = z[(M - k) % M];
+    const float2 E = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    const float2 O = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    if (k == 0 || k == M) {
+      X[k] = make_float2(k == 0 ? E.x + O.x : E.x - O.x, k == 0 ? E.y + O.y : E.y - O.y);
+    } else {
+      const float2 t = c_tw[tw_off(N) + k];                        // w^k = (c, -s)
+      X[k] = make_float2(E.x + O.x * t.x + O.y * t.y, E.y + O.y * t.x - O.x * t.y);
+    }
+  }
+}
+
+// C2R: X[0].y and X[N/2].y are ignored (Im of DC/Nyquist dropped); includes the 1/N scaling.
+template <int N>
+__device__ __forceinline__ void irfft_half(const float2 (&X)[N / 2 + 1], float (&x)[N]) {
+  constexpr int M = N / 2;
+  float2 z[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const float2 xk = (k == 0) ? make_float2(X[0].x, 0.f) : X[k];
+    const float2 xm = (k == 0) ? make_float2(X[M].x, 0.f) : X[M - k];
+    const float2 E = make_float2(0.5f * (xk.x + xm.x), 0.5f * (xk.y - xm.y));
+    const float2 D = make_float2(0.5f * (xk.x - xm.x), 0.5f * (xk.y + xm.y));   // (X_k - conj X_{M-k})/2
+    float2 O;
+    if (k == 0) {
+      O = D;
+    } else {
+      const float2 t = c_tw[tw_off(N) + k];                        // w^{-k} = (c, +s)
+      O = make_float2(D.x * t.x - D.y * t.y, D.x * t.y + D.y * t.x);
+    }
+    // conj(E + i O) for the forward-FFT-based inverse
+    z[k] = make_float2(E.x - O.y, -(E.y + O.x));
+  }
+  cfft_reg<N, M>(z);
+  const float inv_m = 1.f / (float)M;
+#pragma unroll
+  for (int n = 0; n < M; ++n) {          // z = conj(FFT(conj Z)) / M
+    x[2 * n] = z[n].x * inv_m;
+    x[2 * n + 1] = -z[n].y * inv_m;
+  }
+}
+
 template <int N, int ROLE>
 __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict__ X, int64_t P, int64_t Q,
                                                         const unsigned* __restrict__ maxbits,
@@ -46,11 +141,28 @@ __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict_
   float v[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = __ldg(x + PQ * k);
-  float u[K2 + 1], w[K2 + 1];
+  float2 Xf[H];
+  if constexpr (is_pow2(N) && N >= 8) {
+    rfft_half<N>(v, Xf);
+  } else {
+    float u[K2 + 1], w[K2 + 1];
 #pragma unroll
-  for (int k = 1; k <= K2; ++k) {
-    u[k] = v[k] + v[N - k];
-    w[k] = v[k] - v[N - k];
+    for (int k = 1; k <= K2; ++k) {
+      u[k] = v[k] + v[N - k];
+      w[k] = v[k] - v[N - k];
+    }
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      float re = v[0], im = 0.f;
+#pragma unroll
+      for (int k = 1; k <= K2; ++k) {
+        const float2 t = c_tw[tw_off(N) + (f * k) % N];
+        re = fmaf(u[k], t.x, re);
+        im = fmaf(-w[k], t.y, im);
+      }
+      if (N % 2 == 0) re += (f & 1) ? -v[N / 2] : v[N / 2];
+      Xf[f] = make_float2(re, im);
+    }
   }
   const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), N);
   const float sc = pow2f(e);
@@ -59,19 +171,11 @@ __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict_
   __half* o = out + q * ld + p;
 #pragma unroll
   for (int f = 0; f < H; ++f) {
-    float re = v[0], im = 0.f;
-#pragma unroll
-    for (int k = 1; k <= K2; ++k) {
-      const float2 t = c_tw[tw_off(N) + (f * k) % N];
-      re = fmaf(u[k], t.x, re);
-      im = fmaf(-w[k], t.y, im);
-    }
-    if (N % 2 == 0) re += (f & 1) ? -v[N / 2] : v[N / 2];
     __half hi, lo;
-    split_f16(re * sc, hi, lo);
+    split_f16(Xf[f].x * sc, hi, lo);
     o[(int64_t)(4 * f + PL_RE_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_RE_LO) * plane] = lo;
-    split_f16(im * sc, hi, lo);
+    split_f16(Xf[f].y * sc, hi, lo);
     o[(int64_t)(4 * f + PL_IM_HI) * plane] = hi;
     o[(int64_t)(4 * f + PL_IM_LO) * plane] = lo;
   }
@@ -89,6 +193,21 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
   if (p >= P) return;
   const float* cr = Cre + q * ld + p;
   const float* ci = Cim + q * ld + p;
+  const int64_t PQ = P * Q;
+  float* xo = X + p + P * q;
+  if constexpr (is_pow2(N) && N >= 8) {
+    float2 Xf[H];
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      const bool self = (f == 0 || 2 * f == N);
+      Xf[f] = make_float2(__ldg(cr + fstride * f), self ? 0.f : __ldg(ci + fstride * f));
+    }
+    float xt[N];
+    irfft_half<N>(Xf, xt);
+#pragma unroll
+    for (int t = 0; t < N; ++t) xo[PQ * t] = xt[t];
+    return;
+  }
   float R[H], I[H];
 #pragma unroll
   for (int f = 0; f < H; ++f) {
@@ -97,8 +216,6 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
     I[f] = (f == 0 || 2 * f == N) ? 0.f : wf * __ldg(ci + fstride * f);  // Im of DC/Nyquist dropped
   }
   const float inv_n = 1.f / (float)N;
-  const int64_t PQ = P * Q;
-  float* xo = X + p + P * q;
 #pragma unroll
   for (int t = 0; t <= N / 2; ++t) {
     float a = R[0], b = 0.f;
@@ -116,9 +233,7 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
 // Two adjacent tubes (p, p+1) per thread for N <= PAIR_MAX: float2 loads, half2 stores and paired
 // fp16 conversions halve the per-tube instruction count of the memory-bound transforms.
 // Requires P even (then every column start and every plane row stays 8-/4-byte aligned).
-// Superseded by the TMA-staged kernels (transforms_tma.cu) for every shape the pair path could
-// take (even P, aligned); kept compiled out.
-constexpr int PAIR_MAX = 0;
+constexpr int PAIR_MAX = 32;
 
 template <int N, int ROLE>
 __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict__ X, int64_t P,
@@ -136,11 +251,42 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
   float2 v[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) v[k] = __ldg(x + PQh * k);
-  float2 u[K2 + 1], w[K2 + 1];
+  float2 X0[H], X1[H];              // spectra of tube p (X0) and p+1 (X1)
+  if constexpr (is_pow2(N) && N >= 8) {
+    float t0[N], t1[N];
 #pragma unroll
-  for (int k = 1; k <= K2; ++k) {
-    u[k] = make_float2(v[k].x + v[N - k].x, v[k].y + v[N - k].y);
-    w[k] = make_float2(v[k].x - v[N - k].x, v[k].y - v[N - k].y);
+    for (int k = 0; k < N; ++k) {
+      t0[k] = v[k].x;
+      t1[k] = v[k].y;
+    }
+    rfft_half<N>(t0, X0);
+    rfft_half<N>(t1, X1);
+  } else {
+    float2 u[K2 + 1], w[K2 + 1];
+#pragma unroll
+    for (int k = 1; k <= K2; ++k) {
+      u[k] = make_float2(v[k].x + v[N - k].x, v[k].y + v[N - k].y);
+      w[k] = make_float2(v[k].x - v[N - k].x, v[k].y - v[N - k].y);
+    }
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      float2 re = v[0], im = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 1; k <= K2; ++k) {
+        const float2 t = c_tw[tw_off(N) + (f * k) % N];
+        re.x = fmaf(u[k].x, t.x, re.x);
+        re.y = fmaf(u[k].y, t.x, re.y);
+        im.x = fmaf(-w[k].x, t.y, im.x);
+        im.y = fmaf(-w[k].y, t.y, im.y);
+      }
+      if (N % 2 == 0) {
+        const float sg = (f & 1) ? -1.f : 1.f;
+        re.x = fmaf(sg, v[N / 2].x, re.x);
+        re.y = fmaf(sg, v[N / 2].y, re.y);
+      }
+      X0[f] = make_float2(re.x, im.x);
+      X1[f] = make_float2(re.y, im.y);
+    }
   }
   int e0, e1;
   if (ROLE == 0) {
@@ -159,21 +305,7 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
   __half* o = out + q * ld + p;
 #pragma unroll
   for (int f = 0; f < H; ++f) {
-    float2 re = v[0], im = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int k = 1; k <= K2; ++k) {
-      const float2 t = c_tw[tw_off(N) + (f * k) % N];
-      re.x = fmaf(u[k].x, t.x, re.x);
-      re.y = fmaf(u[k].y, t.x, re.y);
-      im.x = fmaf(-w[k].x, t.y, im.x);
-      im.y = fmaf(-w[k].y, t.y, im.y);
-    }
-    if (N % 2 == 0) {
-      const float sg = (f & 1) ? -1.f : 1.f;
-      re.x = fmaf(sg, v[N / 2].x, re.x);
-      re.y = fmaf(sg, v[N / 2].y, re.y);
-    }
-    const float2 rs = make_float2(re.x * s0, re.y * s1), is = make_float2(im.x * s0, im.y * s1);
+    const float2 rs = make_float2(X0[f].x * s0, X1[f].x * s1), is = make_float2(X0[f].y * s0, X1[f].y * s1);
     const __half2 rh = __float22half2_rn(rs), ih = __float22half2_rn(is);
     const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
     const __half2 rl = __float22half2_rn(make_float2(rs.x - rhf.x, rs.y - rhf.y));
@@ -198,6 +330,25 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
   const float2* cr = reinterpret_cast<const float2*>(Cre + q * ld + p);
   const float2* ci = reinterpret_cast<const float2*>(Cim + q * ld + p);
   const int64_t fs = fstride >> 1;
+  const int64_t PQh = (P * Q) >> 1;
+  float2* xo = reinterpret_cast<float2*>(X + p + P * q);
+  if constexpr (is_pow2(N) && N >= 8) {
+    float2 X0[H], X1[H];
+#pragma unroll
+    for (int f = 0; f < H; ++f) {
+      const bool self = (f == 0 || 2 * f == N);
+      const float2 r = __ldg(cr + fs * f);
+      const float2 i = self ? make_float2(0.f, 0.f) : __ldg(ci + fs * f);
+      X0[f] = make_float2(r.x, i.x);
+      X1[f] = make_float2(r.y, i.y);
+    }
+    float x0[N], x1[N];
+    irfft_half<N>(X0, x0);
+    irfft_half<N>(X1, x1);
+#pragma unroll
+    for (int t = 0; t < N; ++t) xo[PQh * t] = make_float2(x0[t], x1[t]);
+    return;
+  }
   float2 R[H], I[H];
 #pragma unroll
   for (int f = 0; f < H; ++f) {
@@ -213,8 +364,6 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
     }
   }
   const float inv_n = 1.f / (float)N;
-  const int64_t PQh = (P * Q) >> 1;
-  float2* xo = reinterpret_cast<float2*>(X + p + P * q);
 #pragma unroll
   for (int t = 0; t <= N / 2; ++t) {
     float2 a = R[0], b = make_float2(0.f, 0.f);

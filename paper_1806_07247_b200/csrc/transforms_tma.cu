@@ -269,17 +269,22 @@ __global__ void __launch_bounds__(TP / tpt_of(N)) inv_tma_kernel(const __grid_co
 using FwdFn = void (*)(CUtensorMap, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
 using InvFn = void (*)(CUtensorMap, int64_t, int64_t, float*);
 
+// Measured (config 3, n3 = 31): the register kernels of transforms_dense.cu (direct warp-coalesced
+// loads, ~14 warps/SM) already run K1 at ~5.5 TB/s and K3 faster than the TMA-staged variants, so
+// the TMA path is instantiated only where it wins: the forward transform for 32 < n3 <= 64
+// (config 5: 18.9 -> 13.9 ms).  TMIN..TMAX bound the instantiated range.
+constexpr int TMIN = 33;
+
 template <int N>
 struct Tab {
   static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
     f0[N] = fwd_tma_kernel<N, 0>;
     f1[N] = fwd_tma_kernel<N, 1>;
-    inv[N] = inv_tma_kernel<N>;
     Tab<N - 1>::fill(f0, f1, inv);
   }
 };
 template <>
-struct Tab<0> {
+struct Tab<TMIN - 1> {
   static void fill(FwdFn*, FwdFn*, InvFn*) {}
 };
 
@@ -357,7 +362,8 @@ int threads_of(int64_t n3) { return TP / (n3 <= 32 ? 2 : 1); }
 
 bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
-  if (n3 < 1 || n3 > TMAX || ld % 2 != 0 || !ensure_tw()) return false;
+  // power-of-two n3 takes the register real-FFT kernels (transforms_dense.cu) instead
+  if (n3 < TMIN || n3 > TMAX || (n3 & (n3 - 1)) == 0 || ld % 2 != 0 || !ensure_tw()) return false;
   CUtensorMap m;
   if (!map_f32(&m, X, (uint64_t)P, (uint64_t)P, (uint64_t)Q, (uint64_t)n3, (uint32_t)n3)) return false;
   FwdFn fn = role == 0 ? fns().f0[n3] : fns().f1[n3];
@@ -374,7 +380,9 @@ bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
 bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
                     cudaStream_t s) {
   // C-bar planes [f][re|im][q][ld] as a 3-D map {P (pitch ld), Q, 2h}
-  if (n3 < 1 || n3 > TMAX || !ensure_tw() || ((uintptr_t)X & 7) != 0 || P % 2 != 0) return false;
+  if (n3 < TMIN || n3 > TMAX || fns().inv[n3] == nullptr || !ensure_tw() || ((uintptr_t)X & 7) != 0 ||
+      P % 2 != 0)
+    return false;
   const int64_t h = n3 / 2 + 1;
   CUtensorMap m;
   if (!map_f32(&m, Cre, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(2 * h), (uint32_t)(2 * h)))
