@@ -27,6 +27,7 @@ struct tprod_ctx {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   std::map<int, float2*> tw32;
+  std::map<int, float2*> st32;   // Stockham FFT tables (power-of-two n3 > 64)
   std::map<int, double2*> tw64;
   void* hbuf[3] = {nullptr, nullptr, nullptr};   // device buffers of the *_host entry points
   size_t hbuf_bytes[3] = {0, 0, 0};
@@ -163,6 +164,28 @@ int get_tw32(tprod_ctx* h, int n3, const float2** out) {
   return TPROD_OK;
 }
 
+// The fp32 twiddles of a call: the (cos, sin) table, plus the Stockham FFT table when n3 takes the
+// FFT path.
+int get_twiddles32(tprod_ctx* h, int n3, Twiddles32* T) {
+  const float2* tw = nullptr;
+  int st = get_tw32(h, n3, &tw);
+  if (st) return st;
+  *T = Twiddles32{tw, n3, nullptr};
+  if (!fft_supported(n3)) return TPROD_OK;
+  auto it = h->st32.find(n3);
+  if (it != h->st32.end()) { T->st = it->second; return TPROD_OK; }
+  std::vector<double> cs(2 * (size_t)n3);
+  host_twiddles(n3, cs.data());
+  std::vector<float2> t(stockham_table_len(n3) + 1);
+  host_stockham_table(n3, cs.data(), t.data());
+  float2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(float2) * t.size()) != cudaSuccess) { cudaGetLastError(); return TPROD_ENOMEM; }
+  CK(cudaMemcpy(d, t.data(), sizeof(float2) * t.size(), cudaMemcpyHostToDevice));
+  h->st32[n3] = d;
+  T->st = d;
+  return TPROD_OK;
+}
+
 int get_tw64(tprod_ctx* h, int n3, const double2** out) {
   auto it = h->tw64.find(n3);
   if (it != h->tw64.end()) { *out = it->second; return TPROD_OK; }
@@ -212,8 +235,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   Layout32 L = layout32(n1, n2, n3, n4);
   int st = ensure_ws(h, L.total);
   if (st) return st;
-  const float2* tw = nullptr;
-  if ((st = get_tw32(h, (int)n3, &tw))) return st;
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   char* ws = (char*)h->ws;
   unsigned* maxA = (unsigned*)(ws + L.off_maxA);
   unsigned* maxB = (unsigned*)(ws + L.off_maxB);
@@ -222,7 +245,6 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   __half* Ab = (__half*)(ws + L.off_Ab);
   __half* Bb = (__half*)(ws + L.off_Bb);
   float* Cb = (float*)(ws + L.off_Cb);
-  Twiddles32 T{tw, (int)n3};
   int64_t launches = 0;
 
   auto mark = [&](int i) { if (h->timing) cudaEventRecord(h->ev[i], s); };
@@ -337,6 +359,7 @@ int tprod_destroy(tprod_handle h) {
   if (h->comm && nccl().ok) nccl().CommDestroy((ncclComm_t)h->comm);
   for (int i = 0; i < 5; ++i) if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   for (auto& kv : h->tw32) cudaFree(kv.second);
+  for (auto& kv : h->st32) cudaFree(kv.second);
   for (auto& kv : h->tw64) cudaFree(kv.second);
   for (int i = 0; i < 3; ++i) if (h->hbuf[i]) cudaFree(h->hbuf[i]);
   if (h->ws) cudaFree(h->ws);
@@ -454,14 +477,14 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   size_t off_u = align_up(4 * (size_t)nmax, 1024);
   size_t off_sp = off_u + align_up(4 * (size_t)nmax, 1024);
   if ((st = ensure_ws(h, off_sp + 2 * (size_t)(hh * NPLANES * q * ld)))) return st;
-  const float2* tw = nullptr;
-  if ((st = get_tw32(h, (int)n3, &tw))) return st;
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   unsigned* mx = (unsigned*)h->ws;
   float* u = (float*)((char*)h->ws + off_u);
   __half* sp = (__half*)((char*)h->ws + off_sp);
   CK(cudaMemsetAsync(mx, 0, 4 * (size_t)nmax, s));
   launch_absmax(X, p, q, n3, role, mx, s);
-  launch_fwd_split(X, p, q, n3, role, mx, Twiddles32{tw, (int)n3}, sp, ld, u, h->num_sms, s);
+  launch_fwd_split(X, p, q, n3, role, mx, T, sp, ld, u, h->num_sms, s);
   launch_decode_split(sp, ld, p, q, n3, role, u, Xre, Xim, s);
   h->last_launches = 3;
   return launch_status();
@@ -474,9 +497,9 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
   if (st) return st;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const float2* tw = nullptr;
-  if ((st = get_tw32(h, (int)n3, &tw))) return st;
-  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, Twiddles32{tw, (int)n3}, X, h->num_sms, s);
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, T, X, h->num_sms, s);
   h->last_launches = 1;
   return launch_status();
 }
@@ -497,7 +520,7 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       h->timing = value != 0;
       return TPROD_OK;
     case TPROD_OPT_GEMM_CLUSTER:
-      if (value != 0 && value != 1 && value != 2) return TPROD_EINVAL;
+      if (value < 0 || value > 3) return TPROD_EINVAL;
       h->force_cn = (int)value;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:

@@ -457,6 +457,274 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------- 2-SM kernel
+// CTA pair (cta_group::2): one 256 x 128 output tile of one frequency per cluster of two CTAs on
+// the two SMs of a TPC.  CTA r holds rows m0 + 128 r .. +127 of A (its own 128 TMEM lanes of the
+// accumulators) and N rows n0 + 64 r .. +63 of B; the leader (r = 0) issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 128), which reads A and B from both CTAs' shared memory
+// at the same offsets.  Per SM and per MMA that is 4 KB of A + 2 KB of B (96 B/clk at the MMA
+// rate, against 128 B/clk for the single-CTA 128 x 128 tile), and 48 KB of TMA traffic per
+// K block.  Barriers:
+//   full[s]      leader's; armed by the leader with both CTAs' bytes, completed by both CTAs'
+//                TMA loads (cta_group::2 TMA signals the leader's barrier)
+//   empty[s]     both CTAs'; the leader's MMA commit arrives on both (multicast)
+//   seg_full[b]  both CTAs'; multicast commit after the last MMA of a promoted segment
+//   seg_empty[b] leader's; all 2 x 8 epilogue warps of the pair arrive (the peer's remotely)
+// Same arithmetic, K order and epilogue as gemm_tc_kernel<128, *>: results are bitwise identical.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA load into this CTA's smem whose completion is counted on the mbarrier at shared::cluster
+// address `bar_cl` (the leader's).
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl, int c0,
+                                                 int c1, int c2) {
+  asm volatile(
+      "{\n"
+      ".reg .pred pe;\n"
+      "elect.sync _|pe, 0xffffffff;\n"
+      "@pe cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma2_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred pe, p;\n"
+      "elect.sync _|pe, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@pe tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred pe;\n"
+      "elect.sync _|pe, 0xffffffff;\n"
+      "@pe tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+template <int SEGKB>
+__global__ void __launch_bounds__(NTHREADS2, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
+                    const float* __restrict__ uA, const float* __restrict__ uB) {
+  constexpr int BN = 128;
+  constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
+  constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
+  constexpr int STAGE = NPLANES * (A_PLANE + B_PLANE);
+  constexpr int STAGES = (227 * 1024 - 2048) / STAGE;
+  constexpr int BUF_COLS = 2 * BN;
+  constexpr int TMEM_COLS = 2 * BUF_COLS;
+  constexpr int CPT = BN / 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* seg_full = empty + STAGES;     // [2]
+  uint64_t* seg_empty = seg_full + 2;      // [2]
+  uint32_t* tmem_slot = (uint32_t*)(seg_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int nk = (n2 + BK - 1) / BK;
+  const int nseg = (nk + SEGKB - 1) / SEGKB;
+  const int mt = (n1 + 2 * BM - 1) / (2 * BM), nt = (n4 + BN - 1) / BN;
+  const int64_t ntiles = (int64_t)mt * nt * h;
+  const int64_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(seg_full + b, 1);
+      mbar_init(seg_empty + b, 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                 // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {
+    n0 = (int)(t % nt) * BN;
+    const int64_t r = t / nt;
+    m0 = (int)(r % mt) * (2 * BM);
+    f = (int)(r / mt);
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer (both CTAs)
+    const uint32_t full_cl = mapa_u32(smem_u32(full), 0);      // leader's full[0]
+    uint32_t it = 0;
+    for (int64_t t = cid; t < ntiles; t += ncl) {
+      int f, m0, n0;
+      tile_of2(t, f, m0, n0);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        uint8_t* st = smem + s * STAGE;
+        if (rank == 0) mbar_expect_tx(full + s, 2 * STAGE);
+        const uint32_t bar = full_cl + s * 8;
+        const int k0 = kb * BK;
+        const int mr = m0 + BM * (int)rank, nr = n0 + (BN / 2) * (int)rank;
+#pragma unroll
+        for (int p = 0; p < NPLANES; ++p) {
+          uint8_t* a = st + p * A_PLANE;
+          tma_load_3d_pair(a, &tmA, bar, mr, k0, 4 * f + p);
+          tma_load_3d_pair(a + BK * 128, &tmA, bar, mr + 64, k0, 4 * f + p);
+          tma_load_3d_pair(st + NPLANES * A_PLANE + p * B_PLANE, &tmB, bar, k0, nr, 4 * f + p);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // -------------------------------------------------------------- MMA issuer (leader only)
+      constexpr uint32_t ID_POS = idesc_f16(2 * BM, BN, 0);
+      constexpr uint32_t ID_NEG = idesc_f16(2 * BM, BN, 1);
+      uint32_t it = 0, g = 0;
+      for (int64_t t = cid; t < ntiles; t += ncl) {
+        for (int sg = 0; sg < nseg; ++sg, ++g) {
+          const uint32_t b = g & 1, use = g >> 1;
+          mbar_wait_cluster(seg_empty + b, (use & 1) ^ 1);    // both CTAs drained this buffer
+          tc_fence_after();
+          const uint32_t tCr = tmem + b * BUF_COLS, tCi = tCr + BN;
+          const int kb_end = min(nk, (sg + 1) * SEGKB);
+          for (int kb = sg * SEGKB; kb < kb_end; ++kb, ++it) {
+            const int s = it % STAGES;
+            const uint32_t ph = (it / STAGES) & 1;
+            mbar_wait_cluster(full + s, ph);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * STAGE);
+            const uint32_t bbase = base + NPLANES * A_PLANE;
+#pragma unroll
+            for (int ks = 0; ks < BK / 16; ++ks) {
+              uint64_t a[NPLANES], bd[NPLANES];
+#pragma unroll
+              for (int p = 0; p < NPLANES; ++p) {
+                a[p] = sdesc(base + p * A_PLANE + ks * 2048, BK * 128, 1024, 2);
+                bd[p] = sdesc(bbase + p * B_PLANE + ks * 32, 16, 8 * B_ROW, B_SWZ);
+              }
+              const uint32_t acc0 = (kb > sg * SEGKB || ks > 0) ? 1u : 0u;
+              mma2_f16(tCr, a[PL_RE_HI], bd[PL_RE_HI], ID_POS, acc0);
+              mma2_f16(tCr, a[PL_RE_HI], bd[PL_RE_LO], ID_POS, 1);
+              mma2_f16(tCr, a[PL_RE_LO], bd[PL_RE_HI], ID_POS, 1);
+              mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
+              mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
+              mma2_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
+              mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
+              mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
+              mma2_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
+              mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
+              mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
+              mma2_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+            }
+            mma2_commit_mc(empty + s, (uint16_t)3);     // slot s free in both CTAs
+          }
+          mma2_commit_mc(seg_full + b, (uint16_t)3);    // segment accumulators complete (both)
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (both CTAs)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const int64_t plane = (int64_t)n4 * ldc;
+    const uint32_t segE_cl = mapa_u32(smem_u32(seg_empty), 0);   // leader's seg_empty[0]
+    uint32_t g = 0;
+    for (int64_t t = cid; t < ntiles; t += ncl) {
+      int f, m0, n0t;
+      tile_of2(t, f, m0, n0t);
+      const int n0 = n0t + half * CPT;
+      float accr[CPT], acci[CPT];
+#pragma unroll
+      for (int x = 0; x < CPT; ++x) accr[x] = acci[x] = 0.f;
+      for (int sg = 0; sg < nseg; ++sg, ++g) {
+        const uint32_t b = g & 1, use = g >> 1;
+        mbar_wait(seg_full + b, use & 1);
+        tc_fence_after();
+        const uint32_t base = tmem + lane_addr + b * BUF_COLS + half * CPT;
+#pragma unroll
+        for (int c = 0; c < CPT; c += 16) {
+          uint32_t vr[16], vi[16];
+          tmem_ld16_nowait(base + c, vr);
+          tmem_ld16_nowait(base + BN + c, vi);
+          tmem_wait();
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            accr[c + x] += __uint_as_float(vr[x]);
+            acci[c + x] += __uint_as_float(vi[x]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(segE_cl + b * 8)
+                       : "memory");
+      }
+      const int i = m0 + BM * (int)rank + q * 32 + lane;
+      if (i < n1) {
+        const float ua = __ldg(uA + i);
+        float* Cr = Cb + (int64_t)(2 * f) * plane + (int64_t)n0 * ldc + i;
+        float* Ci = Cr + plane;
+#pragma unroll
+        for (int x = 0; x < CPT; ++x) {
+          if (n0 + x < n4) {
+            const float ub = __ldg(uB + n0 + x);
+            Cr[(int64_t)x * ldc] = (accr[x] * ua) * ub;
+            Ci[(int64_t)x * ldc] = (acci[x] * ua) * ub;
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -541,6 +809,40 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
+template <int SEGKB>
+int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
+                int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int num_sms,
+                cudaStream_t s) {
+  constexpr int BN = 128;
+  constexpr int STAGE = NPLANES * (BK * BM * 2 + (BN / 2) * BK * 2);
+  constexpr int STAGES = (227 * 1024 - 2048) / STAGE;
+  constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  CUtensorMap mb;
+  if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN / 2,
+                B_TMA_SWZ))
+    return 4;
+  auto kern = gemm_tc2_kernel<SEGKB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return 4;
+  const int64_t nct = ((n1 + 2 * BM - 1) / (2 * BM)) * ((n4 + BN - 1) / BN) * h;
+  const int64_t max_cl = num_sms / 2;
+  const int grid = (int)((nct < max_cl ? nct : max_cl) * 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS2);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB) != cudaSuccess) return 4;
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
 }  // namespace tc
 
 bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
@@ -561,6 +863,12 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   }
   const int64_t nt = (n4 + bn - 1) / bn;
   int cn = force_cn;
+  // cta_group::2 pairs: 256 x 128 tiles (enough of them to fill the SM pairs)
+  const bool pair_ok = bn == 128 || force_bn == 0;
+  if (cn == 3 || (cn == 0 && force_bn == 0 && n1 > 128 &&
+                  ((n1 + 255) / 256) * ((n4 + 127) / 128) * h >= num_sms / 2)) {
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+  }
   if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
   if (bn == 128)
     return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s)

@@ -18,7 +18,11 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // operand of the per-frequency GEMM.  C-bar is fp32 planes [f][re|im][j][ldc] (i fastest).
 enum { PL_RE_HI = 0, PL_RE_LO = 1, PL_IM_HI = 2, PL_IM_LO = 3, NPLANES = 4 };
 
-struct Twiddles32 { const float2* tw; int n3; };   // tw[m] = (cos 2pi m/n3, sin 2pi m/n3)
+struct Twiddles32 {
+  const float2* tw;              // tw[m] = (cos 2pi m/n3, sin 2pi m/n3)
+  int n3;
+  const float2* st = nullptr;    // Stockham per-pass twiddle table (FFT path only), see transforms_fft.cu
+};
 struct Twiddles64 { const double2* tw; int n3; };
 
 // K0: per-index max |x| as float bits (non-negative floats order like unsigned ints).
@@ -83,12 +87,18 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, float* X, cudaStream_t s);
 
-// In-smem radix-4 FFT transforms for power-of-two 64 < n3 <= 16384 (transforms_fft.cu).
+// In-smem radix-16 Stockham FFT transforms for power-of-two 64 < n3 <= 16384 (transforms_fft.cu).
+// `st` is the Stockham table of host_stockham_table (device copy).
 bool fft_supported(int64_t n3);
 bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
-                    const float2* tw, __half* out, int64_t ld, float* unscale, cudaStream_t s);
+                    const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s);
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
-                    int64_t n3, const float2* tw, float* X, cudaStream_t s);
+                    int64_t n3, const float2* st, float* X, cudaStream_t s);
+// Per-pass twiddles of the radix-16 Stockham FFT, laid out [pass][r-1][k] so that a warp's lookups
+// are coalesced: entry (r, k) of the pass with span Ns and radix R is (cos, sin)(2 pi r k / (Ns R)),
+// taken from the fp64 table cs (2n doubles) and rounded to fp32.
+size_t stockham_table_len(int n);
+void host_stockham_table(int n, const double* cs, float2* out);
 
 // Host-side exact twiddle table: (cos, sin)(2 pi m / n), m = 0..n-1, computed in fp64 with exact
 // quadrant reduction so that m = 0, n/4, n/2, 3n/4 give exactly 0 / +-1.

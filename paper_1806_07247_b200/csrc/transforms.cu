@@ -87,22 +87,24 @@ __global__ void absmax_q_kernel(const float* __restrict__ X, int64_t P, int64_t 
 // per p per block.  Blocks [nbA, nbA+nbB) reduce B's columns: one warp per contiguous run
 // B(:, j, k) (float4 loads), one atomic per run.
 __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ A, int64_t n1,
-                                                      int64_t colsA, int gyA, int gxA,
+                                                      int64_t colsA, int gyA, int gxA, int txv,
                                                       const float* __restrict__ B, int64_t n2,
                                                       int64_t n4, int64_t n3,
                                                       unsigned* __restrict__ maxA,
                                                       unsigned* __restrict__ maxB) {
   const int nbA = gxA * gyA;
   if ((int)blockIdx.x < nbA) {
-    __shared__ float red[4][257];
+    // A rows: a strip of 4*txv consecutive p (txv float4 lanes) x ty = 256/txv column lanes
+    __shared__ float red[256 * 4 + 256];
+    const int ty_n = 256 / txv, W = 4 * txv + 1;
     const int bx = blockIdx.x % gxA, by = blockIdx.x / gxA;
-    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    const int64_t p = (int64_t)bx * 256 + 4 * tx;
+    const int tx = threadIdx.x % txv, ty = threadIdx.x / txv;
+    const int64_t p = (int64_t)bx * 4 * txv + 4 * tx;
     float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
     if (p < n1) {
       const float4* base = reinterpret_cast<const float4*>(A + p);
-      const int64_t step = (int64_t)gyA * 4;
-      int64_t c = (int64_t)by * 4 + ty;
+      const int64_t step = (int64_t)gyA * ty_n;
+      int64_t c = (int64_t)by * ty_n + ty;
 #pragma unroll 4
       for (; c < colsA; c += step) {
         float4 v = __ldg(base + (c * n1 >> 2));
@@ -112,30 +114,35 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
         m.w = fmaxf(m.w, fabsf(v.w));
       }
     }
-    red[ty][4 * tx] = m.x;
-    red[ty][4 * tx + 1] = m.y;
-    red[ty][4 * tx + 2] = m.z;
-    red[ty][4 * tx + 3] = m.w;
+    red[ty * W + 4 * tx] = m.x;
+    red[ty * W + 4 * tx + 1] = m.y;
+    red[ty * W + 4 * tx + 2] = m.z;
+    red[ty * W + 4 * tx + 3] = m.w;
     __syncthreads();
     const int t = threadIdx.x;
-    const int64_t pt = (int64_t)bx * 256 + t;
-    if (pt < n1) {
-      float r = fmaxf(fmaxf(red[0][t], red[1][t]), fmaxf(red[2][t], red[3][t]));
+    const int64_t pt = (int64_t)bx * 4 * txv + t;
+    if (t < 4 * txv && pt < n1) {
+      float r = 0.f;
+      for (int y = 0; y < ty_n; ++y) r = fmaxf(r, red[y * W + t]);
       atomicMax(maxA + pt, __float_as_uint(r));
     }
   } else {
+    // B columns: warp w owns column j = w mod n4 and the runs B(:, j, k) for k = w / n4 + i * wpc
+    // (wpc warps per column), one atomic per warp
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)(blockIdx.x - nbA) * 256 + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)(gridDim.x - nbA) * 256) >> 5;
-    const int64_t runs = n4 * n3;
-    for (int64_t r = warp; r < runs; r += nwarps) {
-      const int64_t j = r % n4;
-      const float4* x = reinterpret_cast<const float4*>(B + n2 * r);   // run (j,k): offset n2*(j + n4 k)
+    const int64_t wpc = nwarps >= n4 ? nwarps / n4 : 1;
+    for (int64_t w = warp; w < n4 * wpc; w += nwarps) {
+      const int64_t j = w % n4, k0 = w / n4;
       float m = 0.f;
+      for (int64_t k = k0; k < n3; k += wpc) {
+        const float4* x = reinterpret_cast<const float4*>(B + n2 * (j + n4 * k));   // run (j,k)
 #pragma unroll 4
-      for (int64_t l4 = lane; l4 < (n2 >> 2); l4 += 32) {
-        float4 v = __ldg(x + l4);
-        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        for (int64_t l4 = lane; l4 < (n2 >> 2); l4 += 32) {
+          float4 v = __ldg(x + l4);
+          m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
       }
       for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       if (lane == 0) atomicMax(maxB + j, __float_as_uint(m));
@@ -156,17 +163,19 @@ void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int6
   const int64_t total = (int64_t)num_sms * 8;
   int64_t nbA_target = (int64_t)(total * szA / (szA + szB));
   if (nbA_target < 1) nbA_target = 1;
-  const int64_t gxA = (n1 + 255) / 256;
+  int txv = 1;
+  while (txv < 64 && 4 * txv < n1) txv <<= 1;       // float4 lanes across p (narrow A: more column lanes)
+  const int64_t gxA = (n1 + 4 * txv - 1) / (4 * txv);
   const int64_t colsA = n2 * n3;
   int64_t gyA = (nbA_target + gxA - 1) / gxA;
-  const int64_t maxgy = (colsA + 3) / 4;
+  const int64_t maxgy = (colsA + 256 / txv - 1) / (256 / txv);
   if (gyA > maxgy) gyA = maxgy;
   if (gyA < 1) gyA = 1;
   int64_t nbB = total - gxA * gyA;
   const int64_t runsB = n4 * n3;
-  if (nbB > (runsB + 7) / 8) nbB = (runsB + 7) / 8;
+  if (nbB > (runsB + 7) / 8) nbB = (runsB + 7) / 8;      // at most one run per warp
   if (nbB < 1) nbB = 1;
-  absmax2_kernel<<<(unsigned)(gxA * gyA + nbB), 256, 0, s>>>(A, n1, colsA, (int)gyA, (int)gxA, B, n2,
+  absmax2_kernel<<<(unsigned)(gxA * gyA + nbB), 256, 0, s>>>(A, n1, colsA, (int)gyA, (int)gxA, txv, B, n2,
                                                              n4, n3, maxA, maxB);
 }
 
@@ -238,7 +247,7 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
   if (launch_fwd_tma(X, P, Q, n3, role, maxbits, out, ld, unscale, num_sms, s)) return;
   cudaGetLastError();
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
-  if (launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.tw, out, ld, unscale, s)) return;
+  if (tw.st && launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   size_t smem = sizeof(float2) * (size_t)n3;
@@ -308,7 +317,7 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   if (Cim == Cre + Q * ld && fstride == 2 * Q * ld && launch_inv_tma(Cre, ld, P, Q, n3, X, num_sms, s)) return;
   cudaGetLastError();
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, X, s)) return;
-  if (launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.tw, X, s)) return;
+  if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, X, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   inv_kernel<float, float2><<<(unsigned)blocks, threads, sizeof(float2) * n3, s>>>(

@@ -41,6 +41,35 @@ def normal(shape, seed: int, dtype=np.float32) -> np.ndarray:
     return out.reshape(shape, order="F")
 
 
+def normal_lateral(shape, seed: int, j0: int, j1: int, dtype=np.float32) -> np.ndarray:
+    """Lateral slices [j0, j1) of ``normal(shape, seed, dtype)``, without holding the whole tensor.
+
+    The full stream is drawn chunk by chunk in Matlab order (so the values are bit-identical to the
+    corresponding columns of ``normal(shape, seed)``) and only the wanted columns are kept."""
+    n2, n4, n3 = shape
+    w = j1 - j0
+    out = np.empty((n2, w, n3), dtype=dtype, order="F")
+    flat = out.reshape(-1, order="F")                 # view: column-major (i, j - j0, k)
+    rng = np.random.default_rng(seed)
+    slab = n2 * n4                                    # one frontal slice of the stream
+    lo, hi = n2 * j0, n2 * j1                         # wanted window inside each slice
+    pos = 0                                           # stream position
+    total = slab * n3
+    while pos < total:
+        e = min(total, pos + _CHUNK)
+        vals = rng.standard_normal(e - pos).astype(dtype)
+        # copy the part of [pos, e) that falls in the window of each slice it touches
+        k0, k1 = pos // slab, (e - 1) // slab
+        for k in range(k0, k1 + 1):
+            a = max(pos, k * slab + lo)
+            b = min(e, k * slab + hi)
+            if a < b:
+                d = k * n2 * w + (a - k * slab - lo)
+                flat[d:d + (b - a)] = vals[a - pos:b - pos]
+        pos = e
+    return out
+
+
 def lateral_shard(n4: int, world: int, rank: int) -> tuple[int, int]:
     """Balanced contiguous block [start, stop) of lateral slices owned by ``rank``.
 

@@ -119,19 +119,19 @@ def test_simt_engine_cross_check(T):
 @pytest.mark.parametrize("dims", [(300, 260, 31, 200), (1000, 136, 3, 700), (129, 64, 7, 129)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
-    """GEMM N tile (64/128) and 2-CTA A-multicast clusters change scheduling only: the K order of
-    every output is fixed, so all variants are bitwise identical (odd N-tile counts included)."""
+    """GEMM N tile (64/128), 2-CTA A-multicast clusters and cta_group::2 CTA pairs (256-row tiles
+    across two SMs) change scheduling only: the K order of every output is fixed, so all variants
+    are bitwise identical (odd N-tile counts and a lone 128-row half-pair included)."""
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 11)
     B = normal((n2, n4, n3), 12)
     ref = O.tprod_bcirc(A, B)
     outs = []
-    for bn in (64, 128):
-        for cn in (1, 2):
-            h = T.Handle()
-            h.set_option(T._lib.TPROD_OPT_GEMM_BN, bn)
-            h.set_option(T._lib.TPROD_OPT_GEMM_CLUSTER, cn)
-            outs.append(gpu_tprod(T, A, B, handle=h))
+    for bn, cn in ((64, 1), (64, 2), (128, 1), (128, 2), (128, 3), (0, 0)):
+        h = T.Handle()
+        h.set_option(T._lib.TPROD_OPT_GEMM_BN, bn)
+        h.set_option(T._lib.TPROD_OPT_GEMM_CLUSTER, cn)
+        outs.append(gpu_tprod(T, A, B, handle=h))
     assert O.rel_err(outs[0], ref) <= TOL32
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
