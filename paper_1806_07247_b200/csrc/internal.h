@@ -87,16 +87,17 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, float* X, cudaStream_t s);
 
-// In-smem radix-16 Stockham FFT transforms for power-of-two 64 < n3 <= 16384 (transforms_fft.cu).
+// In-smem mixed-radix (16/8/4/2, 3, 5) Stockham FFT transforms for 5-smooth 64 < n3 <= 16384
+// (transforms_fft.cu).
 // `st` is the Stockham table of host_stockham_table (device copy).
 bool fft_supported(int64_t n3);
 bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s);
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
                     int64_t n3, const float2* st, float* X, cudaStream_t s);
-// Per-pass twiddles of the radix-16 Stockham FFT, laid out [pass][r-1][k] so that a warp's lookups
-// are coalesced: entry (r, k) of the pass with span Ns and radix R is (cos, sin)(2 pi r k / (Ns R)),
-// taken from the fp64 table cs (2n doubles) and rounded to fp32.
+// Per-pass twiddles of the mixed-radix Stockham FFT, laid out [pass][r-1][k] so that a warp's
+// lookups are coalesced: entry (r, k) of the pass with span Ns and radix R is
+// (cos, sin)(2 pi r k / (Ns R)), taken from the fp64 table cs (2n doubles) and rounded to fp32.
 size_t stockham_table_len(int n);
 void host_stockham_table(int n, const double* cs, float2* out);
 

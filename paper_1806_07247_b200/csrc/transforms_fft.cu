@@ -1,6 +1,7 @@
-// Long-tube mode-3 transforms (power-of-two 64 < n3 <= 16384, e.g. config 4's n3 = 4096):
-// in-shared-memory Stockham FFT, O(n3 log n3) per tube, radix-16 passes with the
-// 16-point DFTs held in registers (a final radix-8/4/2 pass when log2 n3 is not a multiple of 4).
+// Long-tube mode-3 transforms (5-smooth 64 < n3 <= 16384, e.g. config 4's n3 = 4096): in-shared-
+// memory mixed-radix Stockham FFT, O(n3 log n3) per tube (the mixed radix-2/3/5
+// decomposition of the north star), radix-16 passes while the power-of-two part allows, then
+// radix 8/4/2, then radix 3 and radix 5 passes, each R-point DFT held in registers.
 //
 // Two real tubes x, y share one complex FFT z = x + i y (real-input packing):
 //   forward  (Alg. 1 step 1, L174):  X_f = (Z_f + conj Z_{N-f}) / 2,  Y_f = (Z_f - conj Z_{N-f}) / (2i),
@@ -9,34 +10,80 @@
 //   inverse  (Alg. 1 step 2b + 3, L177-179): the conjugate fill X_{N-f} = conj X_f is built while
 //            loading (Im of DC/Nyquist dropped), Z = X + i Y, z = IFFT(Z) (sign +, 1/N), x = Re z,
 //            y = Im z.
-// A CTA (512 threads) owns TUB = 2F consecutive tubes, F complex FFTs of N points with F*N = 16384
-// (128 KB of data + 1/16 bank padding), so every global row access touches TUB consecutive
+// A CTA owns TUB = 2F consecutive tubes, F = the largest power of two with F*N <= 16384 complex
+// FFTs (<= 128 KB of data + 1/16 bank padding), so every global row access touches TUB consecutive
 // elements of the contiguous dimension (float4-vectorised when aligned).
 //
-// Stockham pass (radix R, current span Ns), butterfly j in [0, N/R):
-//   v[r] = z[j + r N/R] * w_N^{r k N/(Ns R)},  k = j mod Ns;   v = DFT_R(v);
+// Stockham pass (radix R, span Ns = product of the earlier radices), butterfly j in [0, N/R):
+//   v[r] = z[j + r N/R] * w_{Ns R}^{r k},  k = j mod Ns;   v = DFT_R(v);
 //   z[(j - k) R + k + r Ns] = v[r]
 // Every thread loads all of its butterflies into registers, the CTA synchronises, then writes
-// (in place).  Output is in natural order.  Twiddles come from the handle's fp64-derived table
-// (exact quadrant reduction), read through L1; the DFT_R constants are fp64 literals rounded to fp32.
+// (in place).  Output is in natural order.  Twiddles w_{Ns R}^{r k} come from a per-pass table
+// laid out [pass][r-1][k] (coalesced for consecutive k) built from the handle's fp64 table with
+// exact quadrant reduction; the DFT_R constants are fp64 literals rounded to fp32.
 #include "internal.h"
 #include "common.cuh"
+
+#include <vector>
 
 namespace tprod {
 
 namespace {
 
-constexpr int FFT_POINTS = 16384;        // complex points held in smem per CTA (128 KB)
+constexpr int FFT_POINTS = 16384;      // complex points held in smem per CTA (128 KB)
 constexpr int FFT_THREADS = 512;       // forward kernel
 constexpr int IFFT_THREADS = 1024;     // inverse kernel (measured: 512 better for K1, 1024 for K3)
+constexpr int MAX_PASSES = 16;
+
+// Radix plan of N: radix-16 passes, one radix 8/4/2 pass for the rest of the power of two, then
+// radix-3 and radix-5 passes.  Ns[i] = product of R[0..i-1]; toff[i] = offset of pass i's twiddle
+// table ((R - 1) Ns entries, none for Ns = 1).
+struct FftPlan {
+  int np;
+  int R[MAX_PASSES];
+  int Ns[MAX_PASSES];
+  int toff[MAX_PASSES];
+};
+
+bool make_plan(int n, FftPlan* pl) {
+  if (n < 1) return false;
+  int m = n, a = 0;
+  while (m % 2 == 0) { m /= 2; ++a; }
+  int b = 0, c = 0;
+  while (m % 3 == 0) { m /= 3; ++b; }
+  while (m % 5 == 0) { m /= 5; ++c; }
+  if (m != 1) return false;
+  std::vector<int> rs;
+  while (a >= 4) { rs.push_back(16); a -= 4; }
+  if (a > 0) rs.push_back(1 << a);
+  for (int i = 0; i < b; ++i) rs.push_back(3);
+  for (int i = 0; i < c; ++i) rs.push_back(5);
+  if ((int)rs.size() > MAX_PASSES) return false;
+  pl->np = (int)rs.size();
+  int Ns = 1, off = 0;
+  for (int i = 0; i < pl->np; ++i) {
+    pl->R[i] = rs[i];
+    pl->Ns[i] = Ns;
+    pl->toff[i] = off;
+    if (Ns > 1) off += (rs[i] - 1) * Ns;
+    Ns *= rs[i];
+  }
+  return true;
+}
+
+int fft_F(int n) {             // complex FFTs per CTA: largest power of two with F * n <= FFT_POINTS
+  int F = 1;
+  while (2 * F * n <= FFT_POINTS) F *= 2;
+  return F;
+}
 
 // padded smem index: one float2 of padding per 16 (breaks the radix-16 store stride)
-__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
-__host__ __device__ constexpr int padded_len(int n) { return n + n / 16; }
+__host__ __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 // float2 stride between the F buffers of a CTA: the padded length rounded to 16, plus 16/F (>= 1)
 // so that the F buffers of a half-warp's (f, c) items start in different banks
-__host__ __device__ constexpr int bstride(int n) {
-  return (padded_len(n) + 15) / 16 * 16 + ((16 * n / FFT_POINTS) > 1 ? 16 * n / FFT_POINTS : 1);
+__host__ __device__ __forceinline__ int bstride(int n, int F) {
+  const int pl = n + n / 16 + 1;
+  return (pl + 15) / 16 * 16 + (16 / F > 1 ? 16 / F : 1);
 }
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -44,11 +91,12 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 mul_i(float2 a) { return make_float2(-a.y, a.x); }   // i * a
 
-// w_M^i = exp(DIR * 2 pi i * i / M) for M <= 16, DIR = -1 forward / +1 inverse
+// w_M^i = exp(DIR * 2 pi i * i / M) for M | 16, DIR = -1 forward / +1 inverse
 template <int DIR>
 __device__ __forceinline__ float2 wconst(int M, int i) {
-  // cos / sin of 2 pi i / M for M | 16, from fp64 literals (compile-time after unrolling)
   constexpr double C16[16] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977,
                               0.0, -0.38268343236508977, -0.70710678118654752, -0.92387953251128674,
                               -1.0, -0.92387953251128674, -0.70710678118654752, -0.38268343236508977,
@@ -59,38 +107,63 @@ __device__ __forceinline__ float2 wconst(int M, int i) {
   return make_float2(c, DIR < 0 ? -s : s);
 }
 
-// In-register DFT of R = 2^m points (radix-2 DIF, bit-reversed result reordered by renaming).
+// In-register DFT of R points, natural order in and out.
 template <int R, int DIR>
 __device__ __forceinline__ void dft_reg(float2 (&v)[R]) {
+  if constexpr (R == 3) {
+    const float c = -0.5f, s = (float)(DIR * 0.86602540378443865);      // w_3 = c + i s
+    const float2 t1 = cadd(v[1], v[2]), d = csub(v[1], v[2]);
+    const float2 m = make_float2(v[0].x + c * t1.x, v[0].y + c * t1.y);
+    const float2 id = mul_i(cscale(d, s));
+    v[0] = cadd(v[0], t1);
+    v[1] = cadd(m, id);
+    v[2] = csub(m, id);
+  } else if constexpr (R == 5) {
+    const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
+    const float s1 = (float)(DIR * 0.95105651629515357), s2 = (float)(DIR * 0.58778525229247313);
+    const float2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+    const float2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+    const float2 m1 = make_float2(v[0].x + c1 * a1.x + c2 * a2.x, v[0].y + c1 * a1.y + c2 * a2.y);
+    const float2 m2 = make_float2(v[0].x + c2 * a1.x + c1 * a2.x, v[0].y + c2 * a1.y + c1 * a2.y);
+    const float2 n1 = mul_i(make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
+    const float2 n2 = mul_i(make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
+    v[0] = cadd(v[0], cadd(a1, a2));
+    v[1] = cadd(m1, n1);
+    v[4] = csub(m1, n1);
+    v[2] = cadd(m2, n2);
+    v[3] = csub(m2, n2);
+  } else {
+    // R = 2^m: radix-2 DIF, bit-reversed result reordered by renaming
 #pragma unroll
-  for (int half = R / 2; half >= 1; half >>= 1) {
+    for (int half = R / 2; half >= 1; half >>= 1) {
 #pragma unroll
-    for (int blk = 0; blk < R; blk += 2 * half) {
+      for (int blk = 0; blk < R; blk += 2 * half) {
 #pragma unroll
-      for (int i = 0; i < half; ++i) {
-        const float2 a = v[blk + i], b = v[blk + i + half];
-        v[blk + i] = cadd(a, b);
-        const float2 d = csub(a, b);
-        if (i == 0) {
-          v[blk + i + half] = d;
-        } else if (4 * i == 2 * half) {            // w = -+i
-          v[blk + i + half] = DIR < 0 ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);
-        } else {
-          v[blk + i + half] = cmul(d, wconst<DIR>(2 * half, i));
+        for (int i = 0; i < half; ++i) {
+          const float2 a = v[blk + i], b = v[blk + i + half];
+          v[blk + i] = cadd(a, b);
+          const float2 d = csub(a, b);
+          if (i == 0) {
+            v[blk + i + half] = d;
+          } else if (4 * i == 2 * half) {            // w = -+i
+            v[blk + i + half] = DIR < 0 ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);
+          } else {
+            v[blk + i + half] = cmul(d, wconst<DIR>(2 * half, i));
+          }
         }
       }
     }
+    float2 t[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      int r = 0;
+#pragma unroll
+      for (int b = 1; b < R; b <<= 1) r = (r << 1) | ((k & b) ? 1 : 0);   // bit reversal of k
+      t[k] = v[r];
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = t[k];
   }
-  float2 t[R];
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    int r = 0;
-#pragma unroll
-    for (int b = 1; b < R; b <<= 1) r = (r << 1) | ((k & b) ? 1 : 0);   // bit reversal of k
-    t[k] = v[r];
-  }
-#pragma unroll
-  for (int k = 0; k < R; ++k) v[k] = t[k];
 }
 
 // table twiddle (cos, DIR*sin)
@@ -100,75 +173,108 @@ __device__ __forceinline__ float2 twN(const float2* __restrict__ tw, int m) {
   return make_float2(t.x, DIR < 0 ? -t.y : t.y);
 }
 
-// One Stockham pass of radix R over all F buffers (F*N = FFT_POINTS).
+// Largest F * N / R over the N this file handles (F * N <= 16384).
+template <int R>
+__host__ __device__ constexpr int max_butterflies() {
+  return FFT_POINTS / R;
+}
+
+// Butterfly b of a pass -> (buffer c, butterfly j of that FFT, group g = j / Ns, k = j mod Ns).
+// Power-of-two N uses shifts, other N integer division.
+struct PassIdx {
+  int c, j, g, k;
+};
+__device__ __forceinline__ PassIdx pass_idx(int b, int NB, int Ns, int lognb, int logns) {
+  PassIdx x;
+  if (lognb >= 0) {
+    x.c = b >> lognb;
+    x.j = b & (NB - 1);
+    x.g = x.j >> logns;
+    x.k = x.j & (Ns - 1);
+  } else {
+    x.c = b / NB;
+    x.j = b - x.c * NB;
+    x.g = x.j / Ns;
+    x.k = x.j - x.g * Ns;
+  }
+  return x;
+}
+
+// One Stockham pass of radix R over all F buffers (buffer stride Np).  lognb / logns are log2 of
+// N/R and Ns when N is a power of two, else -1.
 template <int R, int DIR, int NT>
-__device__ __forceinline__ void stockham_pass(float2* z, int N, int logN, int Ns, int logNs,
+__device__ __forceinline__ void stockham_pass(float2* z, int N, int F, int Np, int Ns, int lognb, int logns,
                                               const float2* __restrict__ tp) {
-  constexpr int BPT = FFT_POINTS / R / NT;            // butterflies per thread
-  const int logR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
-  const int nb_log = logN - logR;                     // log2(N / R)
-  const int Np = bstride(N);
+  constexpr int BPT = (max_butterflies<R>() + NT - 1) / NT;   // butterflies per thread (upper bound)
+  const int NB = N / R;                                        // butterflies per FFT
+  const int total = F * NB;
   float2 v[BPT][R];
-  int dst[BPT], cb[BPT];
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
-    const int b = threadIdx.x + u * NT;
-    const int c = b >> nb_log, j = b & ((1 << nb_log) - 1);
-    const int k = j & (Ns - 1);
-    float2* zc = z + c * Np;
+    // past-the-end butterflies redo the last one (registers stay unconditionally defined; their
+    // results are not stored)
+    const int b = min((int)threadIdx.x + u * NT, total - 1);
+    {
+      const PassIdx x = pass_idx(b, NB, Ns, lognb, logns);
+      const float2* zc = z + x.c * Np;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[u][r] = zc[pad(j + (r << nb_log))];
-    if (Ns > 1) {
-      // w_{Ns R}^{r k} = tp[(r - 1) Ns + k]: consecutive k of a warp read consecutive entries
+      for (int r = 0; r < R; ++r) v[u][r] = zc[pad(x.j + r * NB)];
+      if (Ns > 1) {
+        // w_{Ns R}^{r k} = tp[(r - 1) Ns + k]: consecutive k of a warp read consecutive entries
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twN<DIR>(tp, (r - 1) * Ns + k));
+        for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twN<DIR>(tp, (r - 1) * Ns + x.k));
+      }
+      dft_reg<R, DIR>(v[u]);
     }
-    dft_reg<R, DIR>(v[u]);
-    cb[u] = c * Np;
-    dst[u] = ((j - k) << logR) + k;
   }
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
+    const int b = threadIdx.x + u * NT;
+    if (b < total) {
+      const PassIdx x = pass_idx(b, NB, Ns, lognb, logns);
+      float2* zc = z + x.c * Np;
+      const int d0 = x.g * Ns * R + x.k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) z[cb[u] + pad(dst[u] + r * Ns)] = v[u][r];
+      for (int r = 0; r < R; ++r) zc[pad(d0 + r * Ns)] = v[u][r];
+    }
   }
   __syncthreads();
 }
 
-// Passes: radix 16 while >= 4 bits remain, then one radix 8/4/2 pass.  The table of the pass with
-// span Ns > 1 and radix R starts after those of the earlier passes (Ns' R' - Ns' entries each).
 template <int DIR, int NT>
-__device__ void fft_smem(float2* z, int N, int logN, const float2* __restrict__ st) {
-  int Ns = 1, logNs = 0;
-  const float2* tp = st;
-  while (logN - logNs >= 4) {
-    stockham_pass<16, DIR, NT>(z, N, logN, Ns, logNs, tp);
-    if (Ns > 1) tp += 15 * Ns;
-    Ns <<= 4;
-    logNs += 4;
+__device__ void fft_smem(float2* z, int N, int F, int Np, const FftPlan& pl, const float2* __restrict__ st) {
+  const bool p2 = (N & (N - 1)) == 0;
+  for (int i = 0; i < pl.np; ++i) {
+    const float2* tp = st + pl.toff[i];
+    const int R = pl.R[i], Ns = pl.Ns[i];
+    const int lognb = p2 ? __ffs(N / R) - 1 : -1, logns = p2 ? __ffs(Ns) - 1 : -1;
+    switch (R) {
+      case 16: stockham_pass<16, DIR, NT>(z, N, F, Np, Ns, lognb, logns, tp); break;
+      case 8: stockham_pass<8, DIR, NT>(z, N, F, Np, Ns, lognb, logns, tp); break;
+      case 4: stockham_pass<4, DIR, NT>(z, N, F, Np, Ns, lognb, logns, tp); break;
+      case 2: stockham_pass<2, DIR, NT>(z, N, F, Np, Ns, lognb, logns, tp); break;
+      case 3: stockham_pass<3, DIR, NT>(z, N, F, Np, Ns, -1, -1, tp); break;
+      default: stockham_pass<5, DIR, NT>(z, N, F, Np, Ns, -1, -1, tp); break;
+    }
   }
-  const int rem = logN - logNs;
-  if (rem == 3) stockham_pass<8, DIR, NT>(z, N, logN, Ns, logNs, tp);
-  else if (rem == 2) stockham_pass<4, DIR, NT>(z, N, logN, Ns, logNs, tp);
-  else if (rem == 1) stockham_pass<2, DIR, NT>(z, N, logN, Ns, logNs, tp);
 }
 
 template <int ROLE>
 __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
-    const float* __restrict__ X, int64_t P, int64_t Q, int N, int logN,
+    const float* __restrict__ X, int64_t P, int64_t Q, int N, int F, const __grid_constant__ FftPlan pl,
     const unsigned* __restrict__ maxbits, const float2* __restrict__ st, __half* __restrict__ out,
     int64_t ld, float* __restrict__ unscale, int vec) {
   extern __shared__ float2 z[];
-  const int F = FFT_POINTS >> logN, TUB = 2 * F;
-  const int Np = bstride(N);
+  const int TUB = 2 * F;
+  const int Np = bstride(N, F);
   const int64_t pblocks = (P + TUB - 1) / TUB;
   const int64_t q = blockIdx.x / pblocks;
   const int64_t p0 = (blockIdx.x - q * pblocks) * TUB;
   const int64_t PQ = P * Q;
   const float* x = X + P * q + p0;
   // ---- load: tube t = p0 + t, element k -> buffer t/2, real (t even) / imaginary (t odd) part
-  if (vec) {   // TUB % 4 == 0, P % 4 == 0, 16-byte aligned, full block
+  if (vec) {   // TUB % 4 == 0, P % TUB == 0, 16-byte aligned
     const int V = TUB >> 2;                         // float4 per row
     const int total = V * N;
 #pragma unroll 8
@@ -186,7 +292,7 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
     }
   }
   __syncthreads();
-  fft_smem<-1, FFT_THREADS>(z, N, logN, st);
+  fft_smem<-1, FFT_THREADS>(z, N, F, Np, pl, st);
   // ---- Hermitian half, real-pair separation, 2^e scaling, fp16 hi/lo split
   const int H = N / 2 + 1;
   const int64_t plane = Q * ld;
@@ -209,11 +315,11 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
     }
   }
   const float s0 = pow2f(e0), s1 = pow2f(e1);
+  if (p >= P) return;
   for (int idx = threadIdx.x; idx < H * F; idx += FFT_THREADS) {
     const int f = idx / F;
-    if (p >= P) break;
     const float2 zf = z[c * Np + pad(f)];
-    const float2 zm = z[c * Np + pad((N - f) & (N - 1))];
+    const float2 zm = z[c * Np + pad(f == 0 ? 0 : N - f)];
     // X_f = (Z_f + conj Z_{N-f}) / 2 ;  Y_f = (Z_f - conj Z_{N-f}) / (2i)
     const float xr = 0.5f * (zf.x + zm.x), xi = 0.5f * (zf.y - zm.y);
     const float yr = 0.5f * (zf.y + zm.y), yi = -0.5f * (zf.x - zm.x);
@@ -244,14 +350,14 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
 }
 
 __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* __restrict__ Cre,
-                                                                const float* __restrict__ Cim, int64_t ld,
-                                                                int64_t fstride, int64_t P, int64_t Q,
-                                                                int N, int logN,
-                                                                const float2* __restrict__ st,
-                                                                float* __restrict__ X, int vec) {
+                                                                 const float* __restrict__ Cim, int64_t ld,
+                                                                 int64_t fstride, int64_t P, int64_t Q,
+                                                                 int N, int F, const __grid_constant__ FftPlan pl,
+                                                                 const float2* __restrict__ st,
+                                                                 float* __restrict__ X, int vec) {
   extern __shared__ float2 z[];
-  const int F = FFT_POINTS >> logN, TUB = 2 * F;
-  const int Np = bstride(N);
+  const int TUB = 2 * F;
+  const int Np = bstride(N, F);
   const int64_t pblocks = (P + TUB - 1) / TUB;
   const int64_t q = blockIdx.x / pblocks;
   const int64_t p0 = (blockIdx.x - q * pblocks) * TUB;
@@ -276,7 +382,7 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
     if (!self) z[c * Np + pad(N - f)] = make_float2(xr + yi, yr - xi);  // conj X_f + i conj Y_f
   }
   __syncthreads();
-  fft_smem<+1, IFFT_THREADS>(z, N, logN, st);
+  fft_smem<+1, IFFT_THREADS>(z, N, F, Np, pl, st);
   const float inv_n = 1.f / (float)N;
   const int64_t PQ = P * Q;
   float* xo = X + P * q + p0;
@@ -299,13 +405,10 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
   }
 }
 
-int ilog2(int64_t n) {
-  int l = 0;
-  while ((int64_t(1) << l) < n) ++l;
-  return l;
+size_t fft_smem_bytes(int N) {
+  const int F = fft_F(N);
+  return sizeof(float2) * (size_t)F * bstride(N, F);
 }
-
-size_t fft_smem_bytes(int N) { return sizeof(float2) * (size_t)(FFT_POINTS / N) * bstride(N); }
 
 bool fft_smem_ok(const void* kern, int N) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem_bytes(N)) ==
@@ -315,46 +418,40 @@ bool fft_smem_ok(const void* kern, int N) {
 }  // namespace
 
 size_t stockham_table_len(int n) {
-  size_t len = 0;
-  int Ns = 1;
-  int rem = 0;
-  while ((1 << rem) < n) ++rem;          // log2 n
-  while (rem > 0) {
-    const int R = rem >= 4 ? 16 : (1 << rem);
-    if (Ns > 1) len += (size_t)(R - 1) * Ns;
-    Ns *= R;
-    rem -= rem >= 4 ? 4 : rem;
-  }
-  return len;
+  FftPlan pl;
+  if (!make_plan(n, &pl)) return 0;
+  const int last = pl.np - 1;
+  if (last < 0) return 0;
+  return (size_t)pl.toff[last] + (pl.Ns[last] > 1 ? (size_t)(pl.R[last] - 1) * pl.Ns[last] : 0);
 }
 
 void host_stockham_table(int n, const double* cs, float2* out) {
-  int Ns = 1, rem = 0;
-  while ((1 << rem) < n) ++rem;
-  size_t o = 0;
-  while (rem > 0) {
-    const int R = rem >= 4 ? 16 : (1 << rem);
-    if (Ns > 1) {
-      for (int r = 1; r < R; ++r)
-        for (int k = 0; k < Ns; ++k) {
-          const long long m = (long long)r * k * (n / (Ns * R));   // w_{Ns R}^{r k} = w_n^m, m < n
-          out[o++] = make_float2((float)cs[2 * m], (float)cs[2 * m + 1]);
-        }
-    }
-    Ns *= R;
-    rem -= rem >= 4 ? 4 : rem;
+  FftPlan pl;
+  if (!make_plan(n, &pl)) return;
+  for (int i = 0; i < pl.np; ++i) {
+    const int R = pl.R[i], Ns = pl.Ns[i];
+    if (Ns == 1) continue;
+    float2* o = out + pl.toff[i];
+    for (int r = 1; r < R; ++r)
+      for (int k = 0; k < Ns; ++k) {
+        const long long m = (long long)r * k * (n / (Ns * R));   // w_{Ns R}^{r k} = w_n^m, m < n
+        o[(size_t)(r - 1) * Ns + k] = make_float2((float)cs[2 * m], (float)cs[2 * m + 1]);
+      }
   }
 }
 
 bool fft_supported(int64_t n3) {
-  return n3 > 64 && n3 <= FFT_POINTS && (n3 & (n3 - 1)) == 0;
+  FftPlan pl;
+  return n3 > 64 && n3 <= FFT_POINTS && make_plan((int)n3, &pl);
 }
 
 bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s) {
   if (!fft_supported(n3)) return false;
-  const int N = (int)n3, logN = ilog2(n3);
-  const int TUB = 2 * (FFT_POINTS / N);
+  FftPlan pl;
+  make_plan((int)n3, &pl);
+  const int N = (int)n3, F = fft_F(N);
+  const int TUB = 2 * F;
   const size_t smem = fft_smem_bytes(N);
   const int64_t blocks = (P + TUB - 1) / TUB * Q;
   // vectorised loads need every block full and 16-byte aligned rows
@@ -362,10 +459,10 @@ bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
   const void* k = role == 0 ? (const void*)fft_fwd_split_kernel<0> : (const void*)fft_fwd_split_kernel<1>;
   if (!fft_smem_ok(k, N)) return false;
   if (role == 0)
-    fft_fwd_split_kernel<0><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, logN, maxbits, st, out, ld,
+    fft_fwd_split_kernel<0><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, F, pl, maxbits, st, out, ld,
                                                                        unscale, vec);
   else
-    fft_fwd_split_kernel<1><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, logN, maxbits, st, out, ld,
+    fft_fwd_split_kernel<1><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, F, pl, maxbits, st, out, ld,
                                                                        unscale, vec);
   return cudaGetLastError() == cudaSuccess;
 }
@@ -373,15 +470,17 @@ bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
                     int64_t n3, const float2* st, float* X, cudaStream_t s) {
   if (!fft_supported(n3)) return false;
-  const int N = (int)n3, logN = ilog2(n3);
-  const int TUB = 2 * (FFT_POINTS / N);
+  FftPlan pl;
+  make_plan((int)n3, &pl);
+  const int N = (int)n3, F = fft_F(N);
+  const int TUB = 2 * F;
   const size_t smem = fft_smem_bytes(N);
   const int64_t blocks = (P + TUB - 1) / TUB * Q;
   // paired float2 loads of C-bar need both tubes of every pair in range and 8-byte alignment
   const int vec = (P % TUB == 0) && (ld % 2 == 0) && (fstride % 2 == 0) && (((uintptr_t)Cre) & 7) == 0 &&
                   (((uintptr_t)Cim) & 7) == 0;
   if (!fft_smem_ok((const void*)fft_inv_kernel, N)) return false;
-  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, logN, st, X, vec);
+  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, F, pl, st, X, vec);
   return cudaGetLastError() == cudaSuccess;
 }
 

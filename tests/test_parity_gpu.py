@@ -82,6 +82,7 @@ SWEEP = [
     (255, 129, 31, 257), (128, 256, 32, 128), (300, 260, 31, 200), (40, 50, 64, 30),
     (200, 136, 3, 264), (8, 1000, 2, 8), (1000, 8, 2, 3),
     (33, 17, 128, 9), (64, 40, 512, 20), (10, 7, 2048, 5), (70, 30, 100, 40),
+    (33, 17, 240, 9), (20, 12, 375, 7), (16, 16, 1536, 16),
 ]
 
 
@@ -138,7 +139,8 @@ def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
 
 
 # ------------------------------------------------------------------------------- stages
-@pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 65, 100, 128, 256, 2048, 4096, 8192])
+@pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 65, 96, 100, 120, 128, 256, 375, 1000, 1536,
+                                2048, 4096, 6000, 8192, 15360])
 def test_stage_forward_dft(T, n3):
     """S1/S2 vs numpy.fft.rfft (library special case), both operand roles."""
     p, q = (37, 5) if n3 > 64 else (133, 9)
@@ -150,7 +152,8 @@ def test_stage_forward_dft(T, n3):
         assert err < 2e-6, (role, err)
 
 
-@pytest.mark.parametrize("n3", [1, 2, 7, 31, 32, 64, 100, 128, 512, 4096, 8192])
+@pytest.mark.parametrize("n3", [1, 2, 7, 31, 32, 64, 96, 100, 128, 375, 512, 1000, 4096, 6000, 8192,
+                                15360])
 def test_stage_inverse_roundtrip(T, n3):
     """S4(S1(X)) = X and the 1x1xn3 circular-convolution worked example."""
     import torch
