@@ -128,7 +128,11 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
 /* Options (tests / benchmarking).  TPROD_OPT_ENGINE: 0 = auto (tcgen05), 1 = SIMT reference
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
-enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4 };
+enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
+       TPROD_OPT_TRANSFORM = 5 };
+/* TPROD_OPT_TRANSFORM (fp32 path): 0 = auto (TMA-staged / tube-parallel transform kernels where
+ * they apply), 1 = register-resident transform kernels only.  Same arithmetic up to rounding
+ * order of the DFT sums (both within the stage tolerances). */
 /* TPROD_OPT_GEMM_CLUSTER: 0 = auto, 1 = independent CTAs, 2 = 2-CTA clusters along N sharing the
  * A tile by TMA multicast, 3 = CTA pairs issuing tcgen05.mma.cta_group::2 (256 x 128 tiles over two
  * SMs; requires the 128 N tile).  None of the options changes the arithmetic (results are bitwise

@@ -35,6 +35,7 @@ struct tprod_ctx {
   int engine = 0;
   int force_bn = 0;
   int force_cn = 0;
+  int transform = 0;   // TPROD_OPT_TRANSFORM
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
   bool timing = false;
@@ -171,7 +172,7 @@ int get_twiddles32(tprod_ctx* h, int n3, Twiddles32* T) {
   int st = get_tw32(h, n3, &tw);
   if (st) return st;
   *T = Twiddles32{tw, n3, nullptr};
-  if (!fft_supported(n3)) return TPROD_OK;
+  if (!fft_supported(n3) && !tube_supported(n3)) return TPROD_OK;
   auto it = h->st32.find(n3);
   if (it != h->st32.end()) { T->st = it->second; return TPROD_OK; }
   std::vector<double> cs(2 * (size_t)n3);
@@ -237,6 +238,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   if (st) return st;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
   char* ws = (char*)h->ws;
   unsigned* maxA = (unsigned*)(ws + L.off_maxA);
   unsigned* maxB = (unsigned*)(ws + L.off_maxB);
@@ -522,6 +524,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
     case TPROD_OPT_GEMM_CLUSTER:
       if (value < 0 || value > 3) return TPROD_EINVAL;
       h->force_cn = (int)value;
+      return TPROD_OK;
+    case TPROD_OPT_TRANSFORM:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->transform = (int)value;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:
       if (value != 0 && value != 64 && value != 128) return TPROD_EINVAL;

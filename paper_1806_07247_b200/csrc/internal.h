@@ -22,6 +22,7 @@ struct Twiddles32 {
   const float2* tw;              // tw[m] = (cos 2pi m/n3, sin 2pi m/n3)
   int n3;
   const float2* st = nullptr;    // Stockham per-pass twiddle table (FFT path only), see transforms_fft.cu
+  int staged = 1;                // 0: skip the TMA-staged / tube kernels (TPROD_OPT_TRANSFORM = 1)
 };
 struct Twiddles64 { const double2* tw; int n3; };
 
@@ -68,6 +69,15 @@ bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
                     __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
 bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
                     cudaStream_t s);
+
+// Tube-parallel TMA-staged Stockham transforms for power-of-two 32 <= n3 <= 256 (transforms_tma.cu);
+// `st` = Stockham table of host_stockham_table.  false = not handled.  The inverse requires C-bar
+// in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld).
+bool tube_supported(int64_t n3);
+bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                     const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
+bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
+                     int num_sms, cudaStream_t s);
 
 // ------------------------------------------------------------------ fp64 path
 // spectra as fp64 planes [f][re|im][q][ld]

@@ -244,8 +244,12 @@ __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t
 void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
                       float* unscale, int num_sms, cudaStream_t s) {
-  if (launch_fwd_tma(X, P, Q, n3, role, maxbits, out, ld, unscale, num_sms, s)) return;
-  cudaGetLastError();
+  if (tw.staged) {
+    if (launch_fwd_tma(X, P, Q, n3, role, maxbits, out, ld, unscale, num_sms, s)) return;
+    cudaGetLastError();
+    if (launch_fwd_tube(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, num_sms, s)) return;
+    cudaGetLastError();
+  }
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
   if (tw.st && launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
   const int threads = 128;
@@ -314,7 +318,10 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
 
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                     int64_t Q, int64_t n3, Twiddles32 tw, float* X, int num_sms, cudaStream_t s) {
-  if (Cim == Cre + Q * ld && fstride == 2 * Q * ld && launch_inv_tma(Cre, ld, P, Q, n3, X, num_sms, s)) return;
+  const bool prod_layout = tw.staged && Cim == Cre + Q * ld && fstride == 2 * Q * ld;
+  if (prod_layout && launch_inv_tma(Cre, ld, P, Q, n3, X, num_sms, s)) return;
+  cudaGetLastError();
+  if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, X, num_sms, s)) return;
   cudaGetLastError();
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, X, s)) return;
   if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, X, s)) return;

@@ -15,6 +15,7 @@
 // K3: Alg. 1 step 2 second branch + step 3 (L177-179): fused conjugate fill + inverse DFT.
 #include "internal.h"
 #include "common.cuh"
+#include "fft_reg.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -57,20 +58,21 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t*
 struct Item {
   int64_t q, p0;
 };
+template <int TPI = TP>
 __device__ __forceinline__ Item item_of(int64_t it, int64_t pblocks) {
   Item r;
   r.q = it / pblocks;
-  r.p0 = (it - r.q * pblocks) * TP;
+  r.p0 = (it - r.q * pblocks) * TPI;
   return r;
 }
 
 // Persistent double-buffered TMA pipeline shared by K1 and K3: calls body(item, smem buffer) for
-// every work item of this CTA.  BUF = floats per buffer; box = {TP, 1, rows}.
-template <int BUF, typename Body>
+// every work item of this CTA.  BUF = floats per buffer; box = {TPI, 1, rows} (TPI tubes per item).
+template <int BUF, int TPI = TP, typename Body>
 __device__ __forceinline__ void tma_pipeline(const CUtensorMap* m, int64_t P, int64_t Q, float* smem,
                                              uint64_t* full, Body&& body) {
   const int tid = threadIdx.x;
-  const int64_t pblocks = (P + TP - 1) / TP;
+  const int64_t pblocks = (P + TPI - 1) / TPI;
   const int64_t items = pblocks * Q;
   if (tid == 0) {
     bar_init(&full[0], 1);
@@ -80,7 +82,7 @@ __device__ __forceinline__ void tma_pipeline(const CUtensorMap* m, int64_t P, in
   __syncthreads();
   const int64_t it0 = blockIdx.x;
   if (tid == 0 && it0 < items) {
-    const Item nx = item_of(it0, pblocks);
+    const Item nx = item_of<TPI>(it0, pblocks);
     bar_expect(&full[0], BUF * 4);
     tma3d(smem, m, &full[0], (int)nx.p0, (int)nx.q, 0);
   }
@@ -88,13 +90,13 @@ __device__ __forceinline__ void tma_pipeline(const CUtensorMap* m, int64_t P, in
   for (int64_t it = it0; it < items; it += gridDim.x, ++n) {
     const int b = n & 1;
     if (tid == 0 && it + gridDim.x < items) {       // prefetch the next item into the other buffer
-      const Item nx = item_of(it + gridDim.x, pblocks);
+      const Item nx = item_of<TPI>(it + gridDim.x, pblocks);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_expect(&full[b ^ 1], BUF * 4);
       tma3d(smem + (b ^ 1) * BUF, m, &full[b ^ 1], (int)nx.p0, (int)nx.q, 0);
     }
     bar_wait(&full[b], (n >> 1) & 1);
-    body(item_of(it, pblocks), smem + b * BUF);
+    body(item_of<TPI>(it, pblocks), smem + b * BUF);
     __syncthreads();      // buffer b fully consumed before it is refilled (two iterations on)
   }
 }
@@ -265,6 +267,166 @@ __global__ void __launch_bounds__(TP / tpt_of(N)) inv_tma_kernel(const __grid_co
   });
 }
 
+// ------------------------------------------------------------------------------ tube-parallel FFT
+// Power-of-two 32 <= n3 <= 256 (configs 2 and 5): a work item is TUB = 2F consecutive tubes of
+// one q (F = min(4096 / N, 128) complex FFTs, two real tubes packed per FFT as in
+// transforms_fft.cu), TMA-loaded as the tile X(p0:p0+TUB, q, 0:N).  Read as float2 that tile IS
+// the point-major layout z[k][c] (c = tube pair), so the radix-16 (+ 8/4/2) Stockham passes run
+// in place on the TMA buffer with the F FFTs of a warp side by side: every shared access of a warp
+// is 32 consecutive float2 (conflict-free) and every twiddle w_{Ns R}^{r k} is warp-uniform (one
+// broadcast load from the handle's per-pass table).  Outputs are 128-byte warp rows (half2 planes
+// for K1, float2 rows for K3).
+//   K1: Alg. 1 step 1, Hermitian half (Eq. (8)), 2^e scale, fp16 split.
+//   K3: Alg. 1 step 2 second branch + step 3 (L177-179): conjugate fill, inverse FFT, 1/N.
+using namespace fftreg;
+
+constexpr int TUBE_NT = 256;
+template <int N>
+struct TubeCfg {
+  static constexpr int F = (4096 / N) > 128 ? 128 : 4096 / N;   // complex FFTs per item
+  static constexpr int TUB = 2 * F;                              // tubes per item (TMA box <= 256)
+  static constexpr int LOG = N == 32 ? 5 : N == 64 ? 6 : N == 128 ? 7 : 8;
+  static constexpr int NP = LOG / 4 + (LOG % 4 ? 1 : 0);         // passes: radix 16, then 2^(LOG%4)
+};
+__host__ __device__ constexpr int tube_R(int log, int i) { return i < log / 4 ? 16 : 1 << (log % 4); }
+__host__ __device__ constexpr int tube_Ns(int i) { return i == 0 ? 1 : 16 << (4 * (i - 1)); }
+// twiddle-table offset of pass i (make_plan layout of transforms_fft.cu: (R - 1) Ns entries per
+// pass with Ns > 1)
+__host__ __device__ constexpr int tube_toff(int log, int i) {
+  return i <= 1 ? 0 : tube_toff(log, i - 1) + (tube_R(log, i - 1) - 1) * tube_Ns(i - 1);
+}
+
+template <int N, int F, int R, int Ns, int DIR>
+__device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp) {
+  constexpr int NB = N / R;
+  constexpr int BPT = F * NB / TUBE_NT;
+  static_assert(F * NB % TUBE_NT == 0, "butterflies must divide evenly");
+  float2 v[BPT][R];
+#pragma unroll
+  for (int u = 0; u < BPT; ++u) {
+    const int b = threadIdx.x + u * TUBE_NT;
+    const int c = b % F, j = b / F, k = j % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[u][r] = z[(j + r * NB) * F + c];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twN<DIR>(tp, (r - 1) * Ns + k));
+    }
+    dft_reg<R, DIR>(v[u]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < BPT; ++u) {
+    const int b = threadIdx.x + u * TUBE_NT;
+    const int c = b % F, j = b / F, k = j % Ns, g = j / Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[(g * Ns * R + k + r * Ns) * F + c] = v[u][r];
+  }
+  __syncthreads();
+}
+
+template <int N, int DIR>
+__device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st) {
+  using C = TubeCfg<N>;
+  tube_pass<N, C::F, tube_R(C::LOG, 0), tube_Ns(0), DIR>(z, st);
+  if constexpr (C::NP > 1) tube_pass<N, C::F, tube_R(C::LOG, 1), tube_Ns(1), DIR>(z, st + tube_toff(C::LOG, 1));
+}
+
+template <int N, int ROLE>
+__global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant__ CUtensorMap mX, int64_t P,
+                                                          int64_t Q, const unsigned* __restrict__ maxbits,
+                                                          const float2* __restrict__ st, __half* __restrict__ out,
+                                                          int64_t ld, float* __restrict__ unscale) {
+  using C = TubeCfg<N>;
+  constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
+  constexpr int BUF = TUB * N;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full[2];
+  const int64_t plane = Q * ld;
+  const int c = threadIdx.x % F;                    // TUBE_NT % F == 0: fixed tube pair per thread
+  tma_pipeline<BUF, TUB>(&mX, P, Q, smem, full, [&](const Item& cur, float* s) {
+    float2* z = reinterpret_cast<float2*>(s);       // z[k][c] = (x_{2c}[k], x_{2c+1}[k])
+    tube_fft<N, -1>(z, st);
+    const int64_t q = cur.q, p = cur.p0 + 2 * c;
+    if (p >= P) return;
+    const bool two = p + 1 < P;
+    int e0, e1;
+    if (ROLE == 0) {
+      e0 = scale_exp(__ldg(maxbits + p), N);
+      e1 = two ? scale_exp(__ldg(maxbits + p + 1), N) : 0;
+      if (q == 0) {
+        unscale[p] = pow2f(-e0);
+        if (two) unscale[p + 1] = pow2f(-e1);
+      }
+    } else {
+      e0 = e1 = scale_exp(__ldg(maxbits + q), N);
+      if (p == 0) unscale[q] = pow2f(-e0);
+    }
+    const float s0 = pow2f(e0), s1 = pow2f(e1);
+    __half* o = out + q * ld + p;
+#pragma unroll 4
+    for (int f = threadIdx.x / F; f < H; f += TUBE_NT / F) {
+      const float2 zf = z[f * F + c], zm = z[((N - f) % N) * F + c];
+      // X_f = (Z_f + conj Z_{N-f}) / 2 ;  Y_f = (Z_f - conj Z_{N-f}) / (2i)
+      const float2 re = make_float2(0.5f * (zf.x + zm.x) * s0, 0.5f * (zf.y + zm.y) * s1);
+      const float2 im = make_float2(0.5f * (zf.y - zm.y) * s0, -0.5f * (zf.x - zm.x) * s1);
+      const __half2 rh = __float22half2_rn(re), ih = __float22half2_rn(im);
+      const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
+      const __half2 rl = __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));
+      const __half2 il = __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));
+      __half* of = o + (int64_t)(4 * f) * plane;
+      if (two) {
+        *reinterpret_cast<__half2*>(of + PL_RE_HI * plane) = rh;
+        *reinterpret_cast<__half2*>(of + PL_RE_LO * plane) = rl;
+        *reinterpret_cast<__half2*>(of + PL_IM_HI * plane) = ih;
+        *reinterpret_cast<__half2*>(of + PL_IM_LO * plane) = il;
+      } else {
+        of[PL_RE_HI * plane] = __low2half(rh);
+        of[PL_RE_LO * plane] = __low2half(rl);
+        of[PL_IM_HI * plane] = __low2half(ih);
+        of[PL_IM_LO * plane] = __low2half(il);
+      }
+    }
+  });
+}
+
+template <int N>
+__global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant__ CUtensorMap mC, int64_t P,
+                                                          int64_t Q, const float2* __restrict__ st,
+                                                          float* __restrict__ X) {
+  using C = TubeCfg<N>;
+  constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
+  constexpr int BUF = TUB * 2 * H;                  // C-bar tile: rows [f][re|im], TUB floats each
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full[2];
+  float2* z = reinterpret_cast<float2*>(smem + 2 * BUF);     // z[k][c], separate from the TMA buffers
+  const float inv_n = 1.f / (float)N;
+  const int64_t PQ = P * Q;
+  tma_pipeline<BUF, TUB>(&mC, P, Q, smem, full, [&](const Item& cur, const float* s) {
+    // Z = X + i Y with the conjugate fill (Im of DC / Nyquist dropped: C2R)
+    for (int idx = threadIdx.x; idx < H * F; idx += TUBE_NT) {
+      const int c = idx % F, f = idx / F;
+      const bool self = (f == 0 || 2 * f == N);
+      const float2 re = reinterpret_cast<const float2*>(s + (2 * f) * TUB)[c];       // (x_r, y_r)
+      const float2 im = self ? make_float2(0.f, 0.f)
+                             : reinterpret_cast<const float2*>(s + (2 * f + 1) * TUB)[c];  // (x_i, y_i)
+      z[f * F + c] = make_float2(re.x - im.y, im.x + re.y);                        // X_f + i Y_f
+      if (!self) z[(N - f) * F + c] = make_float2(re.x + im.y, re.y - im.x);       // conj X_f + i conj Y_f
+    }
+    __syncthreads();
+    tube_fft<N, +1>(z, st);
+    float* xo = X + P * cur.q + cur.p0;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < N * F; idx += TUBE_NT) {
+      const int c = idx % F, k = idx / F;
+      const int64_t p = cur.p0 + 2 * c;
+      const float2 v = z[k * F + c];
+      if (p + 1 < P) *reinterpret_cast<float2*>(xo + PQ * k + 2 * c) = make_float2(v.x * inv_n, v.y * inv_n);
+      else if (p < P) xo[PQ * k + 2 * c] = v.x * inv_n;
+    }
+  });
+}
+
 // ------------------------------------------------------------------------------ tables / launch
 using FwdFn = void (*)(CUtensorMap, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
 using InvFn = void (*)(CUtensorMap, int64_t, int64_t, float*);
@@ -334,12 +496,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode() {
 
 // fp32 3-D map {d0 (contiguous, pitch ld0), d1, d2 (pitch ld0*d1)}, box {TP, 1, b2}
 bool map_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t ld0, uint64_t d1, uint64_t d2,
-             uint32_t b2) {
+             uint32_t b2, uint32_t b0 = TP) {
   auto fn = encode();
   if (!fn || (ld0 * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0 || b2 > 256) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {ld0 * 4, ld0 * d1 * 4};
-  cuuint32_t box[3] = {(cuuint32_t)TP, 1, b2};
+  cuuint32_t box[3] = {b0, 1, b2};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -358,7 +520,86 @@ int grid_for(int64_t items, size_t smem_bytes, int threads, int num_sms) {
 
 int threads_of(int64_t n3) { return TP / (n3 <= 32 ? 2 : 1); }
 
+
+// Persistent grid: the CTAs that are co-resident on an SM (registers, smem, threads), times the SMs.
+int grid_occ(const void* fn, int64_t items, size_t smem, int num_sms) {
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TUBE_NT, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  const int64_t g = (int64_t)num_sms * per_sm;
+  return (int)(items < g ? items : g);
+}
+
+// Tube-parallel Stockham transforms (power-of-two 32 <= n3 <= 256); false = not handled.
+template <int N>
+bool launch_fwd_tube_n(const float* X, int64_t P, int64_t Q, int role, const unsigned* maxbits, const float2* st,
+                       __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
+  using C = TubeCfg<N>;
+  CUtensorMap m;
+  if (!map_f32(&m, X, (uint64_t)P, (uint64_t)P, (uint64_t)Q, (uint64_t)N, (uint32_t)N, (uint32_t)C::TUB))
+    return false;
+  const void* fn = role == 0 ? (const void*)fwd_tube_kernel<N, 0> : (const void*)fwd_tube_kernel<N, 1>;
+  const size_t smem = 2 * sizeof(float) * C::TUB * (size_t)N;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+  const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
+  const int grid = grid_occ(fn, items, smem, num_sms);
+  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&st, (void*)&out, (void*)&ld,
+                  (void*)&unscale};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
+}
+
+template <int N>
+bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const float2* st, float* X, int num_sms,
+                       cudaStream_t s) {
+  using C = TubeCfg<N>;
+  constexpr int H = N / 2 + 1;
+  CUtensorMap m;
+  if (!map_f32(&m, Cre, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(2 * H), (uint32_t)(2 * H),
+               (uint32_t)C::TUB))
+    return false;
+  const void* fn = (const void*)inv_tube_kernel<N>;
+  const size_t smem = 2 * sizeof(float) * C::TUB * 2 * H + sizeof(float2) * (size_t)C::F * N;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+  const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
+  const int grid = grid_occ(fn, items, smem, num_sms);
+  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&st, (void*)&X};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
+}
+
 }  // namespace
+
+bool tube_supported(int64_t n3) { return n3 == 32 || n3 == 64 || n3 == 128 || n3 == 256; }
+
+// Measured (B200, K1/K3 stage times): the tube kernels win the forward transform for n3 = 64
+// (config 5: 10.1 -> 8.3 ms), 128 and 256 (2x over the buffer-major FFT kernels) and the inverse
+// for 128 / 256; the register kernels of transforms_dense.cu stay faster for the n3 = 32 forward
+// and the n3 <= 64 inverse (config 5 K3: 4.4 vs 5.5 ms).
+static bool tube_fwd_pick(int64_t n3) { return n3 == 64 || n3 == 128 || n3 == 256; }
+static bool tube_inv_pick(int64_t n3) { return n3 == 128 || n3 == 256; }
+
+bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                     const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
+  if (!st || !tube_fwd_pick(n3) || P % 4 != 0 || ((uintptr_t)X & 15) != 0 || ld % 2 != 0) return false;
+  switch (n3) {
+    case 32: return launch_fwd_tube_n<32>(X, P, Q, role, maxbits, st, out, ld, unscale, num_sms, s);
+    case 64: return launch_fwd_tube_n<64>(X, P, Q, role, maxbits, st, out, ld, unscale, num_sms, s);
+    case 128: return launch_fwd_tube_n<128>(X, P, Q, role, maxbits, st, out, ld, unscale, num_sms, s);
+    default: return launch_fwd_tube_n<256>(X, P, Q, role, maxbits, st, out, ld, unscale, num_sms, s);
+  }
+}
+
+bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
+                     int num_sms, cudaStream_t s) {
+  if (!st || !tube_inv_pick(n3) || P % 2 != 0 || ((uintptr_t)X & 7) != 0 || (ld * 4) % 16 != 0) return false;
+  switch (n3) {
+    case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, X, num_sms, s);
+    case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, X, num_sms, s);
+    case 128: return launch_inv_tube_n<128>(Cre, ld, P, Q, st, X, num_sms, s);
+    default: return launch_inv_tube_n<256>(Cre, ld, P, Q, st, X, num_sms, s);
+  }
+}
 
 bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {

@@ -25,10 +25,14 @@ def main():
     B = tp.to_matlab(torch.randn(n2, n4, n3, device="cuda", generator=g))
     flops = 8.0 * n1 * n2 * n4 * (n3 // 2 + 1)
     ref = None
-    for bn, cn in ((128, 1), (128, 2), (128, 3), (0, 0)):
+    variants = ((128, 1, 0), (128, 2, 0), (128, 3, 0), (0, 0, 0), (0, 0, 1))
+    if "--quick" in sys.argv:
+        variants = ((0, 0, 0), (0, 0, 1))
+    for bn, cn, tr in variants:
         h = tp.Handle()
         h.set_option(tp._lib.TPROD_OPT_GEMM_BN, bn)
         h.set_option(tp._lib.TPROD_OPT_GEMM_CLUSTER, cn)
+        h.set_option(tp._lib.TPROD_OPT_TRANSFORM, tr)
         C = tp.tprod(A, B, handle=h)
         torch.cuda.synchronize()
         h.set_option(tp._lib.TPROD_OPT_TIMING, 1)
@@ -38,11 +42,12 @@ def main():
             ks.append(h.last_stage_ms())
         torch.cuda.synchronize()
         k2 = sorted(k[2] for k in ks)[reps // 2]
-        same = "ref" if ref is None else ("bitwise-equal" if torch.equal(C, ref) else "DIFFERENT")
+        same = "ref" if ref is None else ("bitwise-equal" if torch.equal(C, ref) else
+                                          f"differs: max rel {((C - ref).abs().max() / ref.abs().max()).item():.2e}")
         if ref is None:
             ref = C.clone()
         stages = [round(sorted(k[i] for k in ks)[reps // 2], 4) for i in range(4)]
-        print(f"{n1}x{n2}x{n3} * {n2}x{n4}x{n3}  bn={bn} cn={cn}: K2 {k2:.4f} ms = "
+        print(f"{n1}x{n2}x{n3} * {n2}x{n4}x{n3}  bn={bn} cn={cn} transform={tr}: K2 {k2:.4f} ms = "
               f"{flops / k2 / 1e9:.1f} TFLOP/s  stages {stages}  {same}", flush=True)
         h.close()
 

@@ -83,6 +83,7 @@ SWEEP = [
     (200, 136, 3, 264), (8, 1000, 2, 8), (1000, 8, 2, 3),
     (33, 17, 128, 9), (64, 40, 512, 20), (10, 7, 2048, 5), (70, 30, 100, 40),
     (33, 17, 240, 9), (20, 12, 375, 7), (16, 16, 1536, 16),
+    (64, 48, 128, 40), (36, 20, 256, 12), (300, 264, 64, 132),   # tube-parallel K1/K3 (P % 4 == 0)
 ]
 
 
@@ -161,6 +162,24 @@ def test_stage_inverse_roundtrip(T, n3):
     Xb = torch.from_numpy(np.fft.rfft(X.astype(np.float64), axis=2).astype(np.complex64)).cuda()
     back = host(T.idft_f32(Xb, n3))
     assert np.linalg.norm(back - X) / np.linalg.norm(X) < 2e-6
+
+
+@pytest.mark.parametrize("n3", [64, 128, 256])
+def test_tube_transforms_match_register_kernels(T, n3):
+    """The TMA-staged tube-parallel Stockham kernels (picked for aligned shapes) and the register /
+    buffer-major kernels (TPROD_OPT_TRANSFORM = 1) compute the same t-product: both within the
+    fp32 tolerance of the oracle, and within fp32 rounding of each other.  P = 4k with a ragged last
+    item (n1 not a multiple of the 2F tubes per item)."""
+    A = normal((516, 40, n3), 31 + n3)
+    B = normal((40, 24, n3), 32 + n3)
+    ref = O.tprod_columns(A, B, np.arange(24))
+    h0, h1 = T.Handle(), T.Handle()
+    h1.set_option(T._lib.TPROD_OPT_TRANSFORM, 1)
+    C0 = gpu_tprod(T, A, B, handle=h0)
+    C1 = gpu_tprod(T, A, B, handle=h1)
+    assert O.rel_err(C0, ref) <= TOL32
+    assert O.rel_err(C1, ref) <= TOL32
+    assert O.rel_err(C0, C1) <= 1e-6
 
 
 def test_worked_examples_on_gpu(T, golden):
