@@ -161,21 +161,19 @@ def oracle_sample(wl, A64, B, ncols, nslices):
     return dt, F, desc
 
 
-def sample_size(wl, budget_s):
-    """(|J|, |T|) for a CPU sample of roughly budget_s seconds (oracle cost model: one block row
-    gathers n1 n2 n3 doubles and multiplies n1 x n2 n3 by n2 n3 x |J|; ~1.5 GB/s, ~100 GF/s)."""
-    n1, n2, n3, n4 = wl["n1"], wl["n2"], wl["n3"], wl["n4"]
-    per_row_gather = 8.0 * n1 * n2 * n3 / 1.5e9
+def sample_size(wl, A64, B, budget_s):
+    """(|J|, |T|) for a CPU sample of roughly budget_s seconds: |J| = 16 lateral slices, and as
+    many frontal slices as fit the budget after timing one block row of the oracle."""
+    n3, n4 = wl["n3"], wl["n4"]
     ncols = min(n4, 16)
-    per_row = per_row_gather + 2.0 * n1 * n2 * n3 * ncols / 1e11
-    nslices = int(max(1, min(n3, budget_s / per_row)))
-    return ncols, nslices
+    dt1, _, _ = oracle_sample(wl, A64, B, ncols, 1)
+    return ncols, int(max(1, min(n3, budget_s / max(dt1, 1e-6))))
 
 
-def cpu_baseline(wl, A_f32, B_cols, budget_s=12.0):
+def cpu_baseline(wl, A_f32, B_cols, budget_s=15.0):
     import numpy as np
     A64 = np.asarray(A_f32, dtype=np.float64)
-    ncols, nslices = sample_size(wl, budget_s)
+    ncols, nslices = sample_size(wl, A64, B_cols, budget_s)
     dt, F, desc = oracle_sample(wl, A64, B_cols, ncols, nslices)
     return {"value": F / dt / 1e12, "unit": "TFLOP/s", "cores": _cores(), "kind": "oracle",
             "seconds": dt, "sample": desc + f" in {dt:.2f} s"}
@@ -189,9 +187,9 @@ def run_reference(args, wl, rank, world):
     import numpy as np
     from synth import normal
     A64 = normal((wl["n1"], wl["n2"], wl["n3"]), wl["seedA"]).astype(np.float64)
-    ncols, nslices = sample_size(wl, 3.0)
     # the sample's lateral slices of B (a timing sample: drawn directly, not from B's full stream)
-    B = normal((wl["n2"], ncols, wl["n3"]), wl["seedB"])
+    B = normal((wl["n2"], min(16, wl["n4"]), wl["n3"]), wl["seedB"])
+    ncols, nslices = sample_size(wl, A64, B, 3.0)
     for _ in range(args.warmup):
         oracle_sample(wl, A64, B, ncols, nslices)
     ts, F, desc = [], 0.0, ""

@@ -55,6 +55,17 @@ __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, uint64_t*
       : "memory");
 }
 
+// bulk tensor store smem -> global (async proxy); completion tracked by bulk groups
+__device__ __forceinline__ void tma_store3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m),
+               "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 struct Item {
   int64_t q, p0;
 };
@@ -281,6 +292,11 @@ __global__ void __launch_bounds__(TP / tpt_of(N)) inv_tma_kernel(const __grid_co
 using namespace fftreg;
 
 constexpr int TUBE_NT = 256;
+// rows per TMA store box for R output rows: R / k for the smallest k with R / k <= 256, k | R
+__host__ __device__ constexpr int store_rows(int R, int k = 1) {
+  return (R % k == 0 && R / k <= 256) ? R / k : store_rows(R, k + 1);
+}
+
 template <int N>
 struct TubeCfg {
   static constexpr int F = (4096 / N) > 128 ? 128 : 4096 / N;   // complex FFTs per item
@@ -332,38 +348,41 @@ __device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ s
   if constexpr (C::NP > 1) tube_pass<N, C::F, tube_R(C::LOG, 1), tube_Ns(1), DIR>(z, st + tube_toff(C::LOG, 1));
 }
 
+// K1 epilogue staged in shared memory: the item's 4h output rows (f, plane) of TUB halves are
+// written with 32-bit shared stores and leave as TMA bulk tensor stores (<= 256 rows per box), so
+// the SM issues no 64-bit global address arithmetic and HBM sees whole 256-byte rows.
 template <int N, int ROLE>
-__global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant__ CUtensorMap mX, int64_t P,
+__global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant__ CUtensorMap mX,
+                                                          const __grid_constant__ CUtensorMap mO, int64_t P,
                                                           int64_t Q, const unsigned* __restrict__ maxbits,
-                                                          const float2* __restrict__ st, __half* __restrict__ out,
-                                                          int64_t ld, float* __restrict__ unscale) {
+                                                          const float2* __restrict__ st, float* __restrict__ unscale) {
   using C = TubeCfg<N>;
   constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
-  constexpr int BUF = TUB * N;
+  constexpr int BUF = TUB * N;                      // floats per input buffer
   extern __shared__ __align__(128) float smem[];
   __shared__ uint64_t full[2];
-  const int64_t plane = Q * ld;
+  __half2* stg = reinterpret_cast<__half2*>(smem + 2 * BUF);   // [4h][TUB / 2] output rows
   const int c = threadIdx.x % F;                    // TUBE_NT % F == 0: fixed tube pair per thread
   tma_pipeline<BUF, TUB>(&mX, P, Q, smem, full, [&](const Item& cur, float* s) {
     float2* z = reinterpret_cast<float2*>(s);       // z[k][c] = (x_{2c}[k], x_{2c+1}[k])
     tube_fft<N, -1>(z, st);
     const int64_t q = cur.q, p = cur.p0 + 2 * c;
-    if (p >= P) return;
-    const bool two = p + 1 < P;
-    int e0, e1;
+    const bool in0 = p < P, in1 = p + 1 < P;
+    int e0 = 0, e1 = 0;
     if (ROLE == 0) {
-      e0 = scale_exp(__ldg(maxbits + p), N);
-      e1 = two ? scale_exp(__ldg(maxbits + p + 1), N) : 0;
-      if (q == 0) {
-        unscale[p] = pow2f(-e0);
-        if (two) unscale[p + 1] = pow2f(-e1);
+      if (in0) e0 = scale_exp(__ldg(maxbits + p), N);
+      if (in1) e1 = scale_exp(__ldg(maxbits + p + 1), N);
+      if (q == 0 && threadIdx.x < F) {
+        if (in0) unscale[p] = pow2f(-e0);
+        if (in1) unscale[p + 1] = pow2f(-e1);
       }
     } else {
       e0 = e1 = scale_exp(__ldg(maxbits + q), N);
-      if (p == 0) unscale[q] = pow2f(-e0);
+      if (cur.p0 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
     }
     const float s0 = pow2f(e0), s1 = pow2f(e1);
-    __half* o = out + q * ld + p;
+    if (threadIdx.x == 0) bulk_wait_read();         // the previous item's stores have read stg
+    __syncthreads();
 #pragma unroll 4
     for (int f = threadIdx.x / F; f < H; f += TUBE_NT / F) {
       const float2 zf = z[f * F + c], zm = z[((N - f) % N) * F + c];
@@ -372,22 +391,22 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
       const float2 im = make_float2(0.5f * (zf.y - zm.y) * s0, -0.5f * (zf.x - zm.x) * s1);
       const __half2 rh = __float22half2_rn(re), ih = __float22half2_rn(im);
       const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
-      const __half2 rl = __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));
-      const __half2 il = __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));
-      __half* of = o + (int64_t)(4 * f) * plane;
-      if (two) {
-        *reinterpret_cast<__half2*>(of + PL_RE_HI * plane) = rh;
-        *reinterpret_cast<__half2*>(of + PL_RE_LO * plane) = rl;
-        *reinterpret_cast<__half2*>(of + PL_IM_HI * plane) = ih;
-        *reinterpret_cast<__half2*>(of + PL_IM_LO * plane) = il;
-      } else {
-        of[PL_RE_HI * plane] = __low2half(rh);
-        of[PL_RE_LO * plane] = __low2half(rl);
-        of[PL_IM_HI * plane] = __low2half(ih);
-        of[PL_IM_LO * plane] = __low2half(il);
-      }
+      __half2* row = stg + (4 * f) * (TUB / 2) + c;
+      row[PL_RE_HI * (TUB / 2)] = rh;
+      row[PL_RE_LO * (TUB / 2)] = __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));
+      row[PL_IM_HI * (TUB / 2)] = ih;
+      row[PL_IM_LO * (TUB / 2)] = __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      constexpr int RB = store_rows(4 * H);
+#pragma unroll
+      for (int r0 = 0; r0 < 4 * H; r0 += RB) tma_store3d(&mO, stg + r0 * (TUB / 2), (int)cur.p0, (int)q, r0);
+      bulk_commit();
     }
   });
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 template <int N>
@@ -508,6 +527,20 @@ bool map_f32(CUtensorMap* m, const void* base, uint64_t d0, uint64_t ld0, uint64
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp16 3-D map {d0 (contiguous, pitch ld0), d1, d2 (pitch ld0*d1)}, box {b0, 1, b2} (TMA stores)
+bool map_f16_out(CUtensorMap* m, void* base, uint64_t d0, uint64_t ld0, uint64_t d1, uint64_t d2, uint32_t b0,
+                 uint32_t b2) {
+  auto fn = encode();
+  if (!fn || (ld0 * 2) % 16 != 0 || ((uintptr_t)base & 15) != 0 || b0 > 256 || b2 > 256) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {ld0 * 2, ld0 * d1 * 2};
+  cuuint32_t box[3] = {b0, 1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 int grid_for(int64_t items, size_t smem_bytes, int threads, int num_sms) {
   int per_sm = (int)((220 * 1024) / (smem_bytes + 1024));
   const int per_sm_thr = 2048 / threads;
@@ -540,13 +573,17 @@ bool launch_fwd_tube_n(const float* X, int64_t P, int64_t Q, int role, const uns
   CUtensorMap m;
   if (!map_f32(&m, X, (uint64_t)P, (uint64_t)P, (uint64_t)Q, (uint64_t)N, (uint32_t)N, (uint32_t)C::TUB))
     return false;
+  constexpr int H = N / 2 + 1;
+  CUtensorMap mo;   // split planes [f][4][q][ld] as {P (pitch ld), Q, 4h}, fp16, box {TUB, 1, <=256}
+  if (!map_f16_out(&mo, out, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(4 * H), (uint32_t)C::TUB,
+                   (uint32_t)store_rows(4 * H)))
+    return false;
   const void* fn = role == 0 ? (const void*)fwd_tube_kernel<N, 0> : (const void*)fwd_tube_kernel<N, 1>;
-  const size_t smem = 2 * sizeof(float) * C::TUB * (size_t)N;
+  const size_t smem = 2 * sizeof(float) * C::TUB * (size_t)N + sizeof(__half) * 4 * H * C::TUB;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
   const int grid = grid_occ(fn, items, smem, num_sms);
-  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&st, (void*)&out, (void*)&ld,
-                  (void*)&unscale};
+  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&st, (void*)&unscale};
   return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
 }
 

@@ -285,3 +285,16 @@ def test_generator_recipe():
     ref = np.random.default_rng(7).standard_normal(60).astype(np.float32)
     np.testing.assert_array_equal(x.ravel(order="F"), ref)
     assert x.flags.f_contiguous
+
+
+@pytest.mark.parametrize("chunk", [5, 17, 1 << 24])
+def test_normal_lateral_is_the_global_stream(monkeypatch, chunk):
+    """synth.normal_lateral(shape, seed, j0, j1) equals normal(shape, seed)[:, j0:j1, :] for any
+    chunking of the stream (the per-rank inputs of the strong-scaling bench)."""
+    import synth
+    monkeypatch.setattr(synth, "_CHUNK", chunk)
+    full = synth.normal((7, 13, 5), 3)
+    for j0, j1 in ((0, 13), (0, 1), (4, 9), (12, 13)):
+        part = synth.normal_lateral((7, 13, 5), 3, j0, j1)
+        assert part.flags.f_contiguous
+        np.testing.assert_array_equal(part, full[:, j0:j1, :])
