@@ -437,7 +437,7 @@ def main():
                           "roofline": roofline(c3, peaks, src, "c3", False),
                           "e2e": c3["e2e"], "gpu_launches": c3["launches"], "clocks": c3["clocks"],
                           "parity_rel_err_sampled": c3.get("parity_rel_err_sampled")}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:      # rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(wl, meas["A_host"].numpy(), meas["B_cols"])
         print(json.dumps(line), flush=True)
     if world > 1:
