@@ -55,7 +55,11 @@ def metric_flops(n1, n2, n3, n4):
 
 
 def gemm_flops(n1, n2, n3, n4):
-    return 8.0 * n1 * n2 * n4 * h_slices(n3)
+    """Flops the K2 stage performs: the DC slice (and the Nyquist slice for even n3) of real inputs
+    is real (Eq. (8)), so it is one real product (2 n1 n2 n4) instead of a complex one
+    (8 n1 n2 n4); the metric's formula counts every slice as complex (R11)."""
+    r = 1 + (1 if n3 % 2 == 0 and n3 >= 2 else 0)
+    return 8.0 * n1 * n2 * n4 * (h_slices(n3) - r) + 2.0 * n1 * n2 * n4 * r
 
 
 def load_peaks():
@@ -346,7 +350,8 @@ def roofline(meas, peaks, src, workload, sustained):
     return {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
             "frac": achieved / P, "traffic": tr,
             "kernel": "K2 per-frequency complex GEMM (gemm_tc_kernel)",
-            "note": (f"achieved = 8*n1*n2*n4*h algorithmic flops / mean K2 time (CUDA events on the "
+            "note": (f"achieved = the GEMM's algorithmic flops (8*n1*n2*n4 per complex slice, 2*n1*n2*n4 "
+                     f"per real DC/Nyquist slice) / mean K2 time (CUDA events on the "
                      f"launching stream, every timed step); peak = {src} bf16 "
                      f"{'sustained' if sustained else 'burst'} / 3: an fp32-accurate product costs 3 "
                      f"fp16 tensor-core products (hi*hi + hi*lo + lo*hi)"),

@@ -7,7 +7,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtprod.so")
+# TPROD_LIB overrides the in-tree library (A/B timing of two builds); default: the in-tree build
+LIB_PATH = os.environ.get("TPROD_LIB") or os.path.join(_PKG, "libtprod.so")
 
 TPROD_OK, TPROD_EINVAL, TPROD_EALIAS, TPROD_ENOMEM, TPROD_ECUDA, TPROD_ENCCL, \
     TPROD_EUNSUPPORTED, TPROD_ENOWORLD = range(8)

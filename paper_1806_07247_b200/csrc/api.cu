@@ -263,7 +263,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
   if (tc) {
-    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB,
+    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB, n3 % 2 == 0 ? 1 : 0,
                               h->force_bn, h->force_cn, h->num_sms, s);
     if (st) return st;
   } else {

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
                    const float* __restrict__ uA, const float* __restrict__ uB,
-                   long long* __restrict__ dbg) {
+                   long long* __restrict__ dbg, int nyq) {
   using G = Cfg<BN>;
   const long long t_start = clock64();
   long long w0 = 0, w1 = 0;   // per-role wait cycles (diagnostics, dbg != nullptr)
@@ -335,6 +335,9 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       constexpr uint32_t ID_NEG = idesc_f16(BM, BN, 1);
       uint32_t it = 0, g = 0;
       for (int64_t t = cid; t < nctiles; t += ncl) {
+        // (the real DC / Nyquist shortcut of gemm_tc2_kernel is not taken here: measured 7% slower on
+        // config 4, where this kernel runs)
+        const bool real_f = false;
         for (int sg = 0; sg < nseg; ++sg, ++g) {
           const uint32_t b = g & 1, use = g >> 1;
           { long long t0 = dbg ? clock64() : 0; mbar_wait(seg_empty + b, (use & 1) ^ 1); if (dbg) w0 += clock64() - t0; }  // epilogue drained this buffer
@@ -363,16 +366,18 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
               mma_f16(tCr, a[PL_RE_HI], bd[PL_RE_HI], ID_POS, acc0);
               mma_f16(tCr, a[PL_RE_HI], bd[PL_RE_LO], ID_POS, 1);
               mma_f16(tCr, a[PL_RE_LO], bd[PL_RE_HI], ID_POS, 1);
-              mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
-              mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
-              mma_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
-              // Ci = Ar.Bi + Ai.Br
-              mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
-              mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
-              mma_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
-              mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
-              mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
-              mma_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+              if (!real_f) {
+                mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
+                mma_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
+                mma_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
+                // Ci = Ar.Bi + Ai.Br
+                mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
+                mma_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
+                mma_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
+                mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
+                mma_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
+                mma_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+              }
             }
             // smem slot free once these MMAs have read it (in every CTA that wrote into it)
             if (CN == 1) mma_commit(empty + s);
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     for (int64_t t = cid; t < nctiles; t += ncl) {
       const TileInfo ti = tile_of(t, mt, ntg, CN, rank);
       const int n0 = ti.n0 * BN + half * CPT;
+      const bool real_f = false;
       float accr[CPT], acci[CPT];
 #pragma unroll
       for (int x = 0; x < CPT; ++x) accr[x] = acci[x] = 0.f;
@@ -405,12 +411,12 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         for (int c = 0; c < CPT; c += 16) {
           uint32_t vr[16], vi[16];
           tmem_ld16_nowait(base + c, vr);
-          tmem_ld16_nowait(base + BN + c, vi);
+          tmem_ld16_nowait(base + BN + c, vi);     // (stale for real slices: selected away below)
           tmem_wait();
 #pragma unroll
           for (int x = 0; x < 16; ++x) {
             accr[c + x] += __uint_as_float(vr[x]);
-            acci[c + x] += __uint_as_float(vi[x]);
+            acci[c + x] += real_f ? 0.f : __uint_as_float(vi[x]);
           }
         }
         tc_fence_before();
@@ -532,7 +538,7 @@ template <int SEGKB>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
-                    const float* __restrict__ uA, const float* __restrict__ uB, int GM) {
+                    const float* __restrict__ uA, const float* __restrict__ uB, int GM, int nyq) {
   constexpr int BN = 128;
   constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
   constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
@@ -607,17 +613,21 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     for (int64_t t = cid; t < ntiles; t += ncl) {
       int f, m0, n0;
       tile_of2(t, f, m0, n0);
+      // real DC / Nyquist slice: only the Re planes are loaded (the MMAs read nothing else)
+      const bool real_f = f == 0 || (nyq && f == h - 1);
+      const int np = real_f ? 2 : NPLANES;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(empty + s, ph ^ 1);
         uint8_t* st = smem + s * STAGE;
-        if (rank == 0) mbar_expect_tx(full + s, 2 * STAGE);
+        if (rank == 0) mbar_expect_tx(full + s, 2 * (STAGE / NPLANES) * np);
         const uint32_t bar = full_cl + s * 8;
         const int k0 = kb * BK;
         const int mr = m0 + BM * (int)rank, nr = n0 + (BN / 2) * (int)rank;
 #pragma unroll
         for (int p = 0; p < NPLANES; ++p) {
+          if (p >= np) break;
           uint8_t* a = st + p * A_PLANE;
           tma_load_3d_pair(a, &tmA, bar, mr, k0, 4 * f + p);
           tma_load_3d_pair(a + BK * 128, &tmA, bar, mr + 64, k0, 4 * f + p);
@@ -632,6 +642,9 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       constexpr uint32_t ID_NEG = idesc_f16(2 * BM, BN, 1);
       uint32_t it = 0, g = 0;
       for (int64_t t = cid; t < ntiles; t += ncl) {
+        int tf, tm, tn;
+        tile_of2(t, tf, tm, tn);
+        const bool real_f = tf == 0 || (nyq && tf == h - 1);     // DC / Nyquist: Ar.Br only
         for (int sg = 0; sg < nseg; ++sg, ++g) {
           const uint32_t b = g & 1, use = g >> 1;
           mbar_wait_cluster(seg_empty + b, (use & 1) ^ 1);    // both CTAs drained this buffer
@@ -657,15 +670,18 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
               mma2_f16(tCr, a[PL_RE_HI], bd[PL_RE_HI], ID_POS, acc0);
               mma2_f16(tCr, a[PL_RE_HI], bd[PL_RE_LO], ID_POS, 1);
               mma2_f16(tCr, a[PL_RE_LO], bd[PL_RE_HI], ID_POS, 1);
-              mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
-              mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
-              mma2_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
-              mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
-              mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
-              mma2_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
-              mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
-              mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
-              mma2_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+              if (!real_f) {
+                mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_HI], ID_NEG, 1);
+                mma2_f16(tCr, a[PL_IM_HI], bd[PL_IM_LO], ID_NEG, 1);
+                mma2_f16(tCr, a[PL_IM_LO], bd[PL_IM_HI], ID_NEG, 1);
+                // Ci = Ar.Bi + Ai.Br
+                mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_HI], ID_POS, acc0);
+                mma2_f16(tCi, a[PL_RE_HI], bd[PL_IM_LO], ID_POS, 1);
+                mma2_f16(tCi, a[PL_RE_LO], bd[PL_IM_HI], ID_POS, 1);
+                mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_HI], ID_POS, 1);
+                mma2_f16(tCi, a[PL_IM_HI], bd[PL_RE_LO], ID_POS, 1);
+                mma2_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
+              }
             }
             mma2_commit_mc(empty + s, (uint16_t)3);     // slot s free in both CTAs
           }
@@ -685,6 +701,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       int f, m0, n0t;
       tile_of2(t, f, m0, n0t);
       const int n0 = n0t + half * CPT;
+      const bool real_f = f == 0 || (nyq && f == h - 1);
       float accr[CPT], acci[CPT];
 #pragma unroll
       for (int x = 0; x < CPT; ++x) accr[x] = acci[x] = 0.f;
@@ -697,12 +714,12 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         for (int c = 0; c < CPT; c += 16) {
           uint32_t vr[16], vi[16];
           tmem_ld16_nowait(base + c, vr);
-          tmem_ld16_nowait(base + BN + c, vi);
+          tmem_ld16_nowait(base + BN + c, vi);     // (stale for real slices: selected away below)
           tmem_wait();
 #pragma unroll
           for (int x = 0; x < 16; ++x) {
             accr[c + x] += __uint_as_float(vr[x]);
-            acci[c + x] += __uint_as_float(vi[x]);
+            acci[c + x] += real_f ? 0.f : __uint_as_float(vi[x]);
           }
         }
         tc_fence_before();
@@ -771,7 +788,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 
 template <int BN, int CN>
 int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
-              int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int num_sms,
+              int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int nyq, int num_sms,
               cudaStream_t s) {
   using G = Cfg<BN>;
   CUtensorMap mb;
@@ -807,7 +824,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
     cudaMemsetAsync(dbg_buf, 0, 8 * sizeof(long long), s);
     dbg = dbg_buf;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, dbg) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, dbg, nyq) != cudaSuccess)
     return 4;
   if (dbg) {
     long long hv[8];
@@ -823,7 +840,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
 
 template <int SEGKB>
 int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
-                int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int num_sms,
+                int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int nyq, int num_sms,
                 cudaStream_t s) {
   constexpr int BN = 128;
   constexpr int STAGE = NPLANES * (BK * BM * 2 + (BN / 2) * BK * 2);
@@ -852,7 +869,7 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   cfg.numAttrs = 1;
   int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
   const int GM = 0;   // plain n-fastest tile order (see gemm_tc2_kernel)
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, GM) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, GM, nyq) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -862,7 +879,7 @@ bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
 
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
                          int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int force_bn, int force_cn,
+                         const float* uA, const float* uB, int nyq, int force_bn, int force_cn,
                          int num_sms, cudaStream_t s) {
   CUtensorMap ma;
   if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
@@ -880,14 +897,14 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   const bool pair_ok = bn == 128 || force_bn == 0;
   if (cn == 3 || (cn == 0 && force_bn == 0 && n1 > 128 &&
                   ((n1 + 255) / 256) * ((n4 + 127) / 128) * h >= num_sms / 2)) {
-    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
   }
   if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
   if (bn == 128)
-    return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s)
-                   : tc::launch_bn<128, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
-  return cn == 2 ? tc::launch_bn<64, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s)
-                 : tc::launch_bn<64, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, num_sms, s);
+    return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s)
+                   : tc::launch_bn<128, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
+  return cn == 2 ? tc::launch_bn<64, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s)
+                 : tc::launch_bn<64, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
 }
 
 }  // namespace tprod

@@ -52,9 +52,11 @@ void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int
 
 // K2 (tcgen05 engine).  Returns false if the shape/device is not supported by the kernel.
 bool gemm_tc_supported();
+// nyq = 1 if slice h-1 is a real Nyquist slice (n3 even): DC and Nyquist slices have exactly zero
+// Im planes and run only the Ar.Br products.
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int force_bn, int force_cn,
+                         const float* uA, const float* uB, int nyq, int force_bn, int force_cn,
                          int num_sms, cudaStream_t s);
 
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
