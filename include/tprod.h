@@ -76,6 +76,21 @@ int tprod_f32(const float* A, const float* B, float* C,
               int64_t n1, int64_t n2, int64_t n3, int64_t n4,
               void* stream, tprod_handle h);
 
+/* Prepared left operand (fixed A, many B -- the broadcast-once scenario).
+ * tprod_prepare_a_f32 runs the A half of the path once -- the row scales (K0) and the forward
+ * mode-3 DFT of A's Hermitian half in the split GEMM-operand format (Alg. 1 step 1)
+ * -- into handle-owned device memory (8*h*n2*roundup(n1,8) + 4*n1 bytes, h = n3/2+1).  A is read
+ * during the call only (asynchronously on `stream`) and not retained; re-prepare if it changes.
+ * tprod_f32_prepared then computes C = A * B for the prepared A (n1 x n2 x n3) and B (n2 x n4 x n3),
+ * C (n1 x n4 x n3), both DEVICE pointers in Matlab layout, running only K0/K1 of B, the GEMM and
+ * the inverse.  The result is bitwise identical to tprod_f32(A, B, C, ...) (same kernels, same
+ * operand values, same K order).  Errors: TPROD_EINVAL if nothing is prepared or an argument is
+ * invalid, TPROD_EALIAS if C overlaps B, TPROD_ENOMEM.  tprod_release_a frees the prepared
+ * operand (also done by tprod_destroy and by the next tprod_prepare_a_f32). */
+int tprod_prepare_a_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
+int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod_handle h);
+int tprod_release_a(tprod_handle h);
+
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,
               int64_t n1, int64_t n2, int64_t n3, int64_t n4,

@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -85,6 +85,25 @@ class Handle:
         check(lib().tprod_last_stage_ms(self._h, out), "tprod_last_stage_ms")
         return [float(x) for x in out]
 
+    def prepare_a(self, A, stream=None):
+        """Prepared left operand (NEXT-1): run A's scales + forward DFT once (tprod_prepare_a_f32);
+        later tprod_prepared(B) calls on this handle reuse it.  A: float32 CUDA, Matlab layout."""
+        import torch
+        if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda:
+            raise ValueError("prepare_a needs a 3-D float32 CUDA tensor")
+        if not is_matlab_layout(A):
+            raise ValueError("A must have the Matlab layout (strides (1, n1, n1*n2)); use to_matlab()")
+        n1, n2, n3 = (int(x) for x in A.shape)
+        s = stream if stream is not None else torch.cuda.current_stream(A.device)
+        check(lib().tprod_prepare_a_f32(A.data_ptr(), n1, n2, n3, C.c_void_p(s.cuda_stream), self._h),
+              "tprod_prepare_a_f32")
+        self.prepared = (n1, n2, n3)
+        return self
+
+    def release_a(self):
+        check(lib().tprod_release_a(self._h), "tprod_release_a")
+        self.prepared = None
+
     def set_world(self, rank: int, world: int, uid: bytes):
         if len(uid) != 128:
             raise ValueError("NCCL unique id must be 128 bytes")
@@ -141,6 +160,28 @@ def _call(fn_name, A, B, out=None, handle=None, stream=None):
     st = getattr(lib(), fn_name)(A.data_ptr(), B.data_ptr(), out.data_ptr(), n1, n2, n3, n4,
                                  C.c_void_p(s.cuda_stream), h.ptr)
     check(st, fn_name)
+    return out
+
+
+def tprod_prepared(B, out=None, handle=None, stream=None):
+    """C = A * B for the A prepared on `handle` (Handle.prepare_a); bitwise equal to tprod_f32(A, B)."""
+    import torch
+    h = handle
+    if h is None or getattr(h, "prepared", None) is None:
+        raise ValueError("tprod_prepared needs a handle with a prepared A (Handle.prepare_a)")
+    n1, n2, n3 = h.prepared
+    if B.dim() != 3 or B.shape[0] != n2 or B.shape[2] != n3:
+        raise ValueError(f"t-product shape mismatch: prepared A ({n1}, {n2}, {n3}) vs B {tuple(B.shape)}")
+    if B.dtype != torch.float32 or not B.is_cuda or not is_matlab_layout(B):
+        raise ValueError("B must be a float32 CUDA tensor in the Matlab layout")
+    n4 = int(B.shape[1])
+    if out is None:
+        out = matlab_empty(n1, n4, n3, torch.float32, B.device)
+    elif tuple(out.shape) != (n1, n4, n3) or not is_matlab_layout(out) or out.dtype != torch.float32:
+        raise ValueError("out must be a Matlab-layout n1 x n4 x n3 float32 tensor")
+    s = stream if stream is not None else torch.cuda.current_stream(B.device)
+    check(lib().tprod_f32_prepared(B.data_ptr(), out.data_ptr(), n4, C.c_void_p(s.cuda_stream), h.ptr),
+          "tprod_f32_prepared")
     return out
 
 

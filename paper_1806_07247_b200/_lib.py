@@ -35,6 +35,9 @@ SIGNATURES = {
     "tprod_idft_f32": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "tprod_set_option": (_int, [_vp, _int, _i64]),
     "tprod_last_stage_ms": (_int, [_vp, C.POINTER(C.c_float)]),
+    "tprod_prepare_a_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    "tprod_f32_prepared": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "tprod_release_a": (_int, [_vp]),
 }
 
 _lib = None

@@ -21,6 +21,17 @@
 
 using namespace tprod;
 
+// Prepared left operand (tprod_prepare_a_f32): A's row unscale vector and split spectrum planes.
+struct PreparedA {
+  bool valid = false;
+  int64_t n1 = 0, n2 = 0, n3 = 0, lda = 0, h = 0;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  unsigned* maxA = nullptr;
+  float* uA = nullptr;
+  __half* Ab = nullptr;
+};
+
 struct tprod_ctx {
   int device = 0;
   int num_sms = 148;
@@ -41,6 +52,7 @@ struct tprod_ctx {
   bool timing = false;
   bool timed_last = false;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  PreparedA prep;
 };
 
 namespace {
@@ -85,7 +97,8 @@ struct Layout32 {
 };
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
+// with_A = false: no A-bar region (prepared-operand calls read the handle's prepared planes)
+Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = true) {
   Layout32 L;
   L.h = h_slices(n3);
   L.lda = round_up(n1, 8);   // 16-byte row pitch for TMA (fp16)
@@ -96,7 +109,7 @@ Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
   L.off_maxB = o; o = align_up(o + 4 * (size_t)n4, 1024);
   L.off_uA = o;   o = align_up(o + 4 * (size_t)n1, 1024);
   L.off_uB = o;   o = align_up(o + 4 * (size_t)n4, 1024);
-  L.off_Ab = o;  o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
+  L.off_Ab = o;  if (with_A) o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
   L.off_Bb = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n4 * L.ldb), 1024);
   L.off_Cb = o;   o = align_up(o + 4 * (size_t)(L.h * 2 * n4 * L.ldc), 1024);
   L.total = o;
@@ -231,9 +244,10 @@ NcclApi& nccl() {
 }
 
 // ---------------------------------------------------------------- the hot path
+// pa != nullptr: A is the handle's prepared operand (A itself is not read; K0/K1 run for B only)
 int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2,
-            int64_t n3, int64_t n4, cudaStream_t s) {
-  Layout32 L = layout32(n1, n2, n3, n4);
+            int64_t n3, int64_t n4, cudaStream_t s, const PreparedA* pa = nullptr) {
+  Layout32 L = layout32(n1, n2, n3, n4, pa == nullptr);
   int st = ensure_ws(h, L.total);
   if (st) return st;
   Twiddles32 T;
@@ -242,9 +256,9 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   char* ws = (char*)h->ws;
   unsigned* maxA = (unsigned*)(ws + L.off_maxA);
   unsigned* maxB = (unsigned*)(ws + L.off_maxB);
-  float* uA = (float*)(ws + L.off_uA);
+  float* uA = pa ? pa->uA : (float*)(ws + L.off_uA);
   float* uB = (float*)(ws + L.off_uB);
-  __half* Ab = (__half*)(ws + L.off_Ab);
+  __half* Ab = pa ? pa->Ab : (__half*)(ws + L.off_Ab);
   __half* Bb = (__half*)(ws + L.off_Bb);
   float* Cb = (float*)(ws + L.off_Cb);
   int64_t launches = 0;
@@ -253,12 +267,16 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   h->timed_last = false;
   mark(0);
   CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_uA - L.off_maxA, s));
-  launch_absmax2(A, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
-  launches += (n1 % 4 == 0 && n2 % 4 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 2;
+  const float* A0 = pa ? nullptr : A;
+  launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
+  const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0;
+  launches += vec ? 1 : (A0 ? 2 : 1);
   mark(1);
   // B first: the tail of B just streamed by K0 is still resident in L2
   launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
-  launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
+  if (!pa) {
+    launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
+  }
   mark(2);
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
@@ -364,6 +382,7 @@ int tprod_destroy(tprod_handle h) {
   for (auto& kv : h->st32) cudaFree(kv.second);
   for (auto& kv : h->tw64) cudaFree(kv.second);
   for (int i = 0; i < 3; ++i) if (h->hbuf[i]) cudaFree(h->hbuf[i]);
+  if (h->prep.buf) cudaFree(h->prep.buf);
   if (h->ws) cudaFree(h->ws);
   delete h;
   return TPROD_OK;
@@ -393,6 +412,63 @@ int tprod_f32_host(const float* A, const float* B, float* C, int64_t n1, int64_t
 int tprod_f64_host(const double* A, const double* B, double* C, int64_t n1, int64_t n2, int64_t n3,
                    int64_t n4, void* stream, tprod_handle h) {
   return host_call(A, B, C, n1, n2, n3, n4, stream, h);
+}
+
+int tprod_prepare_a_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h) {
+  if (!h || !A) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, 1);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  PreparedA& P = h->prep;
+  const int64_t hh = h_slices(n3), lda = round_up(n1, 8);
+  const size_t off_u = align_up(4 * (size_t)n1, 1024);
+  const size_t off_Ab = off_u + align_up(4 * (size_t)n1, 1024);
+  const size_t bytes = off_Ab + 2 * (size_t)(hh * NPLANES * n2 * lda);
+  if (P.bytes < bytes) {
+    if (P.buf) {
+      CK(cudaDeviceSynchronize());
+      cudaFree(P.buf);
+      P.buf = nullptr;
+      P.bytes = 0;
+    }
+    if (cudaMalloc(&P.buf, bytes) != cudaSuccess) { cudaGetLastError(); P.valid = false; return TPROD_ENOMEM; }
+    P.bytes = bytes;
+  }
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
+  P.maxA = (unsigned*)P.buf;
+  P.uA = (float*)((char*)P.buf + off_u);
+  P.Ab = (__half*)((char*)P.buf + off_Ab);
+  CK(cudaMemsetAsync(P.maxA, 0, 4 * (size_t)n1, s));
+  launch_absmax2(A, nullptr, n1, n2, n3, 1, P.maxA, nullptr, h->num_sms, s);               // K0 (A)
+  launch_fwd_split(A, n1, n2, n3, 0, P.maxA, T, P.Ab, lda, P.uA, h->num_sms, s);         // K1 (A)
+  if ((st = launch_status())) { P.valid = false; return st; }
+  P.valid = true;
+  P.n1 = n1; P.n2 = n2; P.n3 = n3; P.lda = lda; P.h = hh;
+  return TPROD_OK;
+}
+
+int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod_handle h) {
+  if (!h || !B || !C || !h->prep.valid) return TPROD_EINVAL;
+  const PreparedA& P = h->prep;
+  int st = validate_dims(P.n1, P.n2, P.n3, n4);
+  if (st) return st;
+  if (overlaps(C, 4 * (size_t)(P.n1 * n4 * P.n3), B, 4 * (size_t)(P.n2 * n4 * P.n3))) return TPROD_EALIAS;
+  CK(cudaSetDevice(h->device));
+  return run_f32(h, nullptr, B, C, P.n1, P.n2, P.n3, n4, (cudaStream_t)stream, &P);
+}
+
+int tprod_release_a(tprod_handle h) {
+  if (!h) return TPROD_EINVAL;
+  if (h->prep.buf) {
+    CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());
+    cudaFree(h->prep.buf);
+  }
+  h->prep = PreparedA();
+  return TPROD_OK;
 }
 
 int tprod_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t n4, int dtype, size_t* out) {

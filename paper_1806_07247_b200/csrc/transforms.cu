@@ -152,14 +152,16 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
 
 void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int64_t n3, int64_t n4,
                     unsigned* maxA, unsigned* maxB, int num_sms, cudaStream_t s) {
-  const bool vec = n1 % 4 == 0 && n2 % 4 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0;
+  // A or B may be null (prepared-operand calls): that operand's part is skipped
+  const bool vec = (!A || (n1 % 4 == 0 && ((uintptr_t)A & 15) == 0)) && n2 % 4 == 0 &&
+                   (!B || ((uintptr_t)B & 15) == 0);
   if (!vec) {
-    launch_absmax(A, n1, n2, n3, 0, maxA, s);
-    launch_absmax(B, n2, n4, n3, 1, maxB, s);
+    if (A) launch_absmax(A, n1, n2, n3, 0, maxA, s);
+    if (B) launch_absmax(B, n2, n4, n3, 1, maxB, s);
     return;
   }
   // split ~8 CTAs per SM between the two tensors in proportion to their sizes
-  const double szA = (double)n1 * n2 * n3, szB = (double)n2 * n4 * n3;
+  const double szA = A ? (double)n1 * n2 * n3 : 0.0, szB = B ? (double)n2 * n4 * n3 : 0.0;
   const int64_t total = (int64_t)num_sms * 8;
   int64_t nbA_target = (int64_t)(total * szA / (szA + szB));
   if (nbA_target < 1) nbA_target = 1;
@@ -171,10 +173,12 @@ void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int6
   const int64_t maxgy = (colsA + 256 / txv - 1) / (256 / txv);
   if (gyA > maxgy) gyA = maxgy;
   if (gyA < 1) gyA = 1;
+  if (!A) gyA = 0;
   int64_t nbB = total - gxA * gyA;
   const int64_t runsB = n4 * n3;
   if (nbB > (runsB + 7) / 8) nbB = (runsB + 7) / 8;      // at most one run per warp
   if (nbB < 1) nbB = 1;
+  if (!B) nbB = 0;
   absmax2_kernel<<<(unsigned)(gxA * gyA + nbB), 256, 0, s>>>(A, n1, colsA, (int)gyA, (int)gxA, txv, B, n2,
                                                              n4, n3, maxA, maxB);
 }

@@ -182,6 +182,31 @@ def test_tube_transforms_match_register_kernels(T, n3):
     assert O.rel_err(C0, C1) <= 1e-6
 
 
+@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (256, 128, 64, 96), (64, 40, 100, 24), (7, 5, 2, 3)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_prepared_operand_bitwise(T, dims):
+    """NEXT-1 prepared left operand: tprod_prepare_a_f32 once, tprod_f32_prepared for several B --
+    bitwise equal to tprod_f32 (same kernels, same operands, same K order); within the oracle
+    tolerance; errors when nothing is prepared."""
+    import torch
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 61 + n3)
+    h = T.Handle()
+    with pytest.raises(ValueError):
+        T.tprod_prepared(dev(normal((n2, n4, n3), 1)), handle=h)
+    assert h.ptr and T._lib.lib().tprod_f32_prepared(None, None, n4, None, h.ptr) == T._lib.TPROD_EINVAL
+    h.prepare_a(dev(A))
+    for seed in (62, 63):
+        B = normal((n2, n4 + seed - 62, n3), seed)
+        ref = gpu_tprod(T, A, B)
+        got = host(T.tprod_prepared(dev(B), handle=h))
+        assert np.array_equal(got, ref)
+        assert O.rel_err(got, O.tprod_columns(A, B, np.arange(B.shape[1]))) <= TOL32
+    h.release_a()
+    with pytest.raises(ValueError):
+        T.tprod_prepared(dev(B), handle=h)
+
+
 def test_worked_examples_on_gpu(T, golden):
     for dt in (np.float32, np.float64):
         g = golden["tprod_tubes_1x1x3"]
