@@ -588,18 +588,19 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   const uint32_t tmem = *tmem_slot;
 
   // Tile order: n fastest, then m, then f; concurrently running pairs share the A_f panel.
-  // (Measured on config 5: grouping GM m-tiles per n sweep, sized so the A panels fit L2, RAISES
-  // DRAM reads from 149 to 170 GB per launch -- the pairs drift apart in K by up to a tile, longer
-  // than an L2 residency -- so the plain order stays.  GM = 0 keeps it.)
+  // (Measured on config 5, DRAM read per launch: n fastest 149-165 GB, m fastest 185 GB, groups of
+  // 6 m-tiles per n sweep 180 GB -- the pairs drift apart in K by up to a tile, longer than an L2
+  // residency, so no raster order recovers the reuse; the plain order stays.  GM = 0 keeps it.)
   const int64_t tpf = (int64_t)mt * nt;
   auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {
     f = (int)(t / tpf);
     const int r = (int)(t - (int64_t)f * tpf);
-    if (GM <= 0) {
+    if (GM == 0) {
       n0 = (r % nt) * BN;
       m0 = (r / nt) * (2 * BM);
       return;
     }
+
     const int grp = r / (GM * nt), w = r - grp * GM * nt;
     const int gm = min(GM, mt - grp * GM);
     n0 = (w / gm) * BN;
