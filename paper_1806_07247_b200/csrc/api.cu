@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -93,7 +94,7 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 // ---------------------------------------------------------------- workspace layout
 struct Layout32 {
   int64_t h, lda, ldb, ldc;
-  size_t off_maxA, off_maxB, off_uA, off_uB, off_Ab, off_Bb, off_Cb, total;
+  size_t off_maxA, off_maxB, off_uA, off_uB, off_Ab, off_Bb, off_Cb, off_W, W_bytes, total;
 };
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -112,6 +113,11 @@ Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = 
   L.off_Ab = o;  if (with_A) o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
   L.off_Bb = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n4 * L.ldb), 1024);
   L.off_Cb = o;   o = align_up(o + 4 * (size_t)(L.h * 2 * n4 * L.ldc), 1024);
+  // four-step long-tube forward: intermediate the size of the larger operand
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  L.W_bytes = f1 ? 4 * (size_t)(std::max(with_A ? n1 * n2 : 0, n2 * n4) * n3) : 0;
+  L.off_W = o;    o = align_up(o + L.W_bytes, 1024);
   L.total = o;
   return L;
 }
@@ -185,6 +191,14 @@ int get_twiddles32(tprod_ctx* h, int n3, Twiddles32* T) {
   int st = get_tw32(h, n3, &tw);
   if (st) return st;
   *T = Twiddles32{tw, n3, nullptr};
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  if (f1) {
+    Twiddles32 T1, T2;
+    if ((st = get_twiddles32(h, f1, &T1)) || (st = get_twiddles32(h, f2, &T2))) return st;
+    T->st_n1 = T1.st;
+    T->st_n2 = T2.st;
+  }
   if (!fft_supported(n3) && !tube_supported(n3)) return TPROD_OK;
   auto it = h->st32.find(n3);
   if (it != h->st32.end()) { T->st = it->second; return TPROD_OK; }
@@ -254,6 +268,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   T.staged = h->transform == 0;
   char* ws = (char*)h->ws;
+  T.scratch = L.W_bytes ? (float*)(ws + L.off_W) : nullptr;
+  T.scratch_bytes = L.W_bytes;
   unsigned* maxA = (unsigned*)(ws + L.off_maxA);
   unsigned* maxB = (unsigned*)(ws + L.off_maxB);
   float* uA = pa ? pa->uA : (float*)(ws + L.off_uA);
@@ -554,9 +570,16 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   int64_t nmax = role == 0 ? p : q;
   size_t off_u = align_up(4 * (size_t)nmax, 1024);
   size_t off_sp = off_u + align_up(4 * (size_t)nmax, 1024);
-  if ((st = ensure_ws(h, off_sp + 2 * (size_t)(hh * NPLANES * q * ld)))) return st;
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  const size_t w_bytes = f1 ? 4 * (size_t)(p * q * n3) : 0;            // four-step intermediate
+  const size_t off_w = align_up(off_sp + 2 * (size_t)(hh * NPLANES * q * ld), 1024);
+  if ((st = ensure_ws(h, off_w + w_bytes))) return st;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
+  T.scratch = w_bytes ? (float*)((char*)h->ws + off_w) : nullptr;
+  T.scratch_bytes = w_bytes;
   unsigned* mx = (unsigned*)h->ws;
   float* u = (float*)((char*)h->ws + off_u);
   __half* sp = (__half*)((char*)h->ws + off_sp);

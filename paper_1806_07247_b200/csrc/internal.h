@@ -23,6 +23,12 @@ struct Twiddles32 {
   int n3;
   const float2* st = nullptr;    // Stockham per-pass twiddle table (FFT path only), see transforms_fft.cu
   int staged = 1;                // 0: skip the TMA-staged / tube kernels (TPROD_OPT_TRANSFORM = 1)
+  // four-step long-tube forward (n3 = N1*N2 in {4096, 8192, 16384}): Stockham tables of the two
+  // factors and a workspace the size of the larger operand
+  const float2* st_n1 = nullptr;
+  const float2* st_n2 = nullptr;
+  float* scratch = nullptr;
+  size_t scratch_bytes = 0;
 };
 struct Twiddles64 { const double2* tw; int n3; };
 
@@ -76,6 +82,13 @@ bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t 
 // `st` = Stockham table of host_stockham_table.  false = not handled.  The inverse requires C-bar
 // in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld).
 bool tube_supported(int64_t n3);
+// Four-step two-pass forward for long power-of-two tubes (transforms_tma.cu); false = not handled.
+void fourstep_factors(int64_t n3, int* n1, int* n2);
+bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                      const Twiddles32& tw, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
+// inverse: C-bar in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld)
+bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw, float* X,
+                      int num_sms, cudaStream_t s);
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,

@@ -255,6 +255,8 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
     cudaGetLastError();
   }
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
+  if (tw.staged && launch_fwd_4step(X, P, Q, n3, role, maxbits, tw, out, ld, unscale, num_sms, s)) return;
+  cudaGetLastError();
   if (tw.st && launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
@@ -326,6 +328,8 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   if (prod_layout && launch_inv_tma(Cre, ld, P, Q, n3, X, num_sms, s)) return;
   cudaGetLastError();
   if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, X, num_sms, s)) return;
+  cudaGetLastError();
+  if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, X, num_sms, s)) return;
   cudaGetLastError();
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, X, s)) return;
   if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, X, s)) return;

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <algorithm>
 #include <vector>
 
 namespace tprod {
@@ -312,15 +313,15 @@ __host__ __device__ constexpr int tube_toff(int log, int i) {
   return i <= 1 ? 0 : tube_toff(log, i - 1) + (tube_R(log, i - 1) - 1) * tube_Ns(i - 1);
 }
 
-template <int N, int F, int R, int Ns, int DIR>
+template <int N, int F, int R, int Ns, int DIR, int NT = TUBE_NT>
 __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp) {
   constexpr int NB = N / R;
-  constexpr int BPT = F * NB / TUBE_NT;
-  static_assert(F * NB % TUBE_NT == 0, "butterflies must divide evenly");
+  constexpr int BPT = F * NB / NT;
+  static_assert(F * NB % NT == 0, "butterflies must divide evenly");
   float2 v[BPT][R];
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
-    const int b = threadIdx.x + u * TUBE_NT;
+    const int b = threadIdx.x + u * NT;
     const int c = b % F, j = b / F, k = j % Ns;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[u][r] = z[(j + r * NB) * F + c];
@@ -333,7 +334,7 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
-    const int b = threadIdx.x + u * TUBE_NT;
+    const int b = threadIdx.x + u * NT;
     const int c = b % F, j = b / F, k = j % Ns, g = j / Ns;
 #pragma unroll
     for (int r = 0; r < R; ++r) z[(g * Ns * R + k + r * Ns) * F + c] = v[u][r];
@@ -341,11 +342,11 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
   __syncthreads();
 }
 
-template <int N, int DIR>
+template <int N, int DIR, int F = TubeCfg<N>::F, int NT = TUBE_NT>
 __device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st) {
   using C = TubeCfg<N>;
-  tube_pass<N, C::F, tube_R(C::LOG, 0), tube_Ns(0), DIR>(z, st);
-  if constexpr (C::NP > 1) tube_pass<N, C::F, tube_R(C::LOG, 1), tube_Ns(1), DIR>(z, st + tube_toff(C::LOG, 1));
+  tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT>(z, st);
+  if constexpr (C::NP > 1) tube_pass<N, F, tube_R(C::LOG, 1), tube_Ns(1), DIR, NT>(z, st + tube_toff(C::LOG, 1));
 }
 
 // K1 epilogue staged in shared memory: the item's 4h output rows (f, plane) of TUB halves are
@@ -444,6 +445,315 @@ __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant
       else if (p < P) xo[PQ * k + 2 * c] = v.x * inv_n;
     }
   });
+}
+
+// ------------------------------------------------------------------------------ four-step K1
+// Long power-of-two tubes, N = N1 * N2 (N1, N2 in {64, 128}: n3 = 4096, 8192, 16384).  With
+// k = k1 + N1 k2 and f = N2 f1 + f2 (Eq. (2) split into two short DFTs, the four-step form of the
+// FFT of PAPER.md:L102):
+//   pass 1:  Y[k1, f2] = w_N^{k1 f2} sum_{k2} x[k1 + N1 k2] w_{N2}^{k2 f2}      (stored at row k1 + N1 f2)
+//   pass 2:  X[N2 f1 + f2] = sum_{k1} Y[k1, f2] w_{N1}^{k1 f1}
+// Both passes are tube-parallel (TUB consecutive tubes side by side, two real tubes per complex
+// FFT): TMA gathers the N2 rows k1 + N1 k2 (pass 1) or the N1 rows k1 + N1 f2 (pass 2) of a 4-D view
+// {p, q, k1, k2} of the tensor, so every row moved is TUB*4 contiguous bytes (vs 32 bytes for the
+// one-pass kernel, whose 8 tubes x N points fill a CTA's shared memory).  The intermediate Y has
+// the input's shape (W, a workspace the size of the larger operand).  Pass 2 handles f2 together
+// with N2 - f2, so both X_f and X_{N-f} of the real-pair separation are in shared memory.
+template <int N2, int TUB>
+__global__ void __launch_bounds__(2 * TUB) fwd4_pass1_kernel(const __grid_constant__ CUtensorMap mX4,
+                                                            const __grid_constant__ CUtensorMap mW4, int64_t P,
+                                                            int64_t Q, int N1, const float2* __restrict__ st2,
+                                                            const float2* __restrict__ twN) {
+  constexpr int F = TUB / 2, NT = 2 * TUB;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full;
+  float2* z = reinterpret_cast<float2*>(smem);      // z[k2][c]
+  if (threadIdx.x == 0) {
+    bar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  const int64_t items = pblocks * Q * N1;
+  uint32_t ph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1) {
+    const int k1 = (int)(it % N1);
+    const int64_t r = it / N1;
+    const int64_t q = r / pblocks, p0 = (r - q * pblocks) * TUB;
+    if (threadIdx.x == 0) {
+      bulk_wait_read();                             // the previous item's store has read z
+      fence_async_smem();
+      bar_expect(&full, TUB * N2 * 4);
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+          ::"r"(su32(smem)), "l"(&mX4), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(k1), "r"(0)
+          : "memory");
+    }
+    bar_wait(&full, ph);
+    tube_fft<N2, -1, F, NT>(z, st2);                 // over k2 -> z[f2][c]
+    for (int idx = threadIdx.x; idx < N2 * F; idx += NT) {
+      const int f2 = idx / F;
+      const float2 t = __ldg(twN + k1 * f2);          // w_N^{k1 f2} = (cos, -sin), k1 f2 < N
+      z[idx] = cmul(z[idx], make_float2(t.x, -t.y));
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+                   ::"l"(&mW4), "r"(su32(smem)), "r"((int)p0), "r"((int)q), "r"(k1), "r"(0)
+                   : "memory");
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <int N1, int TUB, int ROLE>
+__global__ void __launch_bounds__(2 * TUB) fwd4_pass2_kernel(const __grid_constant__ CUtensorMap mW4, int64_t P,
+                                                            int64_t Q, int N2, const unsigned* __restrict__ maxbits,
+                                                            const float2* __restrict__ st1, __half* __restrict__ out,
+                                                            int64_t ld, float* __restrict__ unscale) {
+  constexpr int F = TUB / 2, NT = 2 * TUB;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full;
+  float2* za = reinterpret_cast<float2*>(smem);               // [f1][c] of column f2
+  float2* zb = za + N1 * F;                                   // [f1][c] of column N2 - f2
+  const int N = N1 * N2;
+  if (threadIdx.x == 0) {
+    bar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  const int half = N2 / 2;
+  const int64_t items = pblocks * Q * (half + 1);
+  const int64_t plane = Q * ld;
+  const int c = threadIdx.x % F;                                // NT % F == 0
+  uint32_t ph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1) {
+    const int f2 = (int)(it % (half + 1));
+    const int64_t r = it / (half + 1);
+    const int64_t q = r / pblocks, p0 = (r - q * pblocks) * TUB;
+    const int f2b = (N2 - f2) % N2;
+    const bool two = f2b != f2;
+    if (threadIdx.x == 0) {
+      bar_expect(&full, (two ? 2 : 1) * TUB * N1 * 4);
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+          ::"r"(su32(za)), "l"(&mW4), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(0), "r"(f2)
+          : "memory");
+      if (two)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+            ::"r"(su32(zb)), "l"(&mW4), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(0), "r"(f2b)
+            : "memory");
+    }
+    bar_wait(&full, ph);
+    tube_fft<N1, -1, F, NT>(za, st1);                           // over k1 -> X[N2 f1 + f2]
+    if (two) tube_fft<N1, -1, F, NT>(zb, st1);
+    // ---- Hermitian half, real-pair separation, 2^e scaling, fp16 hi/lo split
+    const int64_t p = p0 + 2 * c;
+    if (p < P) {
+      const bool in1 = p + 1 < P;
+      int e0 = 0, e1 = 0;
+      if (ROLE == 0) {
+        e0 = scale_exp(__ldg(maxbits + p), N);
+        if (in1) e1 = scale_exp(__ldg(maxbits + p + 1), N);
+        if (q == 0 && f2 == 0 && threadIdx.x < F) {
+          unscale[p] = pow2f(-e0);
+          if (in1) unscale[p + 1] = pow2f(-e1);
+        }
+      } else {
+        e0 = e1 = scale_exp(__ldg(maxbits + q), N);
+        if (p0 == 0 && f2 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
+      }
+      const float s0 = pow2f(e0), s1 = pow2f(e1);
+      __half* o = out + q * ld + p;
+      for (int t = 0; t < (two ? 2 : 1); ++t) {
+        const float2* zt = t == 0 ? za : zb;
+        const float2* zo = t == 0 ? zb : za;                    // tile holding the partners
+        const int fc = t == 0 ? f2 : f2b;
+        for (int f1 = threadIdx.x / F; f1 < N1; f1 += NT / F) {
+          const int f = N2 * f1 + fc;
+          if (2 * f > N) continue;
+          const float2 zf = zt[f1 * F + c];
+          // X_{N-f}: f2 = 0 -> row (N1 - f1) mod N1 of the same column, else row N1-1-f1 of N2 - f2
+          const float2 zm = fc == 0 ? zt[((N1 - f1) % N1) * F + c] : (two ? zo : zt)[(N1 - 1 - f1) * F + c];
+          const float2 re = make_float2(0.5f * (zf.x + zm.x) * s0, 0.5f * (zf.y + zm.y) * s1);
+          const float2 im = make_float2(0.5f * (zf.y - zm.y) * s0, -0.5f * (zf.x - zm.x) * s1);
+          const __half2 rh = __float22half2_rn(re), ih = __float22half2_rn(im);
+          const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
+          const __half2 rl = __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));
+          const __half2 il = __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));
+          __half* of = o + (int64_t)(4 * f) * plane;
+          if (in1) {
+            *reinterpret_cast<__half2*>(of + PL_RE_HI * plane) = rh;
+            *reinterpret_cast<__half2*>(of + PL_RE_LO * plane) = rl;
+            *reinterpret_cast<__half2*>(of + PL_IM_HI * plane) = ih;
+            *reinterpret_cast<__half2*>(of + PL_IM_LO * plane) = il;
+          } else {
+            of[PL_RE_HI * plane] = __low2half(rh);
+            of[PL_RE_LO * plane] = __low2half(rl);
+            of[PL_IM_HI * plane] = __low2half(ih);
+            of[PL_IM_LO * plane] = __low2half(il);
+          }
+        }
+      }
+    }
+    __syncthreads();                                            // tiles consumed before the next loads
+  }
+}
+
+// ------------------------------------------------------------------------------ four-step K3
+// Inverse (Alg. 1 step 2b + 3, L177-179) for the same long tubes, f = f1 + N1 f2, k = N2 k1 + k2:
+//   pass 1:  U[f1, k2] = w_N^{-f1 k2} sum_{f2} Z[f1 + N1 f2] w_{N2}^{-f2 k2}     (stored at row f1 + N1 k2)
+//   pass 2:  z[N2 k1 + k2] = (1/N) sum_{f1} U[f1, k2] w_{N1}^{-f1 k1}
+// with Z_f = X_f + i Y_f of two real tubes and the conjugate fill Z_f = conj X_{N-f} + i conj Y_{N-f}
+// for f > N/2 (Im of DC / Nyquist dropped).  Pass 1 reads C-bar through a 5-D view
+// {p, q, re|im, f1, f2} (row 2f + re|im, f = f1 + N1 f2, f2 <= N2/2) and handles column f1 together
+// with its mirror N1 - f1, whose rows hold X_{N-f}.
+template <int N2, int TUB>
+__global__ void __launch_bounds__(2 * TUB) inv4_pass1_kernel(const __grid_constant__ CUtensorMap mC5,
+                                                            const __grid_constant__ CUtensorMap mW4, int64_t P,
+                                                            int64_t Q, int N1, const float2* __restrict__ st2,
+                                                            const float2* __restrict__ twN) {
+  constexpr int F = TUB / 2, NT = 2 * TUB;
+  constexpr int RB = N2 / 2 + 1;                              // f2 rows per column tile
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full;
+  float* ca = smem;                                           // [f2][re|im][TUB] of column f1
+  float* cb = ca + RB * 2 * TUB;                              // ... of column N1 - f1
+  float2* za = reinterpret_cast<float2*>(cb + RB * 2 * TUB);  // Z / U of column f1: [f2|k2][c]
+  float2* zb = za + N2 * F;                                   // ... of column N1 - f1
+  const int N = N1 * N2;
+  if (threadIdx.x == 0) {
+    bar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  const int hc = N1 / 2;
+  const int64_t items = pblocks * Q * (hc + 1);
+  uint32_t ph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1) {
+    const int f1 = (int)(it % (hc + 1));
+    const int64_t r = it / (hc + 1);
+    const int64_t q = r / pblocks, p0 = (r - q * pblocks) * TUB;
+    const int f1b = (N1 - f1) % N1;
+    const bool two = f1b != f1;
+    if (threadIdx.x == 0) {
+      bulk_wait_read();                                       // previous item's stores have read za/zb
+      fence_async_smem();
+      bar_expect(&full, (two ? 2 : 1) * RB * 2 * TUB * 4);
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+          ::"r"(su32(ca)), "l"(&mC5), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(0), "r"(f1), "r"(0)
+          : "memory");
+      if (two)
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];"
+            ::"r"(su32(cb)), "l"(&mC5), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(0), "r"(f1b), "r"(0)
+            : "memory");
+    }
+    bar_wait(&full, ph);
+    // Z of column fc (t = 0: f1, t = 1: f1b), f = fc + N1 f2: own rows for f <= N/2, the other
+    // column's mirrored rows otherwise
+    for (int t = 0; t < (two ? 2 : 1); ++t) {
+      const int fc = t == 0 ? f1 : f1b;
+      const float* own = t == 0 ? ca : cb;
+      const float* oth = two ? (t == 0 ? cb : ca) : ca;
+      float2* z = t == 0 ? za : zb;
+      for (int idx = threadIdx.x; idx < N2 * F; idx += NT) {
+        const int f2 = idx / F, c = idx % F;
+        const int f = fc + N1 * f2;
+        float2 v;
+        if (2 * f <= N) {
+          const bool self = (f == 0 || 2 * f == N);
+          const float2 re = reinterpret_cast<const float2*>(own + (f2 * 2) * TUB)[c];
+          const float2 im = self ? make_float2(0.f, 0.f) : reinterpret_cast<const float2*>(own + (f2 * 2 + 1) * TUB)[c];
+          v = make_float2(re.x - im.y, im.x + re.y);            // X_f + i Y_f
+        } else {
+          const int g2 = fc == 0 ? N2 - f2 : N2 - 1 - f2;        // row of g = N - f in column (N1 - fc) mod N1
+          const float* src = fc == 0 ? own : oth;
+          const float2 re = reinterpret_cast<const float2*>(src + (g2 * 2) * TUB)[c];
+          const float2 im = reinterpret_cast<const float2*>(src + (g2 * 2 + 1) * TUB)[c];
+          v = make_float2(re.x + im.y, re.y - im.x);            // conj X_g + i conj Y_g
+        }
+        z[idx] = v;
+      }
+    }
+    __syncthreads();
+    tube_fft<N2, +1, F, NT>(za, st2);                         // over f2 -> [k2][c]
+    if (two) tube_fft<N2, +1, F, NT>(zb, st2);
+    for (int t = 0; t < (two ? 2 : 1); ++t) {
+      const int fc = t == 0 ? f1 : f1b;
+      float2* z = t == 0 ? za : zb;
+      for (int idx = threadIdx.x; idx < N2 * F; idx += NT) {
+        const int k2 = idx / F;
+        const float2 w = __ldg(twN + fc * k2);                // w_N^{-fc k2} = (cos, +sin)
+        z[idx] = cmul(z[idx], w);
+      }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+                   ::"l"(&mW4), "r"(su32(za)), "r"((int)p0), "r"((int)q), "r"(f1), "r"(0)
+                   : "memory");
+      if (two)
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+                     ::"l"(&mW4), "r"(su32(zb)), "r"((int)p0), "r"((int)q), "r"(f1b), "r"(0)
+                     : "memory");
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <int N1, int TUB>
+__global__ void __launch_bounds__(2 * TUB) inv4_pass2_kernel(const __grid_constant__ CUtensorMap mW4,
+                                                            const __grid_constant__ CUtensorMap mX4t, int64_t P,
+                                                            int64_t Q, int N2, const float2* __restrict__ st1) {
+  constexpr int F = TUB / 2, NT = 2 * TUB;
+  extern __shared__ __align__(128) float smem[];
+  __shared__ uint64_t full;
+  float2* z = reinterpret_cast<float2*>(smem);                // [f1 -> k1][c]
+  const float inv_n = 1.f / (float)(N1 * N2);
+  if (threadIdx.x == 0) {
+    bar_init(&full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  const int64_t items = pblocks * Q * N2;
+  uint32_t ph = 0;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1) {
+    const int k2 = (int)(it % N2);
+    const int64_t r = it / N2;
+    const int64_t q = r / pblocks, p0 = (r - q * pblocks) * TUB;
+    if (threadIdx.x == 0) {
+      bulk_wait_read();
+      fence_async_smem();
+      bar_expect(&full, TUB * N1 * 4);
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+          ::"r"(su32(smem)), "l"(&mW4), "r"(su32(&full)), "r"((int)p0), "r"((int)q), "r"(0), "r"(k2)
+          : "memory");
+    }
+    bar_wait(&full, ph);
+    tube_fft<N1, +1, F, NT>(z, st1);                          // over f1 -> z[k1][c]
+    for (int idx = threadIdx.x; idx < N1 * F; idx += NT) z[idx] = make_float2(z[idx].x * inv_n, z[idx].y * inv_n);
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // rows k = k2 + N2 k1 of X through the view {p, q, k2, k1}
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+                   ::"l"(&mX4t), "r"(su32(smem)), "r"((int)p0), "r"((int)q), "r"(k2), "r"(0)
+                   : "memory");
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------ tables / launch
@@ -605,9 +915,145 @@ bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const
   return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
 }
 
+
+// 4-D fp32 view {P, Q, N1, N2} of a Matlab-layout P x Q x (N1 N2) tensor (row k1 + N1 k2), box
+// {TUB, 1, b2, b3}
+bool map_f32_4d(CUtensorMap* m, const void* base, uint64_t P, uint64_t Q, uint64_t N1, uint64_t N2, uint32_t tub,
+                uint32_t b2, uint32_t b3) {
+  auto fn = encode();
+  if (!fn || (P * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0) return false;
+  cuuint64_t dims[4] = {P, Q, N1, N2};
+  cuuint64_t strides[3] = {P * 4, P * Q * 4, P * Q * N1 * 4};
+  cuuint32_t box[4] = {tub, 1, b2, b3};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N1, int N2, int TUB>
+bool launch_fwd4_t(const float* X, int64_t P, int64_t Q, int role, const unsigned* maxbits, const Twiddles32& tw,
+                   __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
+  CUtensorMap mx, mw1, mw2;
+  if (!map_f32_4d(&mx, X, P, Q, N1, N2, TUB, 1, N2) || !map_f32_4d(&mw1, tw.scratch, P, Q, N1, N2, TUB, 1, N2) ||
+      !map_f32_4d(&mw2, tw.scratch, P, Q, N1, N2, TUB, N1, 1))
+    return false;
+  const void* k1 = (const void*)fwd4_pass1_kernel<N2, TUB>;
+  const void* k2 = role == 0 ? (const void*)fwd4_pass2_kernel<N1, TUB, 0> : (const void*)fwd4_pass2_kernel<N1, TUB, 1>;
+  const size_t sm1 = sizeof(float) * TUB * N2, sm2 = 2 * sizeof(float) * TUB * N1;
+  if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1) != cudaSuccess ||
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2) != cudaSuccess)
+    return false;
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  int per1 = 1, per2 = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, 2 * TUB, sm1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k2, 2 * TUB, sm2);
+  const int64_t it1 = pblocks * Q * N1, it2 = pblocks * Q * (N2 / 2 + 1);
+  const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
+  const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
+  int n1i = N1, n2i = N2;
+  const float2* st1 = tw.st_n1;
+  const float2* st2 = tw.st_n2;
+  const float2* twn = tw.tw;
+  void* a1[] = {(void*)&mx, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn};
+  if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
+  void* a2[] = {(void*)&mw2, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&maxbits, (void*)&st1, (void*)&out, (void*)&ld,
+                (void*)&unscale};
+  return cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) == cudaSuccess;
+}
+
+// 5-D fp32 view {P (pitch ld), Q, 2, N1, R2} of C-bar planes [f][re|im][q][ld] with f = f1 + N1 f2,
+// box {tub, 1, 2, 1, R2}
+bool map_cbar_5d(CUtensorMap* m, const void* base, uint64_t P, uint64_t ld, uint64_t Q, uint64_t N1, uint64_t R2,
+                 uint32_t tub) {
+  auto fn = encode();
+  if (!fn || (ld * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0) return false;
+  cuuint64_t dims[5] = {P, Q, 2, N1, R2};
+  cuuint64_t strides[4] = {ld * 4, ld * Q * 4, 2 * ld * Q * 4, 2 * N1 * ld * Q * 4};
+  cuuint32_t box[5] = {tub, 1, 2, 1, (cuuint32_t)R2};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N1, int N2, int TUB>
+bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twiddles32& tw, float* X, int num_sms,
+                   cudaStream_t s) {
+  CUtensorMap mc, mw1, mw2, mx;
+  if (!map_cbar_5d(&mc, Cre, P, ld, Q, N1, N2 / 2 + 1, TUB) ||
+      !map_f32_4d(&mw1, tw.scratch, P, Q, N1, N2, TUB, 1, N2) ||
+      !map_f32_4d(&mw2, tw.scratch, P, Q, N1, N2, TUB, N1, 1) ||
+      !map_f32_4d(&mx, X, P, Q, N2, N1, TUB, 1, N1))
+    return false;
+  const void* k1 = (const void*)inv4_pass1_kernel<N2, TUB>;
+  const void* k2 = (const void*)inv4_pass2_kernel<N1, TUB>;
+  const size_t sm1 = sizeof(float) * (2 * (N2 / 2 + 1) * 2 * TUB + 2 * TUB * N2), sm2 = sizeof(float) * TUB * N1;
+  if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1) != cudaSuccess ||
+      cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2) != cudaSuccess)
+    return false;
+  const int64_t pblocks = (P + TUB - 1) / TUB;
+  int per1 = 1, per2 = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, 2 * TUB, sm1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k2, 2 * TUB, sm2);
+  const int64_t it1 = pblocks * Q * (N1 / 2 + 1), it2 = pblocks * Q * N2;
+  const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
+  const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
+  int n1i = N1, n2i = N2;
+  const float2* st1 = tw.st_n1;
+  const float2* st2 = tw.st_n2;
+  const float2* twn = tw.tw;
+  void* a1[] = {(void*)&mc, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn};
+  if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
+  void* a2[] = {(void*)&mw2, (void*)&mx, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&st1};
+  return cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) == cudaSuccess;
+}
 }  // namespace
 
 bool tube_supported(int64_t n3) { return n3 == 32 || n3 == 64 || n3 == 128 || n3 == 256; }
+
+void fourstep_factors(int64_t n3, int* n1, int* n2) {
+  *n1 = *n2 = 0;
+  if (n3 == 4096) { *n1 = 64; *n2 = 64; }
+  else if (n3 == 8192) { *n1 = 128; *n2 = 64; }
+  else if (n3 == 16384) { *n1 = 128; *n2 = 128; }
+}
+
+bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw, float* X,
+                      int num_sms, cudaStream_t s) {
+  int N1, N2;
+  fourstep_factors(n3, &N1, &N2);
+  if (!N1 || !tw.st_n1 || !tw.st_n2 || !tw.scratch || tw.scratch_bytes < (size_t)(4 * P * Q * n3) || P % 4 != 0 ||
+      ((uintptr_t)X & 15) != 0 || ld % 4 != 0)
+    return false;
+  const bool wide = P >= 128;
+  if (N1 == 64 && N2 == 64)
+    return wide ? launch_inv4_t<64, 64, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
+                : launch_inv4_t<64, 64, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
+  if (N1 == 128 && N2 == 64)
+    return wide ? launch_inv4_t<128, 64, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
+                : launch_inv4_t<128, 64, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
+  return wide ? launch_inv4_t<128, 128, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
+              : launch_inv4_t<128, 128, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
+}
+
+bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                      const Twiddles32& tw, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
+  int N1, N2;
+  fourstep_factors(n3, &N1, &N2);
+  if (!N1 || !tw.st_n1 || !tw.st_n2 || !tw.scratch || tw.scratch_bytes < (size_t)(4 * P * Q * n3) || P % 4 != 0 ||
+      ((uintptr_t)X & 15) != 0 || ld % 2 != 0)
+    return false;
+  const bool wide = P >= 128;
+  if (N1 == 64 && N2 == 64)
+    return wide ? launch_fwd4_t<64, 64, 128>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s)
+                : launch_fwd4_t<64, 64, 64>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s);
+  if (N1 == 128 && N2 == 64)
+    return wide ? launch_fwd4_t<128, 64, 128>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s)
+                : launch_fwd4_t<128, 64, 64>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s);
+  return wide ? launch_fwd4_t<128, 128, 128>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s)
+              : launch_fwd4_t<128, 128, 64>(X, P, Q, role, maxbits, tw, out, ld, unscale, num_sms, s);
+}
 
 // Measured (B200, K1/K3 stage times): the tube kernels win the forward transform for n3 = 64
 // (config 5: 10.1 -> 8.3 ms), 128 and 256 (2x over the buffer-major FFT kernels) and the inverse

@@ -207,6 +207,36 @@ def test_prepared_operand_bitwise(T, dims):
         T.tprod_prepared(dev(B), handle=h)
 
 
+@pytest.mark.parametrize("n3,p,q", [(4096, 36, 3), (4096, 132, 2), (8192, 24, 2), (16384, 8, 2)])
+def test_fourstep_forward_stage(T, n3, p, q):
+    """Two-pass four-step forward DFT (long power-of-two tubes, P % 4 == 0; TUB = 64 and 128 tiles,
+    ragged last tile) vs numpy.fft.rfft, both operand roles."""
+    X = normal((p, q, n3), 5 + n3 + p)
+    ref = np.fft.rfft(X.astype(np.float64), axis=2)
+    for role in (0, 1):
+        got = host(T.dft_f32(dev(X), role=role))
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err < 2e-6, (role, err)
+
+
+@pytest.mark.parametrize("dims", [(24, 16, 8192, 8), (132, 8, 4096, 12)], ids=lambda d: "x".join(map(str, d)))
+def test_fourstep_full_path(T, dims):
+    """Full t-product with the four-step forward on sampled frontal slices vs the oracle, and vs the
+    one-pass FFT kernels (TPROD_OPT_TRANSFORM = 1)."""
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 71)
+    B = normal((n2, n4, n3), 72)
+    h1 = T.Handle()
+    h1.set_option(T._lib.TPROD_OPT_TRANSFORM, 1)
+    C = gpu_tprod(T, A, B)
+    C1 = gpu_tprod(T, A, B, handle=h1)
+    tl = np.array([0, 1, n3 // 2, n3 - 1])
+    J = np.arange(n4)
+    ref = O.tprod_blockrow(A, B, tl, J)
+    assert O.rel_err(C[:, :, tl], ref) <= TOL32
+    assert O.rel_err(C, C1) <= 1e-6
+
+
 def test_worked_examples_on_gpu(T, golden):
     for dt in (np.float32, np.float64):
         g = golden["tprod_tubes_1x1x3"]
