@@ -54,6 +54,10 @@ struct tprod_ctx {
   bool timed_last = false;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   PreparedA prep;
+  // pipelined host entry point (tprod_f32_host): copy streams, double-buffer events, its own A
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  PreparedA prep_host;
 };
 
 namespace {
@@ -257,6 +261,48 @@ NcclApi& nccl() {
   return api;
 }
 
+// K0 + K1 of A into a PreparedA (tprod_prepare_a_f32 and the pipelined host entry point).  The
+// four-step transforms get their intermediate from the handle workspace (stream-ordered with every
+// other call on the handle).
+int prepare_into(tprod_ctx* h, PreparedA& P, const float* A, int64_t n1, int64_t n2, int64_t n3, cudaStream_t s) {
+  int st;
+  const int64_t hh = h_slices(n3), lda = round_up(n1, 8);
+  const size_t off_u = align_up(4 * (size_t)n1, 1024);
+  const size_t off_Ab = off_u + align_up(4 * (size_t)n1, 1024);
+  const size_t bytes = off_Ab + 2 * (size_t)(hh * NPLANES * n2 * lda);
+  if (P.bytes < bytes) {
+    if (P.buf) {
+      CK(cudaDeviceSynchronize());
+      cudaFree(P.buf);
+      P.buf = nullptr;
+      P.bytes = 0;
+    }
+    if (cudaMalloc(&P.buf, bytes) != cudaSuccess) { cudaGetLastError(); P.valid = false; return TPROD_ENOMEM; }
+    P.bytes = bytes;
+  }
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  if (f1) {
+    const size_t w = 4 * (size_t)(n1 * n2 * n3);
+    if ((st = ensure_ws(h, w))) return st;
+    T.scratch = (float*)h->ws;
+    T.scratch_bytes = w;
+  }
+  P.maxA = (unsigned*)P.buf;
+  P.uA = (float*)((char*)P.buf + off_u);
+  P.Ab = (__half*)((char*)P.buf + off_Ab);
+  CK(cudaMemsetAsync(P.maxA, 0, 4 * (size_t)n1, s));
+  launch_absmax2(A, nullptr, n1, n2, n3, 1, P.maxA, nullptr, h->num_sms, s);               // K0 (A)
+  launch_fwd_split(A, n1, n2, n3, 0, P.maxA, T, P.Ab, lda, P.uA, h->num_sms, s);         // K1 (A)
+  if ((st = launch_status())) { P.valid = false; return st; }
+  P.valid = true;
+  P.n1 = n1; P.n2 = n2; P.n3 = n3; P.lda = lda; P.h = hh;
+  return TPROD_OK;
+}
+
 // ---------------------------------------------------------------- the hot path
 // pa != nullptr: A is the handle's prepared operand (A itself is not read; K0/K1 run for B only)
 int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2,
@@ -345,12 +391,73 @@ int check_call(tprod_ctx* h, const T* A, const T* B, T* C, int64_t n1, int64_t n
   return TPROD_OK;
 }
 
+// fp32 host entry point, pipelined over lateral-slice chunks (columns of unfold(B) map 1:1 to
+// columns of unfold(C), Eq. (9)): A is copied and prepared (K0 + K1 of A) once, then chunk i of B
+// is copied in on cs_in while chunk i-1 is computed on `s` (the prepared-operand path) and chunk
+// i-2 of C is copied out on cs_out; B / C device chunks are double-buffered.  Every column's result
+// is bitwise identical to the one-shot call (prepared path and W-invariance).  Host buffers should
+// be pinned for the copies to overlap.
+int host_call_f32_pipelined(const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
+                            int64_t n4, cudaStream_t s, tprod_handle h, int64_t w) {
+  int st;
+  if (!h->cs_in) {
+    CK(cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_comp[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_out[i], cudaEventDisableTiming));
+    }
+  }
+  const size_t bA = 4 * (size_t)(n1 * n2 * n3), bBc = 4 * (size_t)(n2 * w * n3), bCc = 4 * (size_t)(n1 * w * n3);
+  if ((st = ensure_hbuf(h, 0, bA)) || (st = ensure_hbuf(h, 1, 2 * bBc)) || (st = ensure_hbuf(h, 2, 2 * bCc))) return st;
+  float* dA = (float*)h->hbuf[0];
+  float* dB[2] = {(float*)h->hbuf[1], (float*)((char*)h->hbuf[1] + bBc)};
+  float* dC[2] = {(float*)h->hbuf[2], (float*)((char*)h->hbuf[2] + bCc)};
+  CK(cudaMemcpyAsync(dA, A, bA, cudaMemcpyHostToDevice, s));
+  if ((st = prepare_into(h, h->prep_host, dA, n1, n2, n3, s))) return st;
+  // the copy streams start after everything already on s (A's copy / preparation, earlier calls)
+  CK(cudaEventRecord(h->ev_comp[0], s));
+  CK(cudaStreamWaitEvent(h->cs_in, h->ev_comp[0], 0));
+  CK(cudaStreamWaitEvent(h->cs_out, h->ev_comp[0], 0));
+  const int64_t nch = (n4 + w - 1) / w;
+  for (int64_t i = 0; i < nch; ++i) {
+    const int b = (int)(i & 1);
+    const int64_t j0 = i * w, wi = std::min(w, n4 - j0);
+    if (i >= 2) CK(cudaStreamWaitEvent(h->cs_in, h->ev_comp[b], 0));     // compute i-2 has read dB[b]
+    // B(:, j0:j0+wi, :): n3 rows of n2*wi floats, host pitch n2*n4
+    CK(cudaMemcpy2DAsync(dB[b], 4 * (size_t)(n2 * wi), B + n2 * j0, 4 * (size_t)(n2 * n4), 4 * (size_t)(n2 * wi),
+                         (size_t)n3, cudaMemcpyHostToDevice, h->cs_in));
+    CK(cudaEventRecord(h->ev_in[b], h->cs_in));
+    CK(cudaStreamWaitEvent(s, h->ev_in[b], 0));
+    if (i >= 2) CK(cudaStreamWaitEvent(s, h->ev_out[b], 0));            // C chunk i-2 has left dC[b]
+    if ((st = run_f32(h, nullptr, dB[b], dC[b], n1, n2, n3, wi, s, &h->prep_host))) return st;
+    CK(cudaEventRecord(h->ev_comp[b], s));
+    CK(cudaStreamWaitEvent(h->cs_out, h->ev_comp[b], 0));
+    CK(cudaMemcpy2DAsync(C + n1 * j0, 4 * (size_t)(n1 * n4), dC[b], 4 * (size_t)(n1 * wi), 4 * (size_t)(n1 * wi),
+                         (size_t)n3, cudaMemcpyDeviceToHost, h->cs_out));
+    CK(cudaEventRecord(h->ev_out[b], h->cs_out));
+  }
+  CK(cudaStreamWaitEvent(s, h->ev_out[0], 0));
+  CK(cudaStreamWaitEvent(s, h->ev_out[1], 0));
+  CK(cudaStreamSynchronize(s));
+  return TPROD_OK;
+}
+
 template <typename T>
 int host_call(const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3, int64_t n4,
                      void* stream, tprod_handle h) {
   int st = check_call(h, A, B, C, n1, n2, n3, n4);
   if (st) return st;
   CK(cudaSetDevice(h->device));
+  if (sizeof(T) == 4) {
+    // pipeline when B is large enough to amortise chunking: ~8 chunks of >= 4 MB of B
+    const double bB = 4.0 * n2 * n4 * n3;
+    int64_t w = (n4 + 7) / 8;
+    if (bB >= 32e6 && n4 >= 4)
+      return host_call_f32_pipelined((const float*)A, (const float*)B, (float*)C, n1, n2, n3, n4,
+                                     (cudaStream_t)stream, h, w);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   size_t bA = sizeof(T) * (size_t)(n1 * n2 * n3), bB = sizeof(T) * (size_t)(n2 * n4 * n3),
          bC = sizeof(T) * (size_t)(n1 * n4 * n3);
@@ -399,6 +506,14 @@ int tprod_destroy(tprod_handle h) {
   for (auto& kv : h->tw64) cudaFree(kv.second);
   for (int i = 0; i < 3; ++i) if (h->hbuf[i]) cudaFree(h->hbuf[i]);
   if (h->prep.buf) cudaFree(h->prep.buf);
+  if (h->prep_host.buf) cudaFree(h->prep_host.buf);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_in[i]) cudaEventDestroy(h->ev_in[i]);
+    if (h->ev_comp[i]) cudaEventDestroy(h->ev_comp[i]);
+    if (h->ev_out[i]) cudaEventDestroy(h->ev_out[i]);
+  }
+  if (h->cs_in) cudaStreamDestroy(h->cs_in);
+  if (h->cs_out) cudaStreamDestroy(h->cs_out);
   if (h->ws) cudaFree(h->ws);
   delete h;
   return TPROD_OK;
@@ -435,35 +550,7 @@ int tprod_prepare_a_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, void
   int st = validate_dims(n1, n2, n3, 1);
   if (st) return st;
   CK(cudaSetDevice(h->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  PreparedA& P = h->prep;
-  const int64_t hh = h_slices(n3), lda = round_up(n1, 8);
-  const size_t off_u = align_up(4 * (size_t)n1, 1024);
-  const size_t off_Ab = off_u + align_up(4 * (size_t)n1, 1024);
-  const size_t bytes = off_Ab + 2 * (size_t)(hh * NPLANES * n2 * lda);
-  if (P.bytes < bytes) {
-    if (P.buf) {
-      CK(cudaDeviceSynchronize());
-      cudaFree(P.buf);
-      P.buf = nullptr;
-      P.bytes = 0;
-    }
-    if (cudaMalloc(&P.buf, bytes) != cudaSuccess) { cudaGetLastError(); P.valid = false; return TPROD_ENOMEM; }
-    P.bytes = bytes;
-  }
-  Twiddles32 T;
-  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
-  P.maxA = (unsigned*)P.buf;
-  P.uA = (float*)((char*)P.buf + off_u);
-  P.Ab = (__half*)((char*)P.buf + off_Ab);
-  CK(cudaMemsetAsync(P.maxA, 0, 4 * (size_t)n1, s));
-  launch_absmax2(A, nullptr, n1, n2, n3, 1, P.maxA, nullptr, h->num_sms, s);               // K0 (A)
-  launch_fwd_split(A, n1, n2, n3, 0, P.maxA, T, P.Ab, lda, P.uA, h->num_sms, s);         // K1 (A)
-  if ((st = launch_status())) { P.valid = false; return st; }
-  P.valid = true;
-  P.n1 = n1; P.n2 = n2; P.n3 = n3; P.lda = lda; P.h = hh;
-  return TPROD_OK;
+  return prepare_into(h, h->prep, A, n1, n2, n3, (cudaStream_t)stream);
 }
 
 int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod_handle h) {

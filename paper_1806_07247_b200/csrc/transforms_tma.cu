@@ -410,10 +410,13 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
+// K3: the 1/N of the inverse is applied while Z is built (a power of two: exact), and the
+// transformed tile z[k][c] -- which read as floats IS the output rows X(p0:p0+TUB, q, k) -- leaves
+// by one TMA bulk tensor store.
 template <int N>
-__global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant__ CUtensorMap mC, int64_t P,
-                                                          int64_t Q, const float2* __restrict__ st,
-                                                          float* __restrict__ X) {
+__global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant__ CUtensorMap mC,
+                                                          const __grid_constant__ CUtensorMap mXo, int64_t P,
+                                                          int64_t Q, const float2* __restrict__ st) {
   using C = TubeCfg<N>;
   constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
   constexpr int BUF = TUB * 2 * H;                  // C-bar tile: rows [f][re|im], TUB floats each
@@ -421,30 +424,29 @@ __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant
   __shared__ uint64_t full[2];
   float2* z = reinterpret_cast<float2*>(smem + 2 * BUF);     // z[k][c], separate from the TMA buffers
   const float inv_n = 1.f / (float)N;
-  const int64_t PQ = P * Q;
   tma_pipeline<BUF, TUB>(&mC, P, Q, smem, full, [&](const Item& cur, const float* s) {
-    // Z = X + i Y with the conjugate fill (Im of DC / Nyquist dropped: C2R)
+    if (threadIdx.x == 0) bulk_wait_read();                  // the previous item's store has read z
+    __syncthreads();
+    // Z / N = (X + i Y) / N with the conjugate fill (Im of DC / Nyquist dropped: C2R)
     for (int idx = threadIdx.x; idx < H * F; idx += TUBE_NT) {
       const int c = idx % F, f = idx / F;
       const bool self = (f == 0 || 2 * f == N);
       const float2 re = reinterpret_cast<const float2*>(s + (2 * f) * TUB)[c];       // (x_r, y_r)
       const float2 im = self ? make_float2(0.f, 0.f)
                              : reinterpret_cast<const float2*>(s + (2 * f + 1) * TUB)[c];  // (x_i, y_i)
-      z[f * F + c] = make_float2(re.x - im.y, im.x + re.y);                        // X_f + i Y_f
-      if (!self) z[(N - f) * F + c] = make_float2(re.x + im.y, re.y - im.x);       // conj X_f + i conj Y_f
+      z[f * F + c] = make_float2((re.x - im.y) * inv_n, (im.x + re.y) * inv_n);        // X_f + i Y_f
+      if (!self) z[(N - f) * F + c] = make_float2((re.x + im.y) * inv_n, (re.y - im.x) * inv_n);
     }
     __syncthreads();
     tube_fft<N, +1>(z, st);
-    float* xo = X + P * cur.q + cur.p0;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < N * F; idx += TUBE_NT) {
-      const int c = idx % F, k = idx / F;
-      const int64_t p = cur.p0 + 2 * c;
-      const float2 v = z[k * F + c];
-      if (p + 1 < P) *reinterpret_cast<float2*>(xo + PQ * k + 2 * c) = make_float2(v.x * inv_n, v.y * inv_n);
-      else if (p < P) xo[PQ * k + 2 * c] = v.x * inv_n;
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store3d(&mXo, z, (int)cur.p0, (int)cur.q, 0);
+      bulk_commit();
     }
   });
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------ four-step K1
@@ -902,16 +904,17 @@ bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const
                        cudaStream_t s) {
   using C = TubeCfg<N>;
   constexpr int H = N / 2 + 1;
-  CUtensorMap m;
+  CUtensorMap m, mo;
   if (!map_f32(&m, Cre, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(2 * H), (uint32_t)(2 * H),
-               (uint32_t)C::TUB))
+               (uint32_t)C::TUB) ||
+      !map_f32(&mo, X, (uint64_t)P, (uint64_t)P, (uint64_t)Q, (uint64_t)N, (uint32_t)N, (uint32_t)C::TUB))
     return false;
   const void* fn = (const void*)inv_tube_kernel<N>;
   const size_t smem = 2 * sizeof(float) * C::TUB * 2 * H + sizeof(float2) * (size_t)C::F * N;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
   const int grid = grid_occ(fn, items, smem, num_sms);
-  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&st, (void*)&X};
+  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&st};
   return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
 }
 
@@ -1060,7 +1063,7 @@ bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 // for 128 / 256; the register kernels of transforms_dense.cu stay faster for the n3 = 32 forward
 // and the n3 <= 64 inverse (config 5 K3: 4.4 vs 5.5 ms).
 static bool tube_fwd_pick(int64_t n3) { return n3 == 64 || n3 == 128 || n3 == 256; }
-static bool tube_inv_pick(int64_t n3) { return n3 == 128 || n3 == 256; }
+static bool tube_inv_pick(int64_t n3) { return n3 == 64 || n3 == 128 || n3 == 256; }
 
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
@@ -1075,7 +1078,7 @@ bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
 
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
                      int num_sms, cudaStream_t s) {
-  if (!st || !tube_inv_pick(n3) || P % 2 != 0 || ((uintptr_t)X & 7) != 0 || (ld * 4) % 16 != 0) return false;
+  if (!st || !tube_inv_pick(n3) || P % 4 != 0 || ((uintptr_t)X & 15) != 0 || (ld * 4) % 16 != 0) return false;
   switch (n3) {
     case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, X, num_sms, s);
     case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, X, num_sms, s);

@@ -315,6 +315,26 @@ def test_host_entry_e2e(T):
         assert O.rel_err(C, O.tprod_bcirc(A, B)) <= tol
 
 
+def test_host_entry_pipelined_bitwise(T):
+    """tprod_f32_host above the pipelining threshold (B >= 32 MB: A prepared once, lateral-slice
+    chunks of B / C double-buffered across copy and compute streams, ragged last chunk) returns
+    exactly the one-shot device result."""
+    import torch
+    n1, n2, n3, n4 = 256, 1024, 32, 1003
+    A = normal((n1, n2, n3), 81)
+    B = normal((n2, n4, n3), 82)
+    ref = gpu_tprod(T, A, B)
+    At, Bt = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+    At, Bt = (x if T.is_matlab_layout(x) else T.to_matlab(x) for x in (At, Bt))
+    out = T.matlab_empty(n1, n4, n3, torch.float32, "cpu").pin_memory()
+    out = out if T.is_matlab_layout(out) else T.to_matlab(out)
+    for _ in range(2):                                       # second call reuses the handle's buffers
+        C = T.tprod_f32_host(At, Bt, out=out).numpy()
+        assert np.array_equal(C, ref)
+    J = np.array([0, 125, 126, 1002])
+    assert O.rel_err(C[:, J, :], O.tprod_columns(A, B, J)) <= TOL32
+
+
 def test_errors(T):
     import torch
     A = T.to_matlab(torch.randn(4, 5, 6, device="cuda"))
