@@ -1059,11 +1059,13 @@ bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 }
 
 // Measured (B200, K1/K3 stage times): the tube kernels win the forward transform for n3 = 64
-// (config 5: 10.1 -> 8.3 ms), 128 and 256 (2x over the buffer-major FFT kernels) and the inverse
-// for 128 / 256; the register kernels of transforms_dense.cu stay faster for the n3 = 32 forward
-// and the n3 <= 64 inverse (config 5 K3: 4.4 vs 5.5 ms).
+// (config 5: 10.1 -> 7.0 ms with the TMA-store epilogue), 128 and 256 (1.6-2.4x over the
+// buffer-major FFT kernels), and with the TMA-store epilogue the inverse for 64 (config 5 K3
+// 4.2 -> 3.7 ms) and 128 (0.27 -> 0.09 ms on 1024x512x128); the register kernels of
+// transforms_dense.cu stay faster for n3 = 32.  (n3 = 256's C-bar tile has 2h = 258 > 256 rows, more
+// than one TMA box; that inverse stays on the FFT kernel.)
 static bool tube_fwd_pick(int64_t n3) { return n3 == 64 || n3 == 128 || n3 == 256; }
-static bool tube_inv_pick(int64_t n3) { return n3 == 64 || n3 == 128 || n3 == 256; }
+static bool tube_inv_pick(int64_t n3) { return n3 == 64 || n3 == 128; }
 
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
