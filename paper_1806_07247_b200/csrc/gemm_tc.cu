@@ -889,8 +889,9 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   int bn = force_bn;
   const int64_t mt = (n1 + tc::BM - 1) / tc::BM;
   if (bn == 0) {
-    // N = 128 unless that leaves SMs idle (small problems), then N = 64
-    bn = (mt * ((n4 + 127) / 128) * h >= num_sms) ? 128 : 64;
+    // N = 128 unless that leaves SMs idle (small problems) or n4 <= 64 fits one 64-wide tile
+    // (a 128-wide tile would be half padding: config 4's 64 x 64 x 64 slices, 84 -> see DESIGN)
+    bn = (n4 > 64 && mt * ((n4 + 127) / 128) * h >= num_sms) ? 128 : 64;
   }
   const int64_t nt = (n4 + bn - 1) / bn;
   int cn = force_cn;
