@@ -104,14 +104,22 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
     if (p < n1) {
       const float4* base = reinterpret_cast<const float4*>(A + p);
       const int64_t step = (int64_t)gyA * ty_n;
-      int64_t c = (int64_t)by * ty_n + ty;
-#pragma unroll 4
-      for (; c < colsA; c += step) {
-        float4 v = __ldg(base + (c * n1 >> 2));
-        m.x = fmaxf(m.x, fabsf(v.x));
-        m.y = fmaxf(m.y, fabsf(v.y));
-        m.z = fmaxf(m.z, fabsf(v.z));
-        m.w = fmaxf(m.w, fabsf(v.w));
+      // batches of U independent loads in flight per thread (latency-bound otherwise on narrow A)
+      constexpr int U = 8;
+      for (int64_t c0 = (int64_t)by * ty_n + ty; c0 < colsA; c0 += U * step) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t c = c0 + u * step;
+          v[u] = c < colsA ? __ldg(base + (c * n1 >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          m.x = fmaxf(m.x, fabsf(v[u].x));
+          m.y = fmaxf(m.y, fabsf(v[u].y));
+          m.z = fmaxf(m.z, fabsf(v[u].z));
+          m.w = fmaxf(m.w, fabsf(v[u].w));
+        }
       }
     }
     red[ty * W + 4 * tx] = m.x;
@@ -136,12 +144,30 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
     for (int64_t w = warp; w < n4 * wpc; w += nwarps) {
       const int64_t j = w % n4, k0 = w / n4;
       float m = 0.f;
-      for (int64_t k = k0; k < n3; k += wpc) {
-        const float4* x = reinterpret_cast<const float4*>(B + n2 * (j + n4 * k));   // run (j,k)
+      const int64_t r4 = n2 >> 2;                      // float4 per run B(:, j, k)
+      if (r4 >= 32) {
+        for (int64_t k = k0; k < n3; k += wpc) {
+          const float4* x = reinterpret_cast<const float4*>(B + n2 * (j + n4 * k));   // run (j,k)
 #pragma unroll 4
-        for (int64_t l4 = lane; l4 < (n2 >> 2); l4 += 32) {
-          float4 v = __ldg(x + l4);
-          m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          for (int64_t l4 = lane; l4 < r4; l4 += 32) {
+            float4 v = __ldg(x + l4);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
+        }
+      } else {
+        // short runs: lanes l4 < r4 of the warp, U runs in flight per batch
+        constexpr int U = 8;
+        for (int64_t kb = k0; kb < n3; kb += U * wpc) {
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t k = kb + u * wpc;
+            v[u] = (k < n3 && lane < r4) ? __ldg(reinterpret_cast<const float4*>(B + n2 * (j + n4 * k)) + lane)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
         }
       }
       for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
