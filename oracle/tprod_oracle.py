@@ -28,7 +28,7 @@ import numpy as np
 __all__ = [
     "dft_matrix", "circ", "bcirc", "unfold", "fold", "tprod_bcirc", "tprod_blockrow",
     "tprod_columns", "dft_mode3", "idft_mode3", "bdiag", "teye", "tran", "tprod_alg1",
-    "hermitian_half", "frobenius", "inner", "rel_err", "h_slices",
+    "hermitian_half", "frobenius", "inner", "rel_err", "h_slices", "tinv", "SingularTensor",
 ]
 
 
@@ -190,6 +190,37 @@ def tran(A: np.ndarray) -> np.ndarray:
     for k in range(1, n3):
         T[:, :, k] = A[:, :, n3 - k].conj().T
     return T
+
+
+class SingularTensor(ValueError):
+    """No inverse to working precision (SPEC.md [OP] tinv errors; the paper is silent)."""
+
+
+def tinv(A: np.ndarray, rtol: float | None = None) -> np.ndarray:
+    """Tensor inverse, Definition 2.4, Eq. (11): the B with A * B = I.
+
+    Literal form through Eq. (9): A * B = I  <=>  bcirc(A) . unfold(B) = unfold(I), so
+    unfold(B) = bcirc(A)^-1 . unfold(teye(n, n3)) (one dense solve); then B * A = I holds as well.
+    Existence check (reading R16; the paper gives none): every spectral slice A-bar^(f)
+    (literal DFT, Eq. (2)) must have sigma_min > rtol * s_max, where s_max is the largest singular
+    value over all slices (= ||bcirc(A)||_2, Eq. (7)) and rtol defaults to n * n3 * float64
+    epsilon; otherwise SingularTensor.  (SPEC.md's per-slice ratio would accept a slice that is
+    zero up to round-off.)"""
+    A = np.asarray(A, dtype=np.float64)
+    n1, n2, n3 = A.shape
+    if n1 != n2:
+        raise ValueError(f"tinv needs square frontal slices, got {A.shape}")
+    if rtol is None:
+        rtol = n1 * n3 * np.finfo(np.float64).eps
+    Abar = dft_mode3(A)
+    svs = [np.linalg.svd(Abar[:, :, f], compute_uv=False) for f in range(n3)]
+    smax = max(float(sv[0]) for sv in svs)
+    for f, sv in enumerate(svs):
+        if not smax > 0 or sv[-1] <= rtol * smax:
+            raise SingularTensor(f"spectral slice {f} is singular (sigma_min / max sigma = "
+                                 f"{(sv[-1] / smax) if smax > 0 else 0.0:.3e})")
+    X = np.linalg.solve(bcirc(A), unfold(teye(n1, n3)))
+    return fold(X, n1, n1, n3)
 
 
 def tprod_alg1(A: np.ndarray, B: np.ndarray, full: bool = False) -> np.ndarray:

@@ -298,3 +298,49 @@ def test_normal_lateral_is_the_global_stream(monkeypatch, chunk):
         part = synth.normal_lateral((7, 13, 5), 3, j0, j1)
         assert part.flags.f_contiguous
         np.testing.assert_array_equal(part, full[:, j0:j1, :])
+
+
+# ------------------------------------------------------------------ Definition 2.4 (NEXT-4)
+def _well_conditioned(n, n3, seed):
+    """Random n x n x n3 tensor whose spectral slices are diagonally dominant (well conditioned)."""
+    A = normal((n, n, n3), seed, np.float64) * 0.2
+    A[:, :, 0] += 2.0 * np.eye(n)                     # adds 2I to every spectral slice (DC of a delta)
+    return A
+
+
+def test_tinv_identity_and_worked_tubes(golden):
+    """tinv(teye) = teye; SPEC's tube examples: (1, 0) and (0, 1) are their own inverses
+    (circ((0,1)) = [[0,1],[1,0]], SPEC.md [OP] tinv examples)."""
+    np.testing.assert_allclose(O.tinv(O.teye(3, 4)), O.teye(3, 4), atol=1e-15)
+    np.testing.assert_allclose(O.tinv(np.array([1.0, 0.0]).reshape(1, 1, 2)).ravel(), [1.0, 0.0], atol=1e-15)
+    np.testing.assert_allclose(O.tinv(np.array([0.0, 1.0]).reshape(1, 1, 2)).ravel(), [0.0, 1.0], atol=1e-15)
+
+
+def test_tinv_eq11_both_sides_and_involution():
+    """Eq. (11): A * B = I and B * A = I (the definition solves only the first); tinv(tinv(A)) = A."""
+    for n, n3, seed in ((4, 5, 1), (3, 8, 2), (6, 1, 3)):
+        A = _well_conditioned(n, n3, seed)
+        B = O.tinv(A)
+        I = O.teye(n, n3)
+        assert O.rel_err(O.tprod_bcirc(A, B), I) < 1e-13
+        assert O.rel_err(O.tprod_bcirc(B, A), I) < 1e-13
+        assert O.rel_err(O.tinv(B), A) < 1e-13
+
+
+def test_tinv_n3_1_is_matrix_inverse():
+    """n3 = 1: bcirc(A) = A, so tinv is numpy.linalg.inv (library special case)."""
+    A = _well_conditioned(7, 1, 4)
+    np.testing.assert_allclose(O.tinv(A)[:, :, 0], np.linalg.inv(A[:, :, 0]), rtol=1e-12, atol=1e-14)
+
+
+def test_tinv_singular():
+    """The zero tensor and a tensor with one planted zero spectral slice have no inverse."""
+    with pytest.raises(O.SingularTensor):
+        O.tinv(np.zeros((3, 3, 4)))
+    A = _well_conditioned(3, 5, 5)
+    Ab = O.dft_mode3(A)
+    Ab[:, :, 2] = 0.0
+    Ab[:, :, 3] = 0.0                                   # its conjugate partner (5 - 2), keeps A real
+    A0 = np.real(O.idft_mode3(Ab))
+    with pytest.raises(O.SingularTensor):
+        O.tinv(A0)
