@@ -52,7 +52,8 @@ enum {
   TPROD_ECUDA = 4,         /* a CUDA runtime / launch error */
   TPROD_ENCCL = 5,         /* NCCL missing or an NCCL call failed */
   TPROD_EUNSUPPORTED = 6,  /* no kernel for this shape / device (not sm_100) */
-  TPROD_ENOWORLD = 7       /* tprod_bcast_* called before tprod_set_world */
+  TPROD_ENOWORLD = 7,      /* tprod_bcast_* called before tprod_set_world */
+  TPROD_ESINGULAR = 8      /* tprod_tinv_f32: a spectral slice has no inverse to working precision */
 };
 
 /* dtype selectors for tprod_workspace_bytes */
@@ -90,6 +91,23 @@ int tprod_f32(const float* A, const float* B, float* C,
 int tprod_prepare_a_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
 int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod_handle h);
 int tprod_release_a(tprod_handle h);
+
+/* NEXT-4 companion operations, DEVICE pointers in Matlab layout, asynchronous on
+ * `stream` unless stated otherwise.
+ * tprod_tran_*: At = A^* (Definition 2.2): A n1 x n2 x n3 -> At n2 x n1 x n3 with
+ *   At(:,:,0) = A(:,:,0)^T and At(:,:,k) = A(:,:,n3-k)^T (real data).  At must not overlap A.
+ * tprod_teye_*: I = the n x n x n3 identity tensor (Definition 2.3).
+ * tprod_tinv_f32: X = A^-1 (Definition 2.4, Eq. (11)), A and X n x n x n3,
+ *   1 <= n <= 96: forward DFT (production K1 kernels), a complex Gauss-Jordan inverse with partial
+ *   pivoting per spectral slice f < h (fp32), inverse DFT with the conjugate fill (production K3
+ *   kernels).  SYNCHRONOUS (waits for `stream`): returns TPROD_ESINGULAR if a pivot falls to
+ *   <= n * 2^-20 times the largest spectral entry (X is then unspecified), TPROD_EUNSUPPORTED for
+ *   n > 96. */
+int tprod_tran_f32(const float* A, float* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
+int tprod_tran_f64(const double* A, double* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
+int tprod_teye_f32(float* I, int64_t n, int64_t n3, void* stream, tprod_handle h);
+int tprod_teye_f64(double* I, int64_t n, int64_t n3, void* stream, tprod_handle h);
+int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream, tprod_handle h);
 
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,

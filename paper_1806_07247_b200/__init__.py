@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -182,6 +182,58 @@ def tprod_prepared(B, out=None, handle=None, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream(B.device)
     check(lib().tprod_f32_prepared(B.data_ptr(), out.data_ptr(), n4, C.c_void_p(s.cuda_stream), h.ptr),
           "tprod_f32_prepared")
+    return out
+
+
+def _h_s(t, handle, stream):
+    import torch
+    h = handle or _default_handle(t.device.index)
+    s = stream if stream is not None else torch.cuda.current_stream(t.device)
+    return h, C.c_void_p(s.cuda_stream)
+
+
+def tran(A, out=None, handle=None, stream=None):
+    """A^* (Definition 2.2): n2 x n1 x n3, slice 0 transposed, slices 1.. reversed and transposed."""
+    import torch
+    if A.dim() != 3 or not A.is_cuda or not is_matlab_layout(A):
+        raise ValueError("tran needs a 3-D CUDA tensor in the Matlab layout")
+    n1, n2, n3 = (int(x) for x in A.shape)
+    if out is None:
+        out = matlab_empty(n2, n1, n3, A.dtype, A.device)
+    fn = {torch.float32: lib().tprod_tran_f32, torch.float64: lib().tprod_tran_f64}.get(A.dtype)
+    if fn is None:
+        raise TypeError(f"tran: unsupported dtype {A.dtype}")
+    h, s = _h_s(A, handle, stream)
+    check(fn(A.data_ptr(), out.data_ptr(), n1, n2, n3, s, h.ptr), "tprod_tran")
+    return out
+
+
+def teye(n: int, n3: int, dtype=None, device="cuda", handle=None, stream=None):
+    """The n x n x n3 identity tensor (Definition 2.3), written by the library."""
+    import torch
+    dtype = dtype or torch.float32
+    out = matlab_empty(n, n, n3, dtype, device)
+    fn = {torch.float32: lib().tprod_teye_f32, torch.float64: lib().tprod_teye_f64}.get(dtype)
+    if fn is None:
+        raise TypeError(f"teye: unsupported dtype {dtype}")
+    h, s = _h_s(out, handle, stream)
+    check(fn(out.data_ptr(), n, n3, s, h.ptr), "tprod_teye")
+    return out
+
+
+def tinv(A, out=None, handle=None, stream=None):
+    """A^-1 (Definition 2.4, Eq. (11)) for a float32 n x n x n3 CUDA tensor, n <= 96.  Synchronous;
+    raises TprodError (status TPROD_ESINGULAR) if a spectral slice is singular to working precision."""
+    import torch
+    if A.dim() != 3 or A.shape[0] != A.shape[1] or A.dtype != torch.float32 or not A.is_cuda:
+        raise ValueError("tinv needs a float32 n x n x n3 CUDA tensor")
+    if not is_matlab_layout(A):
+        raise ValueError("A must have the Matlab layout (strides (1, n1, n1*n2)); use to_matlab()")
+    n, _, n3 = (int(x) for x in A.shape)
+    if out is None:
+        out = matlab_empty(n, n, n3, torch.float32, A.device)
+    h, s = _h_s(A, handle, stream)
+    check(lib().tprod_tinv_f32(A.data_ptr(), out.data_ptr(), n, n3, s, h.ptr), "tprod_tinv_f32")
     return out
 
 

@@ -11,7 +11,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TPROD_LIB") or os.path.join(_PKG, "libtprod.so")
 
 TPROD_OK, TPROD_EINVAL, TPROD_EALIAS, TPROD_ENOMEM, TPROD_ECUDA, TPROD_ENCCL, \
-    TPROD_EUNSUPPORTED, TPROD_ENOWORLD = range(8)
+    TPROD_EUNSUPPORTED, TPROD_ENOWORLD, TPROD_ESINGULAR = range(9)
 TPROD_DTYPE_F32, TPROD_DTYPE_F64 = 0, 1
 TPROD_OPT_ENGINE, TPROD_OPT_GEMM_BN, TPROD_OPT_TIMING, TPROD_OPT_GEMM_CLUSTER, TPROD_OPT_TRANSFORM = 1, 2, 3, 4, 5
 
@@ -38,6 +38,11 @@ SIGNATURES = {
     "tprod_prepare_a_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "tprod_f32_prepared": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "tprod_release_a": (_int, [_vp]),
+    "tprod_tran_f32": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "tprod_tran_f64": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "tprod_teye_f32": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "tprod_teye_f64": (_int, [_vp, _i64, _i64, _vp, _vp]),
+    "tprod_tinv_f32": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
 }
 
 _lib = None

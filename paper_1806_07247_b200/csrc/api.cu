@@ -474,6 +474,29 @@ int host_call(const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3, 
   return TPROD_OK;
 }
 
+template <typename T>
+int tran_impl(const T* A, T* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h) {
+  if (!h || !A || !At) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, 1);
+  if (st) return st;
+  const size_t b = sizeof(T) * (size_t)(n1 * n2 * n3);
+  if (overlaps(A, b, At, b)) return TPROD_EALIAS;
+  if (n3 > 65535) return TPROD_EUNSUPPORTED;
+  CK(cudaSetDevice(h->device));
+  launch_tran<T>(A, At, n1, n2, n3, (cudaStream_t)stream);
+  h->last_launches = 1;
+  return launch_status();
+}
+template <typename T>
+int teye_impl(T* I, int64_t n, int64_t n3, void* stream, tprod_handle h) {
+  if (!h || !I) return TPROD_EINVAL;
+  int st = validate_dims(n, n, n3, 1);
+  if (st) return st;
+  CK(cudaSetDevice(h->device));
+  if (launch_teye<T>(I, n, n3, (cudaStream_t)stream)) return TPROD_ECUDA;
+  h->last_launches = 1;
+  return launch_status();
+}
 }  // namespace
 
 // ====================================================================== exported C ABI
@@ -574,6 +597,72 @@ int tprod_release_a(tprod_handle h) {
   return TPROD_OK;
 }
 
+int tprod_tran_f32(const float* A, float* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h) {
+  return tran_impl(A, At, n1, n2, n3, stream, h);
+}
+int tprod_tran_f64(const double* A, double* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h) {
+  return tran_impl(A, At, n1, n2, n3, stream, h);
+}
+
+int tprod_teye_f32(float* I, int64_t n, int64_t n3, void* stream, tprod_handle h) {
+  return teye_impl(I, n, n3, stream, h);
+}
+int tprod_teye_f64(double* I, int64_t n, int64_t n3, void* stream, tprod_handle h) {
+  return teye_impl(I, n, n3, stream, h);
+}
+
+int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream, tprod_handle h) {
+  if (!h || !A || !X) return TPROD_EINVAL;
+  int st = validate_dims(n, n, n3, 1);
+  if (st) return st;
+  if (!tinv_supported(n)) return TPROD_EUNSUPPORTED;
+  const size_t b = 4 * (size_t)(n * n * n3);
+  if (overlaps(A, b, X, b)) return TPROD_EALIAS;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t hh = h_slices(n3), ld = round_up(n, 8), nn = n * n;
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  size_t o = 0;
+  const size_t off_flag = o; o = align_up(o + 16, 1024);                    // singular flag, max entry
+  const size_t off_max = o;  o = align_up(o + 4 * (size_t)n, 1024);
+  const size_t off_u = o;    o = align_up(o + 4 * (size_t)n, 1024);
+  const size_t off_sp = o;   o = align_up(o + 2 * (size_t)(hh * NPLANES * n * ld), 1024);
+  const size_t off_re = o;   o = align_up(o + 4 * (size_t)(4 * hh * nn), 1024);  // re, im, xre, xim
+  const size_t off_w = o;    o = align_up(o + (f1 ? b : 0), 1024);
+  if ((st = ensure_ws(h, o))) return st;
+  char* ws = (char*)h->ws;
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
+  T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
+  T.scratch_bytes = f1 ? b : 0;
+  int* flag = (int*)(ws + off_flag);
+  unsigned* amax = (unsigned*)(ws + off_flag + 4);
+  unsigned* mx = (unsigned*)(ws + off_max);
+  float* u = (float*)(ws + off_u);
+  __half* sp = (__half*)(ws + off_sp);
+  float* re = (float*)(ws + off_re);
+  float* im = re + hh * nn;
+  float* xre = im + hh * nn;
+  float* xim = xre + hh * nn;
+  CK(cudaMemsetAsync(ws + off_flag, 0, 16, s));
+  CK(cudaMemsetAsync(mx, 0, 4 * (size_t)n, s));
+  launch_absmax(A, n, n, n3, 0, mx, s);                                      // row scales
+  launch_fwd_split(A, n, n, n3, 0, mx, T, sp, ld, u, h->num_sms, s);         // Alg. 1 step 1
+  launch_decode_split(sp, ld, n, n, n3, 0, u, re, im, s);                    // fp32 planes [f][q][p]
+  launch_absmax_planes(re, im, hh * nn, amax, s);
+  const float rtol = (float)n * 9.5367431640625e-07f;                        // n * 2^-20
+  if (launch_slice_inverse(re, im, xre, xim, n, hh, nn, rtol, amax, flag, s)) return TPROD_ECUDA;
+  launch_inv_f32(xre, xim, n, nn, n, n, n3, T, X, h->num_sms, s);            // fill + inverse DFT
+  if ((st = launch_status())) return st;
+  int host_flag = 0;
+  CK(cudaMemcpyAsync(&host_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  h->last_launches = 7;
+  return host_flag ? TPROD_ESINGULAR : TPROD_OK;
+}
+
 int tprod_workspace_bytes(int64_t n1, int64_t n2, int64_t n3, int64_t n4, int dtype, size_t* out) {
   if (!out) return TPROD_EINVAL;
   int st = validate_dims(n1, n2, n3, n4);
@@ -594,6 +683,7 @@ const char* tprod_strerror(int status) {
     case TPROD_ENCCL: return "NCCL unavailable or an NCCL call failed";
     case TPROD_EUNSUPPORTED: return "unsupported device or shape (requires sm_100 / B200)";
     case TPROD_ENOWORLD: return "no NCCL world: call tprod_set_world first";
+    case TPROD_ESINGULAR: return "singular tensor: a spectral slice has no inverse to working precision";
     default: return "unknown tprod status";
   }
 }

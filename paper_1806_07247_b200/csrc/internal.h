@@ -94,6 +94,16 @@ bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
                      int num_sms, cudaStream_t s);
 
+// ------------------------------------------------------------------ NEXT-4 (tensor_ops.cu)
+template <typename T>
+void launch_tran(const T* A, T* At, int64_t n1, int64_t n2, int64_t n3, cudaStream_t s);
+template <typename T>
+int launch_teye(T* I, int64_t n, int64_t n3, cudaStream_t s);
+bool tinv_supported(int64_t n);
+int launch_slice_inverse(const float* re, const float* im, float* xre, float* xim, int64_t n, int64_t h,
+                         int64_t fstride, float rtol, const unsigned* maxp, int* singular, cudaStream_t s);
+void launch_absmax_planes(const float* re, const float* im, int64_t count, unsigned* out, cudaStream_t s);
+
 // ------------------------------------------------------------------ fp64 path
 // spectra as fp64 planes [f][re|im][q][ld]
 void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,

@@ -237,6 +237,60 @@ def test_fourstep_full_path(T, dims):
     assert O.rel_err(C, C1) <= 1e-6
 
 
+# ------------------------------------------------------------------------------- NEXT-4
+@pytest.mark.parametrize("dims", [(33, 17, 5), (7, 64, 1), (64, 3, 2), (40, 40, 31)], ids=lambda d: "x".join(map(str, d)))
+def test_tran_teye_gpu_exact(T, dims):
+    """tran (Def. 2.2) and teye (Def. 2.3) on the GPU equal the oracle exactly (pure data movement)."""
+    import torch
+    n1, n2, n3 = dims
+    for dt in (np.float32, np.float64):
+        A = normal((n1, n2, n3), 91 + n3, dt)
+        assert np.array_equal(host(T.tran(dev(A))), O.tran(A).astype(dt))
+    for dt, tdt in ((np.float32, torch.float32), (np.float64, torch.float64)):
+        assert np.array_equal(host(T.teye(n1, n3, dtype=tdt)), O.teye(n1, n3).astype(dt))
+
+
+def _well_conditioned(n, n3, seed):
+    A = normal((n, n, n3), seed, np.float64) * 0.2
+    A[:, :, 0] += 2.0 * np.eye(n)
+    return A.astype(np.float32)
+
+
+@pytest.mark.parametrize("n,n3", [(1, 1), (5, 4), (32, 7), (96, 2), (16, 64), (8, 100)])
+def test_tinv_gpu_vs_oracle(T, n, n3):
+    """tinv (Def. 2.4) through the production transforms + per-slice Gauss-Jordan vs the oracle's
+    literal bcirc solve, and both sides of Eq. (11) in the oracle."""
+    A = _well_conditioned(n, n3, 93 + n)
+    X = host(T.tinv(dev(A)))
+    ref = O.tinv(A)
+    assert O.rel_err(X, ref) <= 1e-5
+    I = O.teye(n, n3)
+    assert O.rel_err(O.tprod_bcirc(A, X), I) <= 1e-5
+    assert O.rel_err(O.tprod_bcirc(X, A), I) <= 1e-5
+
+
+def test_tinv_gpu_long_tubes_and_errors(T):
+    """tinv on long tubes (four-step transforms) checked by Eq. (11) on sampled slices of the oracle
+    product; singular and unsupported inputs raise."""
+    A = _well_conditioned(12, 4096, 97)
+    X = host(T.tinv(dev(A)))
+    tl = np.array([0, 1, 2048, 4095])
+    AX = O.tprod_blockrow(A, X, tl, np.arange(12))
+    assert O.rel_err(AX, O.teye(12, 4096)[:, :, tl]) <= 1e-5
+    with pytest.raises(T.TprodError) as e:
+        T.tinv(dev(np.zeros((4, 4, 3), np.float32)))
+    assert e.value.status == T._lib.TPROD_ESINGULAR
+    Ab = O.dft_mode3(_well_conditioned(3, 5, 5).astype(np.float64))
+    Ab[:, :, 2] = 0.0
+    Ab[:, :, 3] = 0.0
+    with pytest.raises(T.TprodError) as e:
+        T.tinv(dev(np.real(O.idft_mode3(Ab)).astype(np.float32)))
+    assert e.value.status == T._lib.TPROD_ESINGULAR
+    with pytest.raises(T.TprodError) as e:
+        T.tinv(dev(_well_conditioned(97, 2, 1)))
+    assert e.value.status == T._lib.TPROD_EUNSUPPORTED
+
+
 def test_worked_examples_on_gpu(T, golden):
     for dt in (np.float32, np.float64):
         g = golden["tprod_tubes_1x1x3"]
