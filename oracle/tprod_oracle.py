@@ -29,6 +29,7 @@ __all__ = [
     "dft_matrix", "circ", "bcirc", "unfold", "fold", "tprod_bcirc", "tprod_blockrow",
     "tprod_columns", "dft_mode3", "idft_mode3", "bdiag", "teye", "tran", "tprod_alg1",
     "hermitian_half", "frobenius", "inner", "rel_err", "h_slices", "tinv", "SingularTensor",
+    "tsvt", "tnn_bcirc",
 ]
 
 
@@ -221,6 +222,35 @@ def tinv(A: np.ndarray, rtol: float | None = None) -> np.ndarray:
                                  f"{(sv[-1] / smax) if smax > 0 else 0.0:.3e})")
     X = np.linalg.solve(bcirc(A), unfold(teye(n1, n3)))
     return fold(X, n1, n1, n3)
+
+
+def tsvt(Y: np.ndarray, tau: float) -> np.ndarray:
+    """Algorithm 3, t-SVT, step by step: Prox of tau * TNN (Eq. (19)-(21)).
+
+    1. Y-bar = fft(Y, [], 3) (literal DFT, Eq. (2)).
+    2. For i = 1..ceil((n3+1)/2): [U, S, V] = SVD(Y-bar^(i)); W-bar^(i) = U (S - tau)_+ V^*;
+       for the rest W-bar^(i) = conj(W-bar^(n3-i+2)) (the garbled "ena ioi" of L298-300 read as
+       "end for", R5).
+    3. Prox = ifft(W-bar, [], 3) (real for real Y; the imaginary round-off is dropped)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    n1, n2, n3 = Y.shape
+    Ybar = dft_mode3(Y)
+    Wbar = np.empty_like(Ybar)
+    hh = h_slices(n3)
+    for i in range(1, hh + 1):
+        U, S, Vh = np.linalg.svd(Ybar[:, :, i - 1], full_matrices=False)
+        Wbar[:, :, i - 1] = (U * np.maximum(S - tau, 0.0)) @ Vh
+    for i in range(hh + 1, n3 + 1):
+        Wbar[:, :, i - 1] = np.conj(Wbar[:, :, (n3 - i + 2) - 1])
+    return np.real(idft_mode3(Wbar))
+
+
+def tnn_bcirc(X: np.ndarray) -> float:
+    """Tensor nuclear norm through Eq. (18): ||X||_* = ||bcirc(X)||_* / n3 (the 1/n3
+    makes Eq. (18) agree with Definition 2.9, ||X||_* = sum_i S(i, i, 1), SPEC.md:L340 / DESIGN.md
+    R5); an independent route to the objective of Eq. (19) for testing Algorithm 3."""
+    X = np.asarray(X, dtype=np.float64)
+    return float(np.linalg.svd(bcirc(X), compute_uv=False).sum()) / X.shape[2]
 
 
 def tprod_alg1(A: np.ndarray, B: np.ndarray, full: bool = False) -> np.ndarray:

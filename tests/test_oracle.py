@@ -344,3 +344,49 @@ def test_tinv_singular():
     A0 = np.real(O.idft_mode3(Ab))
     with pytest.raises(O.SingularTensor):
         O.tinv(A0)
+
+
+# ------------------------------------------------------------------ Algorithm 3 (NEXT-2)
+def test_tsvt_limits():
+    """tau = 0 is the identity; tau >= every spectral singular value gives the zero tensor."""
+    Y = normal((5, 4, 6), 11, np.float64)
+    assert O.rel_err(O.tsvt(Y, 0.0), Y) < 1e-14
+    smax = max(np.linalg.svd(O.dft_mode3(Y)[:, :, f], compute_uv=False)[0] for f in range(6))
+    assert np.abs(O.tsvt(Y, smax * 1.0001)).max() < 1e-14
+
+
+def test_tsvt_tube_closed_form():
+    """1 x 1 x n3 tubes: every spectral 'matrix' is a scalar y, whose SVT is y * (1 - tau/|y|)_+ ;
+    worked by hand for the tube (3, 1): spectrum (4, 2), tau = 1 -> (3, 1) -> tube (2, 1)."""
+    got = O.tsvt(np.array([3.0, 1.0]).reshape(1, 1, 2), 1.0).ravel()
+    np.testing.assert_allclose(got, [2.0, 1.0], atol=1e-14)
+
+
+def test_tsvt_is_the_prox_of_eq19():
+    """Eq. (19): X = tsvt(Y, tau) minimises tau * TNN(X) + 1/2 ||X - Y||_F^2, with TNN through
+    bcirc (Eq. (18), an independent route): no random perturbation lowers the objective, and
+    moving towards Y or towards 0 does not either (first-order optimality, checked numerically)."""
+    rng = np.random.default_rng(3)
+    Y = normal((4, 3, 5), 12, np.float64)
+    tau = 1.5
+    X = O.tsvt(Y, tau)
+    obj = lambda Z: tau * O.tnn_bcirc(Z) + 0.5 * np.sum((Z - Y) ** 2)
+    f0 = obj(X)
+    for _ in range(40):
+        D = rng.standard_normal(Y.shape)
+        for eps in (1e-3, 1e-2):
+            assert obj(X + eps * D / np.linalg.norm(D)) >= f0 - 1e-10
+    for t in (0.9, 1.1):
+        assert obj(t * X) >= f0 - 1e-10
+    assert obj(Y) >= f0 and obj(np.zeros_like(Y)) >= f0
+
+
+def test_tsvt_keeps_low_tubal_rank():
+    """Prox of a tubal-rank-2 tensor (U * V, Def. 2.7) has every spectral slice of rank <= 2."""
+    U = normal((6, 2, 7), 13, np.float64)
+    V = normal((2, 5, 7), 14, np.float64)
+    X = O.tsvt(O.tprod_bcirc(U, V), 0.5)
+    Xb = O.dft_mode3(X)
+    for f in range(7):
+        s = np.linalg.svd(Xb[:, :, f], compute_uv=False)
+        assert s[2] < 1e-12 * max(s[0], 1.0)
