@@ -109,6 +109,14 @@ int tprod_teye_f32(float* I, int64_t n, int64_t n3, void* stream, tprod_handle h
 int tprod_teye_f64(double* I, int64_t n, int64_t n3, void* stream, tprod_handle h);
 int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream, tprod_handle h);
 
+/* NEXT-2: t-SVT, the proximal operator of tau * TNN (Algorithm 3, Eq. (19)-(21)).
+ * Y, X: n1 x n2 x n3 DEVICE pointers in Matlab layout, 1 <= n1, n2 <= 64, tau >= 0.  Forward DFT
+ * (production K1 kernels, decoded to fp32), one-sided Jacobi SVD + singular-value shrinkage per
+ * spectral slice f < h, inverse DFT with the conjugate fill (production K3 kernels).  Asynchronous.
+ * TPROD_EUNSUPPORTED beyond 64 x 64 slices, TPROD_EINVAL for tau < 0 or NaN. */
+int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3, float tau, void* stream,
+                   tprod_handle h);
+
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,
               int64_t n1, int64_t n2, int64_t n3, int64_t n4,

@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -234,6 +234,20 @@ def tinv(A, out=None, handle=None, stream=None):
         out = matlab_empty(n, n, n3, torch.float32, A.device)
     h, s = _h_s(A, handle, stream)
     check(lib().tprod_tinv_f32(A.data_ptr(), out.data_ptr(), n, n3, s, h.ptr), "tprod_tinv_f32")
+    return out
+
+
+def tsvt(Y, tau: float, out=None, handle=None, stream=None):
+    """Prox of tau * TNN (Algorithm 3, t-SVT) for a float32 n1 x n2 x n3 CUDA tensor, n1, n2 <= 64."""
+    import torch
+    if Y.dim() != 3 or Y.dtype != torch.float32 or not Y.is_cuda or not is_matlab_layout(Y):
+        raise ValueError("tsvt needs a float32 3-D CUDA tensor in the Matlab layout")
+    n1, n2, n3 = (int(x) for x in Y.shape)
+    if out is None:
+        out = matlab_empty(n1, n2, n3, torch.float32, Y.device)
+    h, s = _h_s(Y, handle, stream)
+    check(lib().tprod_tsvt_f32(Y.data_ptr(), out.data_ptr(), n1, n2, n3, C.c_float(tau), s, h.ptr),
+          "tprod_tsvt_f32")
     return out
 
 

@@ -103,6 +103,9 @@ bool tinv_supported(int64_t n);
 int launch_slice_inverse(const float* re, const float* im, float* xre, float* xim, int64_t n, int64_t h,
                          int64_t fstride, float rtol, const unsigned* maxp, int* singular, cudaStream_t s);
 void launch_absmax_planes(const float* re, const float* im, int64_t count, unsigned* out, cudaStream_t s);
+bool svt_supported(int64_t m, int64_t n);
+int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
+                     int64_t fstride, float tau, cudaStream_t s);
 
 // ------------------------------------------------------------------ fp64 path
 // spectra as fp64 planes [f][re|im][q][ld]

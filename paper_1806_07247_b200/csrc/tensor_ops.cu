@@ -10,6 +10,8 @@
 #include "internal.h"
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace tprod {
 
 // ---------------------------------------------------------------------------------------- tran
@@ -175,6 +177,160 @@ void launch_absmax_planes(const float* re, const float* im, int64_t count, unsig
   int64_t blocks = (count + 255) / 256;
   if (blocks > 1184) blocks = 1184;
   absmax_planes_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(re, im, count, out);
+}
+
+}  // namespace tprod
+
+namespace tprod {
+
+// ------------------------------------------------------------------------------ batched slice SVT
+// NEXT-2, Algorithm 3 step 2: for each spectral slice f < h,
+// W-bar_f = U (S - tau)_+ V^*.  One CTA per slice: one-sided (Hestenes) Jacobi on the m x n complex
+// slice in shared memory -- columns p, q orthogonalised by the complex rotation
+//   a_q' = a_q e (e = conj(g)/|g|, g = a_p^H a_q),  [a_p, a_q'] <- [a_p, a_q'] [[c, s], [-s, c]],
+//   zeta = (beta - alpha) / (2|g|), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1+t^2), s = c t
+// over round-robin pair schedules (one warp per pair), V accumulating the same rotations -- until
+// every |g| <= 1e-12 sqrt(alpha beta).  Then A V = U S, sigma_j = ||(A V)_j|| and
+// W = (A V) diag((1 - tau/sigma_j)_+) V^H.  The Jacobi iteration runs in fp64 (an fp32 one stalls at
+// its round-off floor, ~m eps, above a useful orthogonality tolerance for 64 columns); the
+// spectra in and W out are fp32.
+constexpr int SVT_MAX = 64;
+
+__device__ __forceinline__ double warp_sum(double x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
+                                                        float* __restrict__ wre, float* __restrict__ wim, int m, int n,
+                                                        int64_t fstride, float tau) {
+  extern __shared__ double2 sm[];
+  double2* a = sm;                                      // column j at a + j*m
+  double2* v = a + n * m;                               // column j at v + j*n
+  __shared__ unsigned offmax;
+  __shared__ double wgt[SVT_MAX];
+  const int f = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const float* ar = re + (int64_t)f * fstride;
+  const float* ai = im + (int64_t)f * fstride;
+  // wide slices (m < n) are processed as their conjugate transpose: SVT(Y^H) = SVT(Y)^H, so the
+  // Jacobi iteration always orthogonalises min(m, n) columns of length max(m, n)
+  const int M = m, N = n;
+  const bool tr = m < n;
+  if (tr) {
+    m = N;
+    n = M;
+  }
+  for (int idx = tid; idx < n * m; idx += blockDim.x) {
+    if (!tr) {
+      a[idx] = make_double2(ar[idx], ai[idx]);
+    } else {                                            // a(i, j) = conj(Y(j, i)), Y(r, c) at c*M + r
+      const int j = idx / m, i = idx - j * m;
+      a[idx] = make_double2(ar[(int64_t)i * M + j], -ai[(int64_t)i * M + j]);
+    }
+  }
+  for (int idx = tid; idx < n * n; idx += blockDim.x) v[idx] = make_double2((idx / n) == (idx % n) ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  const int np = (n + 1) & ~1;                          // players (one dummy when n is odd)
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) offmax = 0u;
+    __syncthreads();
+    for (int r = 0; r < np - 1; ++r) {
+      for (int k = warp; k < np / 2; k += nw) {
+        // circle method: player np-1 fixed, pairs (r+k, r-k) mod (np-1)
+        const int p = k == 0 ? r : (r + k) % (np - 1);
+        const int q = k == 0 ? np - 1 : (r - k + np - 1) % (np - 1);
+        if (p >= n || q >= n) continue;
+        double2* ap = a + p * m;
+        double2* aq = a + q * m;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double2 x = ap[i], y = aq[i];
+          al += x.x * x.x + x.y * x.y;
+          be += y.x * y.x + y.y * y.y;
+          gr += x.x * y.x + x.y * y.y;                  // conj(x) * y
+          gi += x.x * y.y - x.y * y.x;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        gr = warp_sum(gr);
+        gi = warp_sum(gi);
+        const double g = sqrt(gr * gr + gi * gi);
+        const double nrm = sqrt(al * be);
+        if (!(g > 1e-12 * nrm) || !(g > 0.0)) continue;   // already orthogonal (or a zero column)
+        if (lane == 0) atomicMax(&offmax, __float_as_uint((float)(g / nrm)));
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const double er = gr / g, ei = -gi / g;          // e = conj(g) / |g|
+        for (int i = lane; i < m; i += 32) {
+          const double2 x = ap[i], y0 = aq[i];
+          const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
+          ap[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          aq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+        }
+        double2* vp = v + p * n;
+        double2* vq = v + q * n;
+        for (int i = lane; i < n; i += 32) {
+          const double2 x = vp[i], y0 = vq[i];
+          const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
+          vp[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+          vq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+        }
+      }
+      __syncthreads();
+    }
+    if (__uint_as_float(offmax) < 1e-12f) break;        // uniform: shared value after a barrier
+  }
+  // sigma_j = ||(A V)_j||, weights (1 - tau / sigma_j)_+
+  for (int j = warp; j < n; j += nw) {
+    double ss = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      const double2 x = a[j * m + i];
+      ss += x.x * x.x + x.y * x.y;
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) {
+      const double sg = sqrt(ss);
+      wgt[j] = sg > (double)tau ? 1.0 - (double)tau / sg : 0.0;
+    }
+  }
+  __syncthreads();
+  // W = (A V) diag(w) V^H : W(i, k) = sum_j a_j[i] w_j conj(v_j[k])
+  float* orr = wre + (int64_t)f * fstride;
+  float* oii = wim + (int64_t)f * fstride;
+  for (int idx = tid; idx < m * n; idx += blockDim.x) {
+    const int k = idx / m, i = idx - k * m;
+    double xr = 0.0, xi = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const double w = wgt[j];
+      if (w == 0.0) continue;
+      const double2 x = a[j * m + i], y = v[j * n + k];
+      xr += w * (x.x * y.x + x.y * y.y);                // x * conj(y)
+      xi += w * (x.y * y.x - x.x * y.y);
+    }
+    if (!tr) {
+      orr[idx] = (float)xr;
+      oii[idx] = (float)xi;
+    } else {                                            // W = (W')^H: W(k, i) = conj(W'(i, k))
+      orr[(int64_t)i * M + k] = (float)xr;
+      oii[(int64_t)i * M + k] = -(float)xi;
+    }
+  }
+}
+
+bool svt_supported(int64_t m, int64_t n) { return m >= 1 && n >= 1 && m <= SVT_MAX && n <= SVT_MAX; }
+
+int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
+                     int64_t fstride, float tau, cudaStream_t s) {
+  if (!svt_supported(m, n)) return 6;
+  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
+  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 4;
+  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
+  if (threads < 64) threads = 64;
+  if (threads > 1024) threads = 1024;
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 }  // namespace tprod

@@ -291,6 +291,22 @@ def test_tinv_gpu_long_tubes_and_errors(T):
     assert e.value.status == T._lib.TPROD_EUNSUPPORTED
 
 
+@pytest.mark.parametrize("dims,tau", [((5, 4, 6), 1.5), ((64, 64, 7), 20.0), ((33, 17, 31), 8.0),
+                                      ((8, 40, 1024), 6.0), ((1, 1, 2), 1.0), ((16, 16, 64), 0.0)],
+                         ids=lambda d: "x".join(map(str, d)) if isinstance(d, tuple) else str(d))
+def test_tsvt_gpu_vs_oracle(T, dims, tau):
+    """t-SVT (Algorithm 3) on the GPU -- production transforms + per-slice one-sided Jacobi SVT -- vs
+    the oracle's step-by-step Algorithm 3 (numpy SVD per slice); tau = 0 returns Y."""
+    n1, n2, n3 = dims
+    Y = normal((n1, n2, n3), 101 + n3)
+    X = host(T.tsvt(dev(Y), tau))
+    err = O.rel_err(X, O.tsvt(Y, tau))
+    print("tsvt", dims, tau, "rel_err", err)
+    assert err <= 1e-5
+    if tau == 0.0:
+        assert O.rel_err(X, Y) <= 1e-6
+
+
 def test_worked_examples_on_gpu(T, golden):
     for dt in (np.float32, np.float64):
         g = golden["tprod_tubes_1x1x3"]
