@@ -29,7 +29,7 @@ __all__ = [
     "dft_matrix", "circ", "bcirc", "unfold", "fold", "tprod_bcirc", "tprod_blockrow",
     "tprod_columns", "dft_mode3", "idft_mode3", "bdiag", "teye", "tran", "tprod_alg1",
     "hermitian_half", "frobenius", "inner", "rel_err", "h_slices", "tinv", "SingularTensor",
-    "tsvt", "tnn_bcirc",
+    "tsvt", "tnn_bcirc", "tsvd_values",
 ]
 
 
@@ -243,6 +243,24 @@ def tsvt(Y: np.ndarray, tau: float) -> np.ndarray:
     for i in range(hh + 1, n3 + 1):
         Wbar[:, :, i - 1] = np.conj(Wbar[:, :, (n3 - i + 2) - 1])
     return np.real(idft_mode3(Wbar))
+
+
+def tsvd_values(A: np.ndarray, rtol: float = 1e-10):
+    """Scalars of the t-SVD (Theorem 2.2, Algorithm 2 step 2), literally:
+      singular values of A:  S(i, i, 1) = (1/n3) sum_j S-bar(i, i, j)         (Eq. (14)), i < min(n1, n2),
+        S-bar(:, :, j) = the singular values of A-bar^(j) for ALL n3 slices (no symmetry used);
+      tubal rank:  #{i : S(i, i, 1) > rtol * S(1, 1, 1)}                        (Eq. (16));
+      TSN:  ||bcirc(A)||_2                                                       (Definition 2.8);
+      TNN:  sum_i S(i, i, 1)                                                     (Definition 2.9).
+    Returns (s, tnn, tsn, rank)."""
+    A = np.asarray(A, dtype=np.float64)
+    n1, n2, n3 = A.shape
+    Abar = dft_mode3(A)
+    Sbar = np.stack([np.linalg.svd(Abar[:, :, j], compute_uv=False) for j in range(n3)], axis=1)
+    s = Sbar.mean(axis=1)
+    tsn = float(np.linalg.norm(bcirc(A), 2))
+    rank = int(np.sum(s > rtol * s[0])) if s[0] > 0 else 0
+    return s, float(s.sum()), tsn, rank
 
 
 def tnn_bcirc(X: np.ndarray) -> float:

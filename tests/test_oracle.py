@@ -390,3 +390,23 @@ def test_tsvt_keeps_low_tubal_rank():
     for f in range(7):
         s = np.linalg.svd(Xb[:, :, f], compute_uv=False)
         assert s[2] < 1e-12 * max(s[0], 1.0)
+
+
+# ------------------------------------------------------------------ t-SVD scalars (NEXT-3)
+def test_tsvd_values_pins():
+    """Eq. (13): S(i,i,1) non-increasing; Def. 2.9 TNN = ||bcirc||_* / n3 (Eq. (18), independent
+    route); Def. 2.8 TSN = max spectral sigma_max (Eq. (17)); Eq. (16) tubal rank of U * V (rank 3)
+    and of teye (n); n3 = 1 reduces to the matrix singular values."""
+    A = normal((6, 5, 7), 21, np.float64)
+    s, tnn, tsn, rank = O.tsvd_values(A)
+    assert np.all(np.diff(s) <= 1e-12)
+    assert abs(tnn - O.tnn_bcirc(A)) < 1e-10 * tnn
+    Ab = O.dft_mode3(A)
+    assert abs(tsn - max(np.linalg.svd(Ab[:, :, j], compute_uv=False)[0] for j in range(7))) < 1e-10 * tsn
+    assert rank == 5
+    U = normal((6, 3, 7), 22, np.float64)
+    V = normal((3, 5, 7), 23, np.float64)
+    assert O.tsvd_values(O.tprod_bcirc(U, V))[3] == 3
+    assert O.tsvd_values(O.teye(4, 5))[3] == 4
+    np.testing.assert_allclose(O.tsvd_values(A[:, :, :1])[0], np.linalg.svd(A[:, :, 0], compute_uv=False),
+                               rtol=1e-12)
