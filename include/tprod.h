@@ -117,6 +117,15 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
 int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3, float tau, void* stream,
                    tprod_handle h);
 
+/* NEXT-3: t-SVD scalars (Theorem 2.2 / Algorithm 2 step 2, Eq. (13)-(18)) of a
+ * DEVICE n1 x n2 x n3 tensor A (Matlab layout, 1 <= n1, n2 <= 64).  Writes to the DEVICE array
+ * `out` (r + 3 floats, r = min(n1, n2)): out[0..r) = the singular values S(i,i,1) of A (Eq. (14),
+ * non-increasing), out[r] = TNN (Def. 2.9), out[r+1] = TSN = ||bcirc(A)||_2 (Def. 2.8),
+ * out[r+2] = tubal rank #{i : S(i,i,1) > rtol * S(1,1,1)} (Eq. (16)).  Same transforms and per-slice
+ * Jacobi SVD (fp64) as tprod_tsvt_f32.  Asynchronous. */
+int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, float rtol, float* out, void* stream,
+                          tprod_handle h);
+
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,
               int64_t n1, int64_t n2, int64_t n3, int64_t n4,

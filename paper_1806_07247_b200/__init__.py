@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tsvd_values", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -248,6 +248,20 @@ def tsvt(Y, tau: float, out=None, handle=None, stream=None):
     h, s = _h_s(Y, handle, stream)
     check(lib().tprod_tsvt_f32(Y.data_ptr(), out.data_ptr(), n1, n2, n3, C.c_float(tau), s, h.ptr),
           "tprod_tsvt_f32")
+    return out
+
+
+def tsvd_values(A, rtol: float = 1e-6, handle=None, stream=None):
+    """t-SVD scalars of a float32 n1 x n2 x n3 CUDA tensor (n1, n2 <= 64): returns a CUDA float32
+    vector [S(1,1,1) .. S(r,r,1), TNN, TSN, tubal rank] (Eq. (14), Def. 2.9, Def. 2.8, Eq. (16))."""
+    import torch
+    if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda or not is_matlab_layout(A):
+        raise ValueError("tsvd_values needs a float32 3-D CUDA tensor in the Matlab layout")
+    n1, n2, n3 = (int(x) for x in A.shape)
+    out = torch.empty(min(n1, n2) + 3, dtype=torch.float32, device=A.device)
+    h, s = _h_s(A, handle, stream)
+    check(lib().tprod_tsvd_values_f32(A.data_ptr(), n1, n2, n3, C.c_float(rtol), out.data_ptr(), s, h.ptr),
+          "tprod_tsvd_values_f32")
     return out
 
 

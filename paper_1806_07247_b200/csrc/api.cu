@@ -497,6 +497,44 @@ int teye_impl(T* I, int64_t n, int64_t n3, void* stream, tprod_handle h) {
   h->last_launches = 1;
   return launch_status();
 }
+// Forward transform of an n1 x n2 x n3 tensor decoded to fp32 spectral planes re/im [f][q][p]
+// (the production K1 kernels), into the handle workspace; `extra` bytes are reserved after the
+// planes (returned in *extra_ptr).  Used by t-SVT / t-SVD scalars.
+int spectral_planes(tprod_ctx* h, const float* Y, int64_t n1, int64_t n2, int64_t n3, size_t extra, float** re,
+                    float** im, void** extra_ptr, Twiddles32* Tout, cudaStream_t s) {
+  int st;
+  const int64_t hh = h_slices(n3), ld = round_up(n1, 8), mn = n1 * n2;
+  int f1 = 0, f2 = 0;
+  fourstep_factors(n3, &f1, &f2);
+  const size_t wb = f1 ? 4 * (size_t)(n1 * n2 * n3) : 0;
+  size_t o = 0;
+  const size_t off_max = o;  o = align_up(o + 4 * (size_t)n1, 1024);
+  const size_t off_u = o;    o = align_up(o + 4 * (size_t)n1, 1024);
+  const size_t off_sp = o;   o = align_up(o + 2 * (size_t)(hh * NPLANES * n2 * ld), 1024);
+  const size_t off_re = o;   o = align_up(o + 4 * (size_t)(2 * hh * mn), 1024);
+  const size_t off_x = o;    o = align_up(o + extra, 1024);
+  const size_t off_w = o;    o = align_up(o + wb, 1024);
+  if ((st = ensure_ws(h, o))) return st;
+  char* ws = (char*)h->ws;
+  Twiddles32 T;
+  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  T.staged = h->transform == 0;
+  T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
+  T.scratch_bytes = wb;
+  unsigned* mx = (unsigned*)(ws + off_max);
+  float* u = (float*)(ws + off_u);
+  __half* sp = (__half*)(ws + off_sp);
+  *re = (float*)(ws + off_re);
+  *im = *re + hh * mn;
+  *extra_ptr = ws + off_x;
+  CK(cudaMemsetAsync(mx, 0, 4 * (size_t)n1, s));
+  launch_absmax(Y, n1, n2, n3, 0, mx, s);
+  launch_fwd_split(Y, n1, n2, n3, 0, mx, T, sp, ld, u, h->num_sms, s);
+  launch_decode_split(sp, ld, n1, n2, n3, 0, u, *re, *im, s);
+  *Tout = T;
+  return launch_status();
+}
+
 }  // namespace
 
 // ====================================================================== exported C ABI
@@ -673,35 +711,33 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   if (overlaps(Y, b, X, b)) return TPROD_EALIAS;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t hh = h_slices(n3), ld = round_up(n1, 8), mn = n1 * n2;
-  int f1 = 0, f2 = 0;
-  fourstep_factors(n3, &f1, &f2);
-  size_t o = 0;
-  const size_t off_max = o;  o = align_up(o + 4 * (size_t)n1, 1024);
-  const size_t off_u = o;    o = align_up(o + 4 * (size_t)n1, 1024);
-  const size_t off_sp = o;   o = align_up(o + 2 * (size_t)(hh * NPLANES * n2 * ld), 1024);
-  const size_t off_re = o;   o = align_up(o + 4 * (size_t)(4 * hh * mn), 1024);   // re, im, wre, wim
-  const size_t off_w = o;    o = align_up(o + (f1 ? b : 0), 1024);
-  if ((st = ensure_ws(h, o))) return st;
-  char* ws = (char*)h->ws;
+  const int64_t hh = h_slices(n3), mn = n1 * n2;
+  float *re, *im;
+  void* extra;
   Twiddles32 T;
-  if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
-  T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
-  T.scratch_bytes = f1 ? b : 0;
-  unsigned* mx = (unsigned*)(ws + off_max);
-  float* u = (float*)(ws + off_u);
-  __half* sp = (__half*)(ws + off_sp);
-  float* re = (float*)(ws + off_re);
-  float* im = re + hh * mn;
-  float* wre = im + hh * mn;
+  if ((st = spectral_planes(h, Y, n1, n2, n3, 4 * (size_t)(2 * hh * mn), &re, &im, &extra, &T, s))) return st;  // Alg. 3 step 1
+  float* wre = (float*)extra;
   float* wim = wre + hh * mn;
-  CK(cudaMemsetAsync(mx, 0, 4 * (size_t)n1, s));
-  launch_absmax(Y, n1, n2, n3, 0, mx, s);
-  launch_fwd_split(Y, n1, n2, n3, 0, mx, T, sp, ld, u, h->num_sms, s);        // Alg. 3 step 1
-  launch_decode_split(sp, ld, n1, n2, n3, 0, u, re, im, s);
   if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, s)) return TPROD_ECUDA;   // step 2
   launch_inv_f32(wre, wim, n1, mn, n1, n2, n3, T, X, h->num_sms, s);         // step 2b + 3
+  h->last_launches = 5;
+  return launch_status();
+}
+
+int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, float rtol, float* out, void* stream,
+                          tprod_handle h) {
+  if (!h || !A || !out || !(rtol >= 0.f)) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, 1);
+  if (st) return st;
+  if (!svt_supported(n1, n2)) return TPROD_EUNSUPPORTED;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t hh = h_slices(n3), r = std::min(n1, n2);
+  float *re, *im;
+  void* extra;
+  Twiddles32 T;
+  if ((st = spectral_planes(h, A, n1, n2, n3, 8 * (size_t)(hh * r), &re, &im, &extra, &T, s))) return st;  // Alg. 2 step 1
+  if (launch_tsvd_values(re, im, n1, n2, hh, n3, n1 * n2, (double*)extra, rtol, out, s)) return TPROD_ECUDA;
   h->last_launches = 5;
   return launch_status();
 }

@@ -203,7 +203,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
                                                         float* __restrict__ wre, float* __restrict__ wim, int m, int n,
-                                                        int64_t fstride, float tau) {
+                                                        int64_t fstride, float tau, double* __restrict__ sv) {
   extern __shared__ double2 sm[];
   double2* a = sm;                                      // column j at a + j*m
   double2* v = a + n * m;                               // column j at v + j*n
@@ -291,10 +291,19 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
     ss = warp_sum(ss);
     if (lane == 0) {
       const double sg = sqrt(ss);
-      wgt[j] = sg > (double)tau ? 1.0 - (double)tau / sg : 0.0;
+      wgt[j] = sv ? sg : (sg > (double)tau ? 1.0 - (double)tau / sg : 0.0);
     }
   }
   __syncthreads();
+  if (sv) {
+    // singular values only (t-SVD scalars): slice f's n values in non-increasing order
+    for (int j = tid; j < n; j += blockDim.x) {
+      int pos = 0;
+      for (int k = 0; k < n; ++k) pos += (wgt[k] > wgt[j]) || (wgt[k] == wgt[j] && k < j);
+      sv[(int64_t)f * n + pos] = wgt[j];
+    }
+    return;
+  }
   // W = (A V) diag(w) V^H : W(i, k) = sum_j a_j[i] w_j conj(v_j[k])
   float* orr = wre + (int64_t)f * fstride;
   float* oii = wim + (int64_t)f * fstride;
@@ -329,7 +338,53 @@ int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, i
   int threads = 32 * (int)((std::min(m, n) + 1) / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau);
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
+// t-SVD scalars (NEXT-3).  sv: [h][r] per-slice singular values (r = min(m, n), non-increasing).
+// out[0..r) = S(i, i, 1) = (1/n3) sum_{j < n3} S-bar(i, i, j) (Eq. (14)) with the conjugate pairs
+// j, n3 - j sharing singular values (Eq. (8)); out[r] = TNN = sum_i S(i,i,1) (Def. 2.9);
+// out[r+1] = TSN = max_j S-bar(1, 1, j) (Def. 2.8, Eq. (17)); out[r+2] = #{i : S(i,i,1) > rtol S(1,1,1)}
+// (Eq. (16)).  One CTA.
+__global__ void tsvd_reduce_kernel(const double* __restrict__ sv, int r, int h, int n3, float rtol,
+                                   float* __restrict__ out) {
+  __shared__ double s[SVT_MAX];
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    double acc = 0.0;
+    for (int f = 0; f < h; ++f) {
+      const double w = (f == 0 || 2 * f == n3) ? 1.0 : 2.0;
+      acc += w * sv[(int64_t)f * r + i];
+    }
+    s[i] = acc / n3;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tnn = 0.0, tsn = 0.0;
+    int rank = 0;
+    for (int i = 0; i < r; ++i) {
+      tnn += s[i];
+      out[i] = (float)s[i];
+      if (s[0] > 0.0 && s[i] > (double)rtol * s[0]) ++rank;
+    }
+    for (int f = 0; f < h; ++f) tsn = fmax(tsn, sv[(int64_t)f * r]);
+    out[r] = (float)tnn;
+    out[r + 1] = (float)tsn;
+    out[r + 2] = (float)rank;
+  }
+}
+
+int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
+                       double* sv, float rtol, float* out, cudaStream_t s) {
+  if (!svt_supported(m, n)) return 6;
+  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
+  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 4;
+  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
+  if (threads < 64) threads = 64;
+  if (threads > 1024) threads = 1024;
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, sv);
+  tsvd_reduce_kernel<<<1, 64, 0, s>>>(sv, (int)std::min(m, n), (int)h, (int)n3, rtol, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

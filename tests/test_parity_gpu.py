@@ -307,6 +307,30 @@ def test_tsvt_gpu_vs_oracle(T, dims, tau):
         assert O.rel_err(X, Y) <= 1e-6
 
 
+@pytest.mark.parametrize("dims", [(6, 5, 7), (64, 64, 8), (40, 12, 33), (16, 16, 100)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_tsvd_values_gpu_vs_oracle(T, dims):
+    """t-SVD scalars on the GPU (per-slice Jacobi SVD + Eq. (14) reduction) vs the oracle: singular
+    values, TNN, TSN (the oracle's through bcirc), tubal rank."""
+    n1, n2, n3 = dims
+    A = normal((n1, n2, n3), 111 + n3)
+    out = host(T.tsvd_values(dev(A), rtol=1e-6))
+    r = min(n1, n2)
+    s, tnn, tsn, rank = O.tsvd_values(A, rtol=1e-6)
+    np.testing.assert_allclose(out[:r], s, rtol=2e-5, atol=2e-5 * s[0])
+    assert abs(out[r] - tnn) <= 2e-5 * tnn and abs(out[r + 1] - tsn) <= 2e-5 * tsn
+    assert int(out[r + 2]) == rank
+
+
+def test_tsvd_tubal_rank_gpu(T):
+    """Tubal rank of U * V (Def. 2.7) with U 40 x 5 x 31, V 5 x 30 x 31 is 5 on the GPU."""
+    U = normal((40, 5, 31), 121, np.float64)
+    V = normal((5, 30, 31), 122, np.float64)
+    A = O.tprod_bcirc(U, V).astype(np.float32)
+    out = host(T.tsvd_values(dev(A), rtol=1e-4))
+    assert int(out[30 + 2]) == 5
+
+
 def test_worked_examples_on_gpu(T, golden):
     for dt in (np.float32, np.float64):
         g = golden["tprod_tubes_1x1x3"]
