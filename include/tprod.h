@@ -87,7 +87,8 @@ int tprod_f32(const float* A, const float* B, float* C,
  * the inverse.  The result is bitwise identical to tprod_f32(A, B, C, ...) (same kernels, same
  * operand values, same K order).  Errors: TPROD_EINVAL if nothing is prepared or an argument is
  * invalid, TPROD_EALIAS if C overlaps B, TPROD_ENOMEM.  tprod_release_a frees the prepared
- * operand (also done by tprod_destroy and by the next tprod_prepare_a_f32). */
+ * operand (also done by tprod_destroy and by the next tprod_prepare_a_f32).  Calls on one handle are
+ * stream-ordered: prepare on the stream of the later tprod_f32_prepared calls, or synchronise. */
 int tprod_prepare_a_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
 int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod_handle h);
 int tprod_release_a(tprod_handle h);

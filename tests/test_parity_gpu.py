@@ -3,6 +3,7 @@
 Bar (BASELINE.json north_star): relative Frobenius error <= 1e-5 on the fp32 path and <= 1e-12
 on the fp64 path, the oracle always evaluated on the exact (rounded) values the GPU saw."""
 import numpy as np
+from ctypes import c_float as C_float
 import pytest
 
 import oracle as O
@@ -329,6 +330,29 @@ def test_tsvd_tubal_rank_gpu(T):
     A = O.tprod_bcirc(U, V).astype(np.float32)
     out = host(T.tsvd_values(dev(A), rtol=1e-4))
     assert int(out[30 + 2]) == 5
+
+
+def test_next_rows_argument_errors(T):
+    """Argument errors of the NEXT-row entry points come back before any work: tau < 0 / NaN,
+    slices beyond the 64 x 64 Jacobi kernel, aliasing output."""
+    import torch
+    L = T._lib.lib()
+    h = T.Handle()
+    Y = dev(normal((4, 3, 5), 1))
+    X = dev(normal((4, 3, 5), 2))
+    assert L.tprod_tsvt_f32(Y.data_ptr(), X.data_ptr(), 4, 3, 5, C_float(-1.0), None, h.ptr) == T._lib.TPROD_EINVAL
+    assert L.tprod_tsvt_f32(Y.data_ptr(), X.data_ptr(), 4, 3, 5, C_float(float("nan")), None, h.ptr) == T._lib.TPROD_EINVAL
+    assert L.tprod_tsvt_f32(Y.data_ptr(), Y.data_ptr(), 4, 3, 5, C_float(1.0), None, h.ptr) == T._lib.TPROD_EALIAS
+    big = dev(normal((65, 3, 2), 3))
+    with pytest.raises(T.TprodError) as e:
+        T.tsvt(big, 1.0)
+    assert e.value.status == T._lib.TPROD_EUNSUPPORTED
+    with pytest.raises(T.TprodError) as e:
+        T.tsvd_values(big)
+    assert e.value.status == T._lib.TPROD_EUNSUPPORTED
+    assert L.tprod_tran_f32(Y.data_ptr(), Y.data_ptr(), 4, 3, 5, None, h.ptr) == T._lib.TPROD_EALIAS
+    assert L.tprod_teye_f32(None, 3, 2, None, h.ptr) == T._lib.TPROD_EINVAL
+    assert L.tprod_tinv_f32(Y.data_ptr(), X.data_ptr(), 0, 5, None, h.ptr) == T._lib.TPROD_EINVAL
 
 
 def test_worked_examples_on_gpu(T, golden):
