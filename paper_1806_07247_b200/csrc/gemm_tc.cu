@@ -538,7 +538,7 @@ template <int SEGKB>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
-                    const float* __restrict__ uA, const float* __restrict__ uB, int GM, int nyq) {
+                    const float* __restrict__ uA, const float* __restrict__ uB, int nyq) {
   constexpr int BN = 128;
   constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
   constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
@@ -590,21 +590,13 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   // Tile order: n fastest, then m, then f; concurrently running pairs share the A_f panel.
   // (Measured on config 5, DRAM read per launch: n fastest 149-165 GB, m fastest 185 GB, groups of
   // 6 m-tiles per n sweep 180 GB -- the pairs drift apart in K by up to a tile, longer than an L2
-  // residency, so no raster order recovers the reuse; the plain order stays.  GM = 0 keeps it.)
+  // residency, so no raster order recovers the reuse; the plain order stays.)
   const int64_t tpf = (int64_t)mt * nt;
   auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {
     f = (int)(t / tpf);
     const int r = (int)(t - (int64_t)f * tpf);
-    if (GM == 0) {
-      n0 = (r % nt) * BN;
-      m0 = (r / nt) * (2 * BM);
-      return;
-    }
-
-    const int grp = r / (GM * nt), w = r - grp * GM * nt;
-    const int gm = min(GM, mt - grp * GM);
-    n0 = (w / gm) * BN;
-    m0 = (grp * GM + w % gm) * (2 * BM);
+    n0 = (r % nt) * BN;
+    m0 = (r / nt) * (2 * BM);
   };
 
   if (warp == 0) {
@@ -869,8 +861,7 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
-  const int GM = 0;   // plain n-fastest tile order (see gemm_tc2_kernel)
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, GM, nyq) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, nyq) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
