@@ -29,7 +29,7 @@ __all__ = [
     "dft_matrix", "circ", "bcirc", "unfold", "fold", "tprod_bcirc", "tprod_blockrow",
     "tprod_columns", "dft_mode3", "idft_mode3", "bdiag", "teye", "tran", "tprod_alg1",
     "hermitian_half", "frobenius", "inner", "rel_err", "h_slices", "tinv", "SingularTensor",
-    "tsvt", "tnn_bcirc", "tsvd_values",
+    "tsvt", "tnn_bcirc", "tsvd_values", "tsvd",
 ]
 
 
@@ -261,6 +261,30 @@ def tsvd_values(A: np.ndarray, rtol: float = 1e-10):
     tsn = float(np.linalg.norm(bcirc(A), 2))
     rank = int(np.sum(s > rtol * s[0])) if s[0] > 0 else 0
     return s, float(s.sum()), tsn, rank
+
+
+def tsvd(A: np.ndarray):
+    """Algorithm 2, T-SVD, step by step, in its skinny form (r = min(n1, n2)
+    columns, reading R17): A-bar = fft(A, [], 3); for i = 1..ceil((n3+1)/2):
+    [U-bar, S-bar, V-bar] = SVD(A-bar^(i)); the rest by conjugation (S-bar copied); U = ifft(U-bar),
+    S = ifft(S-bar), V = ifft(V-bar).  Returns (U n1 x r x n3, S r x r x n3, V n2 x r x n3) with
+    A = U * S * V^* (Theorem 2.2, Eq. (12)).  The factors are unique up to a unit phase per
+    singular vector and spectral slice; S is unique."""
+    A = np.asarray(A, dtype=np.float64)
+    n1, n2, n3 = A.shape
+    r = min(n1, n2)
+    Ab = dft_mode3(A)
+    Ub = np.empty((n1, r, n3), dtype=np.complex128)
+    Sb = np.zeros((r, r, n3), dtype=np.complex128)
+    Vb = np.empty((n2, r, n3), dtype=np.complex128)
+    hh = h_slices(n3)
+    for i in range(1, hh + 1):
+        U, S, Vh = np.linalg.svd(Ab[:, :, i - 1], full_matrices=False)
+        Ub[:, :, i - 1], Sb[:, :, i - 1], Vb[:, :, i - 1] = U, np.diag(S), Vh.conj().T
+    for i in range(hh + 1, n3 + 1):
+        j = (n3 - i + 2) - 1
+        Ub[:, :, i - 1], Sb[:, :, i - 1], Vb[:, :, i - 1] = np.conj(Ub[:, :, j]), Sb[:, :, j], np.conj(Vb[:, :, j])
+    return (np.real(idft_mode3(Ub)), np.real(idft_mode3(Sb)), np.real(idft_mode3(Vb)))
 
 
 def tnn_bcirc(X: np.ndarray) -> float:

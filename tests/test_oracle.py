@@ -410,3 +410,21 @@ def test_tsvd_values_pins():
     assert O.tsvd_values(O.teye(4, 5))[3] == 4
     np.testing.assert_allclose(O.tsvd_values(A[:, :, :1])[0], np.linalg.svd(A[:, :, 0], compute_uv=False),
                                rtol=1e-12)
+
+
+def test_tsvd_factors_pins():
+    """Theorem 2.2 / Eq. (12): A = U * S * V^* (t-products through bcirc, Def. 2.2 transpose);
+    skinny orthogonality U^* * U = V^* * V = I (Def. 2.5 on r columns); S f-diagonal (Def. 2.6)
+    with S(:,:,1)'s diagonal = the Eq. (14) singular values; wide and tall shapes."""
+    for dims, seed in (((6, 4, 5), 31), ((3, 7, 4), 32), ((5, 5, 1), 33)):
+        A = normal(dims, seed, np.float64)
+        U, S, V = O.tsvd(A)
+        r = min(dims[0], dims[1])
+        assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A) < 1e-13
+        assert O.rel_err(O.tprod_bcirc(O.tran(U), U), O.teye(r, dims[2])) < 1e-13
+        assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, dims[2])) < 1e-13
+        off = S.copy()
+        for k in range(dims[2]):
+            off[:, :, k] -= np.diag(np.diag(S[:, :, k]))
+        assert np.abs(off).max() < 1e-13
+        np.testing.assert_allclose(np.diag(S[:, :, 0]), O.tsvd_values(A)[0], rtol=1e-12)
