@@ -126,6 +126,14 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
  * Jacobi SVD (fp64) as tprod_tsvt_f32.  Asynchronous. */
 int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, float rtol, float* out, void* stream,
                           tprod_handle h);
+/* Skinny t-SVD factors (Algorithm 2, Theorem 2.2 Eq. (12); R17): A = U * S * V^* with
+ * U n1 x r x n3, S r x r x n3 (f-diagonal), V n2 x r x n3, r = min(n1, n2) <= 64, all DEVICE
+ * pointers in Matlab layout.  Per spectral slice f < h the Jacobi SVD's factors (columns in
+ * non-increasing singular-value order), conjugate fill and inverse DFT of each factor.  Singular
+ * vectors are unique up to a unit phase per column and slice (S is unique); a zero singular value
+ * leaves a zero left-vector column.  Asynchronous. */
+int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3, void* stream,
+                   tprod_handle h);
 
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,

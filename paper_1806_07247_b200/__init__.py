@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tsvd_values", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tsvd_values", "tsvd", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -263,6 +263,23 @@ def tsvd_values(A, rtol: float = 1e-6, handle=None, stream=None):
     check(lib().tprod_tsvd_values_f32(A.data_ptr(), n1, n2, n3, C.c_float(rtol), out.data_ptr(), s, h.ptr),
           "tprod_tsvd_values_f32")
     return out
+
+
+def tsvd(A, handle=None, stream=None):
+    """Skinny t-SVD (Algorithm 2) of a float32 n1 x n2 x n3 CUDA tensor (min(n1, n2) <= 64, both <= 64):
+    returns (U n1 x r x n3, S r x r x n3, V n2 x r x n3) with A = U * S * V^*."""
+    import torch
+    if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda or not is_matlab_layout(A):
+        raise ValueError("tsvd needs a float32 3-D CUDA tensor in the Matlab layout")
+    n1, n2, n3 = (int(x) for x in A.shape)
+    r = min(n1, n2)
+    U = matlab_empty(n1, r, n3, torch.float32, A.device)
+    S = matlab_empty(r, r, n3, torch.float32, A.device)
+    V = matlab_empty(n2, r, n3, torch.float32, A.device)
+    h, s = _h_s(A, handle, stream)
+    check(lib().tprod_tsvd_f32(A.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), n1, n2, n3, s, h.ptr),
+          "tprod_tsvd_f32")
+    return U, S, V
 
 
 def tprod_f32(A, B, out=None, handle=None, stream=None):

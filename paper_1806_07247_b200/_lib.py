@@ -45,6 +45,7 @@ SIGNATURES = {
     "tprod_tinv_f32": (_int, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "tprod_tsvt_f32": (_int, [_vp, _vp, _i64, _i64, _i64, C.c_float, _vp, _vp]),
     "tprod_tsvd_values_f32": (_int, [_vp, _i64, _i64, _i64, C.c_float, _vp, _vp, _vp]),
+    "tprod_tsvd_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
 }
 
 _lib = None

@@ -724,6 +724,37 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   return launch_status();
 }
 
+int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3, void* stream,
+                   tprod_handle h) {
+  if (!h || !A || !U || !S || !V) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, 1);
+  if (st) return st;
+  if (!svt_supported(n1, n2)) return TPROD_EUNSUPPORTED;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t hh = h_slices(n3), r = std::min(n1, n2);
+  const int64_t nu = n1 * r, ns = r * r, nv = n2 * r;
+  float *re, *im;
+  void* extra;
+  Twiddles32 T;
+  const size_t ex = 4 * (size_t)(hh * (2 * nu + 2 * ns + 2 * nv));
+  if ((st = spectral_planes(h, A, n1, n2, n3, ex, &re, &im, &extra, &T, s))) return st;   // Alg. 2 step 1
+  float* ure = (float*)extra;
+  float* uim = ure + hh * nu;
+  float* sre = uim + hh * nu;
+  float* sim = sre + hh * ns;
+  float* vre = sim + hh * ns;
+  float* vim = vre + hh * nv;
+  CK(cudaMemsetAsync(sim, 0, 4 * (size_t)(hh * ns), s));                                  // S-bar is real
+  if (launch_slice_svd_factors(re, im, n1, n2, hh, n1 * n2, ure, uim, sre, vre, vim, s)) return TPROD_ECUDA;  // step 2
+  // step 2b + 3: conjugate fill + inverse DFT of each factor (S-bar's copy rule = conj of a real slice)
+  launch_inv_f32(ure, uim, n1, nu, n1, r, n3, T, U, h->num_sms, s);
+  launch_inv_f32(sre, sim, r, ns, r, r, n3, T, S, h->num_sms, s);
+  launch_inv_f32(vre, vim, n2, nv, n2, r, n3, T, V, h->num_sms, s);
+  h->last_launches = 8;
+  return launch_status();
+}
+
 int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, float rtol, float* out, void* stream,
                           tprod_handle h) {
   if (!h || !A || !out || !(rtol >= 0.f)) return TPROD_EINVAL;

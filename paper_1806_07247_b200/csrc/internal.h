@@ -106,6 +106,8 @@ void launch_absmax_planes(const float* re, const float* im, int64_t count, unsig
 bool svt_supported(int64_t m, int64_t n);
 int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
                      int64_t fstride, float tau, cudaStream_t s);
+int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
+                             float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s);
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
                        double* sv, float rtol, float* out, cudaStream_t s);
 

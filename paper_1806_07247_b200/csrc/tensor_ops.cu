@@ -201,9 +201,14 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+struct SvdOut {               // per-slice skinny SVD factors (t-SVD), planes [f][col][row], r = min(M, N)
+  float *ure, *uim, *sre, *vre, *vim;
+};
+
 __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
                                                         float* __restrict__ wre, float* __restrict__ wim, int m, int n,
-                                                        int64_t fstride, float tau, double* __restrict__ sv) {
+                                                        int64_t fstride, float tau, double* __restrict__ sv,
+                                                        SvdOut fo) {
   extern __shared__ double2 sm[];
   double2* a = sm;                                      // column j at a + j*m
   double2* v = a + n * m;                               // column j at v + j*n
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
     ss = warp_sum(ss);
     if (lane == 0) {
       const double sg = sqrt(ss);
-      wgt[j] = sv ? sg : (sg > (double)tau ? 1.0 - (double)tau / sg : 0.0);
+      wgt[j] = (sv || fo.ure) ? sg : (sg > (double)tau ? 1.0 - (double)tau / sg : 0.0);   // sigma or SVT weight
     }
   }
   __syncthreads();
@@ -301,6 +306,38 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
       int pos = 0;
       for (int k = 0; k < n; ++k) pos += (wgt[k] > wgt[j]) || (wgt[k] == wgt[j] && k < j);
       sv[(int64_t)f * n + pos] = wgt[j];
+    }
+    return;
+  }
+  if (fo.ure) {
+    // skinny SVD factors, columns in non-increasing sigma order: left vectors (A V)_j / sigma_j
+    // (zero for sigma_j = 0), right vectors v_j; for a transposed (wide) slice the roles swap:
+    // Y^H = L S R^H gives Y = R S L^H, i.e. U = R and V = L (no conjugation)
+    const int r = n;                                     // n = min(M, N) after the swap
+    const int64_t uo = (int64_t)f * M * r, vo = (int64_t)f * N * r, so = (int64_t)f * r * r;
+    for (int idx = tid; idx < r * r; idx += blockDim.x) fo.sre[so + idx] = 0.f;
+    __syncthreads();
+    for (int j = tid; j < n; j += blockDim.x) {
+      int pos = 0;
+      for (int k = 0; k < n; ++k) pos += (wgt[k] > wgt[j]) || (wgt[k] == wgt[j] && k < j);
+      const double sg = wgt[j];
+      const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
+      fo.sre[so + (int64_t)pos * r + pos] = (float)sg;
+      // left vectors: length m (rows of the processed matrix), right: length n
+      float* lre = tr ? fo.vre + vo : fo.ure + uo;        // left vectors of the processed matrix
+      float* lim = tr ? fo.vim + vo : fo.uim + uo;
+      float* rre = tr ? fo.ure + uo : fo.vre + vo;
+      float* rim = tr ? fo.uim + uo : fo.vim + vo;
+      for (int i = 0; i < m; ++i) {
+        const double2 x = a[j * m + i];
+        lre[(int64_t)pos * m + i] = (float)(x.x * inv);
+        lim[(int64_t)pos * m + i] = (float)(x.y * inv);
+      }
+      for (int i = 0; i < n; ++i) {
+        const double2 y = v[j * n + i];
+        rre[(int64_t)pos * n + i] = (float)y.x;
+        rim[(int64_t)pos * n + i] = (float)y.y;
+      }
     }
     return;
   }
@@ -338,7 +375,8 @@ int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, i
   int threads = 32 * (int)((std::min(m, n) + 1) / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, nullptr);
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, nullptr,
+                                                      SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr});
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -374,6 +412,20 @@ __global__ void tsvd_reduce_kernel(const double* __restrict__ sv, int r, int h, 
   }
 }
 
+int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
+                             float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s) {
+  if (!svt_supported(m, n)) return 6;
+  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
+  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 4;
+  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
+  if (threads < 64) threads = 64;
+  if (threads > 1024) threads = 1024;
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, nullptr,
+                                                      SvdOut{ure, uim, sre, vre, vim});
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
                        double* sv, float rtol, float* out, cudaStream_t s) {
   if (!svt_supported(m, n)) return 6;
@@ -383,7 +435,8 @@ int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, i
   int threads = 32 * (int)((std::min(m, n) + 1) / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, sv);
+  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, sv,
+                                                      SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr});
   tsvd_reduce_kernel<<<1, 64, 0, s>>>(sv, (int)std::min(m, n), (int)h, (int)n3, rtol, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }

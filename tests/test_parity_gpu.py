@@ -332,6 +332,24 @@ def test_tsvd_tubal_rank_gpu(T):
     assert int(out[30 + 2]) == 5
 
 
+@pytest.mark.parametrize("dims", [(6, 4, 5), (3, 7, 4), (64, 48, 9), (20, 64, 31), (8, 8, 64)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_tsvd_factors_gpu(T, dims):
+    """Skinny t-SVD on the GPU: S equals the oracle's (unique); U, V (unique only up to phases) are
+    checked by what holds for any valid factorisation, in the oracle: A = U * S * V^* and
+    U^* * U = V^* * V = I."""
+    n1, n2, n3 = dims
+    r = min(n1, n2)
+    A = normal(dims, 131 + n3)
+    U, S, V = (host(x) for x in T.tsvd(dev(A)))
+    _, S_ref, _ = O.tsvd(A)
+    assert O.rel_err(S, S_ref) <= 1e-5
+    A64 = A.astype(np.float64)
+    assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A64) <= 1e-5
+    assert O.rel_err(O.tprod_bcirc(O.tran(U), U), O.teye(r, n3)) <= 1e-5
+    assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, n3)) <= 1e-5
+
+
 def test_next_rows_argument_errors(T):
     """Argument errors of the NEXT-row entry points come back before any work: tau < 0 / NaN,
     slices beyond the 64 x 64 Jacobi kernel, aliasing output."""
