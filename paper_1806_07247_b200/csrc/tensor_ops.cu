@@ -190,7 +190,7 @@ namespace tprod {
 //   a_q' = a_q e (e = conj(g)/|g|, g = a_p^H a_q),  [a_p, a_q'] <- [a_p, a_q'] [[c, s], [-s, c]],
 //   zeta = (beta - alpha) / (2|g|), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1+t^2), s = c t
 // over round-robin pair schedules (one warp per pair), V accumulating the same rotations -- until
-// every |g| <= 1e-12 sqrt(alpha beta).  Then A V = U S, sigma_j = ||(A V)_j|| and
+// every |g| <= 1e-10 sqrt(alpha beta) (the fp32 spectra in are accurate to ~1e-7).  Then A V = U S, sigma_j = ||(A V)_j|| and
 // W = (A V) diag((1 - tau/sigma_j)_+) V^H.  The Jacobi iteration runs in fp64 (an fp32 one stalls at
 // its round-off floor, ~m eps, above a useful orthogonality tolerance for 64 columns); the
 // spectra in and W out are fp32.
@@ -259,14 +259,20 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
         be = warp_sum(be);
         gr = warp_sum(gr);
         gi = warp_sum(gi);
-        const double g = sqrt(gr * gr + gi * gi);
-        const double nrm = sqrt(al * be);
-        if (!(g > 1e-12 * nrm) || !(g > 0.0)) continue;   // already orthogonal (or a zero column)
-        if (lane == 0) atomicMax(&offmax, __float_as_uint((float)(g / nrm)));
-        const double zeta = (be - al) / (2.0 * g);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        const double er = gr / g, ei = -gi / g;          // e = conj(g) / |g|
+        const double g2 = gr * gr + gi * gi;
+        if (!(g2 > 1e-20 * al * be) || !(g2 > 0.0)) continue;   // already orthogonal (or a zero column)
+        // fp64 divisions / square roots are slow: the angle comes from fp32 estimates (an approximate
+        // Jacobi angle still converges), and the quantities that must be exact to fp64 -- the unit
+        // phase e and the rotation's c^2 + s^2 = 1 -- get one Newton step of rsqrt in fp64
+        float ig32 = rsqrtf((float)g2);
+        const double ig = (double)ig32 * (1.5 - 0.5 * g2 * (double)ig32 * (double)ig32);   // 1 / |g|
+        if (lane == 0) atomicMax(&offmax, __float_as_uint((float)(g2 / (al * be))));
+        const float zeta = (float)((be - al) * 0.5 * ig);
+        const float t32 = copysignf(1.f, zeta) / (fabsf(zeta) + sqrtf(1.f + zeta * zeta));
+        const double t = t32, t2p1 = 1.0 + t * t;
+        const float c32 = rsqrtf((float)t2p1);
+        const double c = (double)c32 * (1.5 - 0.5 * t2p1 * (double)c32 * (double)c32), s = c * t;
+        const double er = gr * ig, ei = -gi * ig;         // e = conj(g) / |g|
         for (int i = lane; i < m; i += 32) {
           const double2 x = ap[i], y0 = aq[i];
           const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
@@ -284,7 +290,7 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
       }
       __syncthreads();
     }
-    if (__uint_as_float(offmax) < 1e-12f) break;        // uniform: shared value after a barrier
+    if (__uint_as_float(offmax) < 1e-20f) break;        // (|g|^2 / alpha beta) uniform: shared value after a barrier
   }
   // sigma_j = ||(A V)_j||, weights (1 - tau / sigma_j)_+
   for (int j = warp; j < n; j += nw) {
