@@ -11,6 +11,8 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace tprod {
 
@@ -189,30 +191,33 @@ namespace tprod {
 // slice in shared memory -- columns p, q orthogonalised by the complex rotation
 //   a_q' = a_q e (e = conj(g)/|g|, g = a_p^H a_q),  [a_p, a_q'] <- [a_p, a_q'] [[c, s], [-s, c]],
 //   zeta = (beta - alpha) / (2|g|), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), c = 1/sqrt(1+t^2), s = c t
-// over round-robin pair schedules (one warp per pair), V accumulating the same rotations -- until
+// over round-robin pair schedules (a group of G lanes per pair), V accumulating the same rotations -- until
 // every |g| <= 1e-10 sqrt(alpha beta) (the fp32 spectra in are accurate to ~1e-7).  Then A V = U S, sigma_j = ||(A V)_j|| and
 // W = (A V) diag((1 - tau/sigma_j)_+) V^H.  The Jacobi iteration runs in fp64 (an fp32 one stalls at
 // its round-off floor, ~m eps, above a useful orthogonality tolerance for 64 columns); the
 // spectra in and W out are fp32.
 constexpr int SVT_MAX = 64;
 
-__device__ __forceinline__ double warp_sum(double x) {
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+template <int G>
+__device__ __forceinline__ double group_sum(double x) {   // sum over an aligned group of G lanes
+  for (int o = G / 2; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
+__device__ __forceinline__ double warp_sum(double x) { return group_sum<32>(x); }
 
 struct SvdOut {               // per-slice skinny SVD factors (t-SVD), planes [f][col][row], r = min(M, N)
   float *ure, *uim, *sre, *vre, *vim;
 };
 
-__global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
+template <int G>
+__global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
                                                         float* __restrict__ wre, float* __restrict__ wim, int m, int n,
                                                         int64_t fstride, float tau, double* __restrict__ sv,
                                                         SvdOut fo) {
   extern __shared__ double2 sm[];
   double2* a = sm;                                      // column j at a + j*m
   double2* v = a + n * m;                               // column j at v + j*n
-  __shared__ unsigned offmax;
+  __shared__ int rotated[3];                            // per-sweep "some pair rotated" flags, cycled mod 3
   __shared__ double wgt[SVT_MAX];
   const int f = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   const float* ar = re + (int64_t)f * fstride;
@@ -233,65 +238,111 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
       a[idx] = make_double2(ar[(int64_t)i * M + j], -ai[(int64_t)i * M + j]);
     }
   }
-  for (int idx = tid; idx < n * n; idx += blockDim.x) v[idx] = make_double2((idx / n) == (idx % n) ? 1.0 : 0.0, 0.0);
+  if (sv == nullptr)                                    // V is not formed for singular values only
+    for (int idx = tid; idx < n * n; idx += blockDim.x) v[idx] = make_double2((idx / n) == (idx % n) ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  if (tid < 3) rotated[tid] = 0;
   __syncthreads();
   const int np = (n + 1) & ~1;                          // players (one dummy when n is odd)
+  const bool want_v = sv == nullptr;                    // singular values only: V is never formed
+  constexpr int GPW = 32 / G;                           // pairs per warp
+  constexpr int L = (G == 8 ? 32 : SVT_MAX) / G;        // elements per lane (G = 8 only for columns <= 32)
+  const int gl = lane & (G - 1), gw = lane / G;
+#ifdef TPROD_SVT_DEBUG
+  const long long t0 = clock64();
+  int nsweeps = 0;
+#endif
   for (int sweep = 0; sweep < 40; ++sweep) {
-    if (tid == 0) offmax = 0u;
-    __syncthreads();
+#ifdef TPROD_SVT_DEBUG
+    nsweeps = sweep + 1;
+#endif
+    // rotated[(sweep+1)%3] was last read at the end of sweep - 2 and is next written in sweep + 1:
+    // both separated from this store by barriers
+    if (tid == 0) rotated[(sweep + 1) % 3] = 0;
     for (int r = 0; r < np - 1; ++r) {
-      for (int k = warp; k < np / 2; k += nw) {
+      // warp-uniform trip count (the group sums shuffle across the whole warp)
+      for (int kb = warp * GPW; kb < np / 2; kb += nw * GPW) {
         // circle method: player np-1 fixed, pairs (r+k, r-k) mod (np-1)
-        const int p = k == 0 ? r : (r + k) % (np - 1);
-        const int q = k == 0 ? np - 1 : (r - k + np - 1) % (np - 1);
-        if (p >= n || q >= n) continue;
-        double2* ap = a + p * m;
-        double2* aq = a + q * m;
+        const int k = kb + gw;
+        int p = r + k, q = r - k + np - 1;              // (r + k) mod (np - 1), (r - k) mod (np - 1): one wrap each
+        if (p >= np - 1) p -= np - 1;
+        if (q >= np - 1) q -= np - 1;
+        if (k == 0) q = np - 1;
+        const bool valid = k < np / 2 && p < n && q < n;
+        double2* ap = a + (valid ? p : 0) * m;
+        double2* aq = a + (valid ? q : 0) * m;
+        double2* vp = v + (valid ? p : 0) * n;
+        double2* vq = v + (valid ? q : 0) * n;
+        // this group owns columns p, q for the round: they are read once (predicated, so the loads
+        // batch), kept in registers through the reductions and the angle, and written back rotated;
+        // V's columns are fetched at the same time so their latency hides behind the reductions
+        const double2 z = make_double2(0.0, 0.0);
+        double2 xs[L], ys[L], vx[L], vy[L];
+#pragma unroll
+        for (int it = 0; it < L; ++it) {
+          const int i = gl + it * G;
+          xs[it] = valid && i < m ? ap[i] : z;
+          ys[it] = valid && i < m ? aq[i] : z;
+          vx[it] = want_v && valid && i < n ? vp[i] : z;
+          vy[it] = want_v && valid && i < n ? vq[i] : z;
+        }
         double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-        for (int i = lane; i < m; i += 32) {
-          const double2 x = ap[i], y = aq[i];
+#pragma unroll
+        for (int it = 0; it < L; ++it) {
+          const double2 x = xs[it], y = ys[it];
           al += x.x * x.x + x.y * x.y;
           be += y.x * y.x + y.y * y.y;
           gr += x.x * y.x + x.y * y.y;                  // conj(x) * y
           gi += x.x * y.y - x.y * y.x;
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        gr = warp_sum(gr);
-        gi = warp_sum(gi);
+        al = group_sum<G>(al);
+        be = group_sum<G>(be);
+        gr = group_sum<G>(gr);
+        gi = group_sum<G>(gi);
         const double g2 = gr * gr + gi * gi;
-        if (!(g2 > 1e-20 * al * be) || !(g2 > 0.0)) continue;   // already orthogonal (or a zero column)
+        if (!valid || !(g2 > 1e-20 * al * be) || !(g2 > 0.0)) continue;   // already orthogonal (or a zero column)
+        if (gl == 0) rotated[sweep % 3] = 1;
         // fp64 divisions / square roots are slow: the angle comes from fp32 estimates (an approximate
         // Jacobi angle still converges), and the quantities that must be exact to fp64 -- the unit
         // phase e and the rotation's c^2 + s^2 = 1 -- get one Newton step of rsqrt in fp64
         float ig32 = rsqrtf((float)g2);
         const double ig = (double)ig32 * (1.5 - 0.5 * g2 * (double)ig32 * (double)ig32);   // 1 / |g|
-        if (lane == 0) atomicMax(&offmax, __float_as_uint((float)(g2 / (al * be))));
         const float zeta = (float)((be - al) * 0.5 * ig);
         const float t32 = copysignf(1.f, zeta) / (fabsf(zeta) + sqrtf(1.f + zeta * zeta));
         const double t = t32, t2p1 = 1.0 + t * t;
         const float c32 = rsqrtf((float)t2p1);
         const double c = (double)c32 * (1.5 - 0.5 * t2p1 * (double)c32 * (double)c32), s = c * t;
         const double er = gr * ig, ei = -gi * ig;         // e = conj(g) / |g|
-        for (int i = lane; i < m; i += 32) {
-          const double2 x = ap[i], y0 = aq[i];
+#pragma unroll
+        for (int it = 0; it < L; ++it) {
+          const int i = gl + it * G;
+          const double2 x = xs[it], y0 = ys[it];
           const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
-          ap[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
-          aq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+          if (i < m) {
+            ap[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+            aq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+          }
         }
-        double2* vp = v + p * n;
-        double2* vq = v + q * n;
-        for (int i = lane; i < n; i += 32) {
-          const double2 x = vp[i], y0 = vq[i];
-          const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
-          vp[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
-          vq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+        if (want_v) {
+#pragma unroll
+          for (int it = 0; it < L; ++it) {
+            const int i = gl + it * G;
+            const double2 x = vx[it], y0 = vy[it];
+            const double2 y = make_double2(y0.x * er - y0.y * ei, y0.x * ei + y0.y * er);
+            if (i < n) {
+              vp[i] = make_double2(c * x.x - s * y.x, c * x.y - s * y.y);
+              vq[i] = make_double2(s * x.x + c * y.x, s * x.y + c * y.y);
+            }
+          }
         }
       }
       __syncthreads();
     }
-    if (__uint_as_float(offmax) < 1e-20f) break;        // (|g|^2 / alpha beta) uniform: shared value after a barrier
+    if (!rotated[sweep % 3]) break;                     // no pair above the tolerance: read after a barrier
   }
+#ifdef TPROD_SVT_DEBUG
+  if (tid == 0 && f < 2) printf("svt f=%d m=%d n=%d G=%d sweeps=%d cycles=%lld\n", f, m, n, G, nsweeps, clock64() - t0);
+#endif
   // sigma_j = ||(A V)_j||, weights (1 - tau / sigma_j)_+
   for (int j = warp; j < n; j += nw) {
     double ss = 0.0;
@@ -372,18 +423,35 @@ __global__ void __launch_bounds__(1024) slice_svt_kernel(const float* __restrict
 
 bool svt_supported(int64_t m, int64_t n) { return m >= 1 && n >= 1 && m <= SVT_MAX && n <= SVT_MAX; }
 
+// One CTA per slice.  G lanes per column pair: a pair's reductions and angle are warp-instruction
+// overhead shared by the 32/G pairs of a warp, so narrow groups cut the instruction count (the
+// iteration is issue-bound on one SM); columns are max(m, n) <= 64 long.  The pairs of a round
+// (ceil(min(m, n) / 2)) fill ceil(pairs * G / 32) warps.
+static int launch_svt_common(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n,
+                             int64_t h, int64_t fstride, float tau, double* sv, SvdOut fo, cudaStream_t s) {
+  if (!svt_supported(m, n)) return 6;
+  // the slice (m n) and, unless only singular values are wanted, V (r x r, r = min(m, n))
+  const int64_t len = std::max(m, n), r = std::min(m, n), pairs = (r + 1) / 2;
+  const size_t smem = sizeof(double2) * (size_t)(n * m + (sv ? 0 : r * r));
+  int G = len > 32 ? 16 : 8;
+  if (const char* e = getenv("TPROD_SVT_GROUP")) {     // tuning override (G = 8 needs columns <= 32)
+    const int g = atoi(e);
+    if ((g == 8 && len <= 32) || g == 16 || g == 32) G = g;
+  }
+  int threads = (int)(((pairs * G + 31) / 32) * 32);
+  if (threads < 64) threads = 64;
+  auto go = [&](auto kern) -> int {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 4;
+    kern<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, sv, fo);
+    return cudaGetLastError() == cudaSuccess ? 0 : 4;
+  };
+  return G == 8 ? go(slice_svt_kernel<8>) : G == 16 ? go(slice_svt_kernel<16>) : go(slice_svt_kernel<32>);
+}
+
 int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
                      int64_t fstride, float tau, cudaStream_t s) {
-  if (!svt_supported(m, n)) return 6;
-  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
-  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 4;
-  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
-  if (threads < 64) threads = 64;
-  if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, nullptr,
-                                                      SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr});
-  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+  return launch_svt_common(re, im, wre, wim, m, n, h, fstride, tau, nullptr,
+                           SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, s);
 }
 
 // t-SVD scalars (NEXT-3).  sv: [h][r] per-slice singular values (r = min(m, n), non-increasing).
@@ -420,29 +488,14 @@ __global__ void tsvd_reduce_kernel(const double* __restrict__ sv, int r, int h, 
 
 int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
                              float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s) {
-  if (!svt_supported(m, n)) return 6;
-  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
-  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 4;
-  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
-  if (threads < 64) threads = 64;
-  if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, nullptr,
-                                                      SvdOut{ure, uim, sre, vre, vim});
-  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+  return launch_svt_common(re, im, nullptr, nullptr, m, n, h, fstride, 0.f, nullptr, SvdOut{ure, uim, sre, vre, vim}, s);
 }
 
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
                        double* sv, float rtol, float* out, cudaStream_t s) {
-  if (!svt_supported(m, n)) return 6;
-  const size_t smem = sizeof(double2) * (size_t)(n * m + n * n);
-  if (cudaFuncSetAttribute(slice_svt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return 4;
-  int threads = 32 * (int)((std::min(m, n) + 1) / 2);
-  if (threads < 64) threads = 64;
-  if (threads > 1024) threads = 1024;
-  slice_svt_kernel<<<(unsigned)h, threads, smem, s>>>(re, im, nullptr, nullptr, (int)m, (int)n, fstride, 0.f, sv,
-                                                      SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr});
+  const int rc = launch_svt_common(re, im, nullptr, nullptr, m, n, h, fstride, 0.f, sv,
+                                   SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, s);
+  if (rc) return rc;
   tsvd_reduce_kernel<<<1, 64, 0, s>>>(sv, (int)std::min(m, n), (int)h, (int)n3, rtol, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
