@@ -239,7 +239,7 @@ def test_fourstep_full_path(T, dims):
 
 
 # ------------------------------------------------------------------------------- NEXT-4
-@pytest.mark.parametrize("dims", [(33, 17, 5), (7, 64, 1), (64, 3, 2), (40, 40, 31)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("dims", [(33, 17, 5), (7, 64, 1), (64, 3, 2), (40, 40, 31), (132, 68, 3), (4, 4, 2), (256, 128, 4)], ids=lambda d: "x".join(map(str, d)))
 def test_tran_teye_gpu_exact(T, dims):
     """tran (Def. 2.2) and teye (Def. 2.3) on the GPU equal the oracle exactly (pure data movement)."""
     import torch
