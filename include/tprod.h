@@ -188,7 +188,14 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
-       TPROD_OPT_TRANSFORM = 5 };
+       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6 };
+/* TPROD_OPT_GRAPHS (tprod_f32 / tprod_f64 / tprod_f32_prepared): 1 (default) = the second and later
+ * calls with the same operand pointers, shapes and options replay the call's launch sequence as
+ * one CUDA graph (captured on a private stream at the second call, launched on the caller's
+ * stream); 0 = always launch kernel by kernel.  Identical kernels and results either way; the
+ * graph only removes per-kernel host work and launch gaps.  Bypassed while TPROD_OPT_TIMING is on
+ * (stage events between direct launches) and when the caller's stream is being captured.  The handle keeps at most 64 graphs (all are
+ * dropped, after a device synchronisation, when a 65th key arrives or the workspace grows). */
 /* TPROD_OPT_TRANSFORM (fp32 path): 0 = auto (TMA-staged / tube-parallel transform kernels where
  * they apply), 1 = register-resident transform kernels only.  Same arithmetic up to rounding
  * order of the DFT sums (both within the stage tolerances). */

@@ -29,8 +29,16 @@ def h_slices(n3: int) -> int:
 
 
 def is_matlab_layout(t) -> bool:
-    """True if element (i,j,k) of the 3-D tensor t is at i + n1*j + n1*n2*k (contiguous)."""
-    return t.dim() == 3 and t.permute(2, 1, 0).is_contiguous()
+    """True if element (i,j,k) of the 3-D tensor t is at i + n1*j + n1*n2*k (contiguous).
+    Stride test (what permute(2, 1, 0).is_contiguous() decides, without building a view: this
+    runs on every call)."""
+    if t.dim() != 3:
+        return False
+    n1, n2, n3 = t.shape
+    if n1 == 0 or n2 == 0 or n3 == 0:
+        return True
+    s0, s1, s2 = t.stride()
+    return (n1 == 1 or s0 == 1) and (n2 == 1 or s1 == n1) and (n3 == 1 or s2 == n1 * n2)
 
 
 def matlab_empty(n1: int, n2: int, n3: int, dtype=None, device="cuda"):

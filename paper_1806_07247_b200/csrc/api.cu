@@ -58,6 +58,16 @@ struct tprod_ctx {
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   PreparedA prep_host;
+  // CUDA-graph cache of the launch sequence (TPROD_OPT_GRAPHS): key = everything the kernels'
+  // parameters derive from (operand / workspace / table pointers, shapes, options)
+  bool graphs = true;
+  cudaStream_t cap = nullptr;                          // private capture stream
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int seen = 0;                                      // direct runs before capture (< 0: capture failed, never retry)
+    int64_t launches = 0;
+  };
+  std::map<std::vector<int64_t>, GraphEntry> graph_cache;
 };
 
 namespace {
@@ -141,10 +151,13 @@ Layout64 layout64(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
   return L;
 }
 
+void clear_graphs(tprod_ctx* h);
+
 int ensure_ws(tprod_ctx* h, size_t bytes) {
   if (h->ws_bytes >= bytes) return TPROD_OK;
   if (h->ws) {
     CK(cudaDeviceSynchronize());
+    clear_graphs(h);                                   // their kernels address the old workspace
     cudaFree(h->ws);
     h->ws = nullptr;
     h->ws_bytes = 0;
@@ -303,8 +316,70 @@ int prepare_into(tprod_ctx* h, PreparedA& P, const float* A, int64_t n1, int64_t
   return TPROD_OK;
 }
 
+// ---------------------------------------------------------------- CUDA-graph replay
+constexpr size_t GRAPH_CACHE_MAX = 64;
+
+void clear_graphs(tprod_ctx* h) {
+  for (auto& kv : h->graph_cache)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  h->graph_cache.clear();
+}
+
+// Runs `body(stream)` -- the whole launch sequence of one call, host-side setup (workspace, tables)
+// already done -- directly the first time a key is seen and, from the second time on, as one
+// cudaGraphLaunch of its captured graph: the per-kernel host work (argument and tensor-map
+// encoding, launch calls) of a call with a repeated key is paid once, and the kernels start
+// back to back on the device.  A key fixes every kernel parameter, so replay is exactly the direct
+// launch sequence on the current contents of the buffers.  Not used while TPROD_OPT_TIMING is on
+// (the stage events are recorded between direct launches) or when the caller's stream is itself
+// being captured (the launches then join the caller's graph).
+template <class Body>
+int graph_run(tprod_ctx* h, std::vector<int64_t>&& key, cudaStream_t s, Body&& body) {
+  if (!h->graphs || h->timing) return body(s);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return body(s);
+  auto it = h->graph_cache.find(key);
+  if (it == h->graph_cache.end()) {
+    if (h->graph_cache.size() >= GRAPH_CACHE_MAX) {   // rare: drop the lot (an exec may be in flight)
+      CK(cudaDeviceSynchronize());
+      clear_graphs(h);
+    }
+    it = h->graph_cache.emplace(std::move(key), tprod_ctx::GraphEntry{}).first;
+  }
+  tprod_ctx::GraphEntry& e = it->second;
+  if (!e.exec) {
+    if (e.seen < 1) {                                  // first sighting (or capture failed before): direct
+      if (e.seen >= 0) ++e.seen;
+      return body(s);
+    }
+    if (!h->cap) CK(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    CK(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeRelaxed));
+    const int st = body(h->cap);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(h->cap, &g);
+    cudaError_t ie = cudaErrorUnknown;
+    if (!st && ce == cudaSuccess && g) ie = cudaGraphInstantiate(&e.exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {                           // not capturable: stay on direct launches
+      cudaGetLastError();
+      e.exec = nullptr;
+      e.seen = -1;
+      return body(s);
+    }
+    e.launches = h->last_launches;
+  }
+  CK(cudaGraphLaunch(e.exec, s));
+  h->last_launches = e.launches;
+  h->timed_last = false;
+  return TPROD_OK;
+}
+
 // ---------------------------------------------------------------- the hot path
 // pa != nullptr: A is the handle's prepared operand (A itself is not read; K0/K1 run for B only)
+int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
+               int64_t n4, cudaStream_t s, const PreparedA* pa, const Layout32& L, Twiddles32 T);
+
 int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2,
             int64_t n3, int64_t n4, cudaStream_t s, const PreparedA* pa = nullptr) {
   Layout32 L = layout32(n1, n2, n3, n4, pa == nullptr);
@@ -312,6 +387,17 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   if (st) return st;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
+  std::vector<int64_t> key = {1, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
+                              (int64_t)(uintptr_t)h->ws, pa ? (int64_t)(uintptr_t)pa->Ab : 0,
+                              pa ? (int64_t)(uintptr_t)pa->uA : 0, pa ? pa->lda : 0, h->engine, h->force_bn,
+                              h->force_cn, h->transform};
+  return graph_run(h, std::move(key), s,
+                   [&](cudaStream_t ls) { return launch_f32(h, A, B, C, n1, n2, n3, n4, ls, pa, L, T); });
+}
+
+int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
+               int64_t n4, cudaStream_t s, const PreparedA* pa, const Layout32& L, Twiddles32 T) {
+  int st = 0;
   T.staged = h->transform == 0;
   char* ws = (char*)h->ws;
   T.scratch = L.W_bytes ? (float*)(ws + L.off_W) : nullptr;
@@ -370,12 +456,16 @@ int run_f64(tprod_ctx* h, const double* A, const double* B, double* C, int64_t n
   double* Bb = (double*)(ws + L.off_Bb);
   double* Cb = (double*)(ws + L.off_Cb);
   Twiddles64 T{tw, (int)n3};
-  launch_fwd_f64(A, n1, n2, n3, T, Ab, n1, s);
-  launch_fwd_f64(B, n2, n4, n3, T, Bb, n2, s);
-  launch_gemm_simt_f64(Ab, n1, Bb, n2, Cb, n1, n1, n2, n4, L.h, s);
-  launch_inv_f64(Cb, n1, n1, n4, n3, T, C, s);
-  h->last_launches = 4;
-  return launch_status();
+  std::vector<int64_t> key = {2, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
+                              (int64_t)(uintptr_t)h->ws};
+  return graph_run(h, std::move(key), s, [&](cudaStream_t ls) {
+    launch_fwd_f64(A, n1, n2, n3, T, Ab, n1, ls);
+    launch_fwd_f64(B, n2, n4, n3, T, Bb, n2, ls);
+    launch_gemm_simt_f64(Ab, n1, Bb, n2, Cb, n1, n1, n2, n4, L.h, ls);
+    launch_inv_f64(Cb, n1, n1, n4, n3, T, C, ls);
+    h->last_launches = 4;
+    return launch_status();
+  });
 }
 
 template <typename T>
@@ -575,6 +665,8 @@ int tprod_destroy(tprod_handle h) {
   }
   if (h->cs_in) cudaStreamDestroy(h->cs_in);
   if (h->cs_out) cudaStreamDestroy(h->cs_out);
+  clear_graphs(h);
+  if (h->cap) cudaStreamDestroy(h->cap);
   if (h->ws) cudaFree(h->ws);
   delete h;
   return TPROD_OK;
@@ -918,6 +1010,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
     case TPROD_OPT_GEMM_BN:
       if (value != 0 && value != 64 && value != 128) return TPROD_EINVAL;
       h->force_bn = (int)value;
+      return TPROD_OK;
+    case TPROD_OPT_GRAPHS:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->graphs = value != 0;
       return TPROD_OK;
     default:
       return TPROD_EINVAL;

@@ -414,6 +414,100 @@ def test_determinism_and_w_invariance(T):
             assert np.array_equal(Cr, C1[:, s:e, :]), (W, r)
 
 
+def test_graph_replay_matches_direct(T):
+    """TPROD_OPT_GRAPHS: from the second call with the same pointers / shapes / options the launch
+    sequence replays as one CUDA graph.  Replays equal kernel-by-kernel launches bitwise, read the
+    buffers' current contents (new data in the same tensors), keep the launch count, survive a
+    workspace reallocation, cover the prepared-operand and fp64 paths, and still match the oracle."""
+    import torch
+    hg, hd = T.Handle(), T.Handle()
+    hd.set_option(T._lib.TPROD_OPT_GRAPHS, 0)
+    for dims in ((96, 80, 31, 72), (33, 17, 64, 40), (24, 16, 8192, 8)):
+        n1, n2, n3, n4 = dims
+        A = normal((n1, n2, n3), 31 + n3)
+        B = normal((n2, n4, n3), 32 + n3)
+        dA, dB = dev(A), dev(B)
+        Cg = T.matlab_empty(n1, n4, n3, torch.float32, "cuda")
+        Cd = T.matlab_empty(n1, n4, n3, torch.float32, "cuda")
+        T.tprod(dA, dB, out=Cd, handle=hd)
+        ref = host(Cd)
+        if n3 <= 64:                                    # (the long-tube oracle check: test_fourstep_full_path)
+            assert O.rel_err(ref, O.tprod_alg1(A.astype(np.float64), B.astype(np.float64))) <= TOL32
+        counts = []
+        for _ in range(3):                              # direct, capture + replay, replay
+            Cg.zero_()
+            T.tprod(dA, dB, out=Cg, handle=hg)
+            assert np.array_equal(host(Cg), ref), dims
+            counts.append(hg.last_launch_count())
+        assert counts[0] == counts[1] == counts[2] == hd.last_launch_count()
+        # new contents, same tensors: the replay reads them
+        A2 = normal((n1, n2, n3), 41 + n3)
+        dA.copy_(dev(A2))
+        T.tprod(dA, dB, out=Cg, handle=hg)
+        T.tprod(dA, dB, out=Cd, handle=hd)
+        assert np.array_equal(host(Cg), host(Cd)), dims
+    # workspace growth drops the cached graphs; the small shape captured before still runs right
+    A = normal((40, 24, 7), 51)
+    B = normal((24, 16, 7), 52)
+    dA, dB = dev(A), dev(B)
+    Cg = T.matlab_empty(40, 16, 7, torch.float32, "cuda")
+    for _ in range(2):
+        T.tprod(dA, dB, out=Cg, handle=hg)
+    big_A, big_B = dev(normal((512, 512, 17), 53)), dev(normal((512, 512, 17), 54))
+    T.tprod(big_A, big_B, handle=hg)
+    for _ in range(3):
+        T.tprod(dA, dB, out=Cg, handle=hg)
+        assert np.array_equal(host(Cg), host(T.tprod(dA, dB, handle=hd)))
+    # prepared operand
+    A = normal((128, 96, 31), 55)
+    dA = dev(A)
+    hg.prepare_a(dA)
+    hd.prepare_a(dA)
+    dB = dev(normal((96, 40, 31), 56))
+    Cg = T.matlab_empty(128, 40, 31, torch.float32, "cuda")
+    for _ in range(3):
+        T.tprod_prepared(dB, out=Cg, handle=hg)
+        assert np.array_equal(host(Cg), host(T.tprod_prepared(dB, handle=hd)))
+    # stage timing (TPROD_OPT_TIMING) bypasses the graphs: stage events between direct launches
+    hg.set_option(T._lib.TPROD_OPT_TIMING, 1)
+    dA, dB = dev(normal((96, 80, 31), 59)), dev(normal((80, 72, 31), 60))
+    Cg = T.matlab_empty(96, 72, 31, torch.float32, "cuda")
+    for _ in range(3):
+        T.tprod(dA, dB, out=Cg, handle=hg)
+        ms = hg.last_stage_ms()
+        assert len(ms) == 4 and all(x > 0 for x in ms), ms
+        assert np.array_equal(host(Cg), host(T.tprod(dA, dB, handle=hd)))
+    hg.set_option(T._lib.TPROD_OPT_TIMING, 0)
+    # fp64
+    A64, B64 = normal((20, 12, 9), 57, np.float64), normal((12, 8, 9), 58, np.float64)
+    dA64, dB64 = dev(A64), dev(B64)
+    C64 = T.matlab_empty(20, 8, 9, torch.float64, "cuda")
+    for _ in range(3):
+        T.tprod(dA64, dB64, out=C64, handle=hg)
+        assert O.rel_err(host(C64), O.tprod_bcirc(A64, B64)) <= TOL64
+
+
+def test_inside_caller_graph_capture(T):
+    """A call made while the caller captures its stream joins the caller's graph (no nested
+    capture); replaying that graph recomputes the product from the buffers' current contents."""
+    import torch
+    A, B = normal((64, 48, 16), 61), normal((48, 32, 16), 62)
+    dA, dB = dev(A), dev(B)
+    h = T.Handle()
+    C = T.tprod(dA, dB, handle=h)                       # warm-up: workspace and tables exist
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            T.tprod(dA, dB, out=C, handle=h)
+    A2 = normal((64, 48, 16), 63)
+    dA.copy_(dev(A2))
+    C.zero_()
+    g.replay()
+    assert O.rel_err(host(C), O.tprod_alg1(A2.astype(np.float64), B.astype(np.float64))) <= TOL32
+
+
 def test_nccl_world_of_one(T):
     """The multi-GPU plumbing through the C ABI on one GPU: NCCL unique id, communicator init
     (world size 1) and the in-place broadcast used to replicate A; then a t-product on the
