@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -505,11 +506,12 @@ int host_call_f32_pipelined(const float* A, const float* B, float* C, int64_t n1
   float* dB[2] = {(float*)h->hbuf[1], (float*)((char*)h->hbuf[1] + bBc)};
   float* dC[2] = {(float*)h->hbuf[2], (float*)((char*)h->hbuf[2] + bCc)};
   CK(cudaMemcpyAsync(dA, A, bA, cudaMemcpyHostToDevice, s));
-  if ((st = prepare_into(h, h->prep_host, dA, n1, n2, n3, s))) return st;
-  // the copy streams start after everything already on s (A's copy / preparation, earlier calls)
+  // the copy streams start after everything already on s up to A's copy (earlier work, earlier
+  // calls), so B's first chunk streams in while A is prepared
   CK(cudaEventRecord(h->ev_comp[0], s));
   CK(cudaStreamWaitEvent(h->cs_in, h->ev_comp[0], 0));
   CK(cudaStreamWaitEvent(h->cs_out, h->ev_comp[0], 0));
+  if ((st = prepare_into(h, h->prep_host, dA, n1, n2, n3, s))) return st;
   const int64_t nch = (n4 + w - 1) / w;
   for (int64_t i = 0; i < nch; ++i) {
     const int b = (int)(i & 1);
@@ -541,9 +543,13 @@ int host_call(const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3, 
   if (st) return st;
   CK(cudaSetDevice(h->device));
   if (sizeof(T) == 4) {
-    // pipeline when B is large enough to amortise chunking: ~8 chunks of >= 4 MB of B
+    // pipeline when B is large enough to amortise chunking: 8 to 32 chunks of ~256 MB of B (the
+    // tail -- the last chunk's compute and copy-out -- shrinks with the chunk; measured on config 5:
+    // 8 chunks 295 ms, 16 279 ms, 32 275 ms against 246 ms of host-to-device copy)
     const double bB = 4.0 * n2 * n4 * n3;
-    int64_t w = (n4 + 7) / 8;
+    int64_t chunks = std::min<int64_t>(32, std::max<int64_t>(8, (int64_t)(bB / 256e6 + 0.5)));
+    if (const char* e = getenv("TPROD_HOST_CHUNKS")) chunks = std::max(2, atoi(e));   // tuning override
+    int64_t w = (n4 + chunks - 1) / chunks;
     if (bB >= 32e6 && n4 >= 4)
       return host_call_f32_pipelined((const float*)A, (const float*)B, (float*)C, n1, n2, n3, n4,
                                      (cudaStream_t)stream, h, w);
