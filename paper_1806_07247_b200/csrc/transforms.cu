@@ -155,15 +155,17 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
           }
         }
       } else {
-        // short runs: lanes l4 < r4 of the warp, U runs in flight per batch
+        // short runs: the warp splits into G = 32 / r4 lane groups, each on its own run (j, k) of
+        // column j (r4 float4 lanes per run), U loads per lane in flight per batch
         constexpr int U = 8;
-        for (int64_t kb = k0; kb < n3; kb += U * wpc) {
+        const int G = 32 / (int)r4, g = lane / (int)r4, l4 = lane - g * (int)r4;
+        for (int64_t kb = k0; kb < n3; kb += (int64_t)U * G * wpc) {
           float4 v[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int64_t k = kb + u * wpc;
-            v[u] = (k < n3 && lane < r4) ? __ldg(reinterpret_cast<const float4*>(B + n2 * (j + n4 * k)) + lane)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int64_t k = kb + (int64_t)(u * G + g) * wpc;
+            v[u] = (g < G && k < n3) ? __ldg(reinterpret_cast<const float4*>(B + n2 * (j + n4 * k)) + l4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
           for (int u = 0; u < U; ++u)

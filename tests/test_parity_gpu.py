@@ -398,6 +398,37 @@ def test_identity_shift_transpose_fp32(T):
     assert O.rel_err(Ct, O.tran(C)) <= TOL32
 
 
+@pytest.mark.parametrize("dims", [(64, 64, 33, 48), (16, 8, 5, 12), (36, 100, 7, 20), (256, 160, 31, 40),
+                                  (4, 12, 16, 8), (33, 17, 9, 10)], ids=lambda d: "x".join(map(str, d)))
+def test_operand_scales_follow_rows_and_columns(T, dims):
+    """K0's exact power-of-two scales are per row of A and per column of B (the fp16 split keeps
+    fp32 accuracy only if every row / column is scaled by its own maximum): rows and columns
+    spread over 2^-24 .. 2^24 and one planted outlier per operand (10^4 x its row / column) must
+    come out finite and accurate row by row.  A scale that missed the outlier's run would overflow
+    the fp16 high part; a shared scale would flush the small rows."""
+    n1, n2, n3, n4 = dims
+    rng = np.random.default_rng(7 + n1 + n4)
+    A = normal((n1, n2, n3), 71 + n1).astype(np.float64)
+    B = normal((n2, n4, n3), 72 + n4).astype(np.float64)
+    A *= np.exp2(rng.integers(-24, 25, size=n1)).reshape(n1, 1, 1)
+    B *= np.exp2(rng.integers(-24, 25, size=n4)).reshape(1, n4, 1)
+    ia, ja, ka = rng.integers(n1), rng.integers(n2), rng.integers(n3)
+    A[ia, ja, ka] = 1e4 * np.abs(A[ia]).max()
+    ib, jb, kb = rng.integers(n2), rng.integers(n4), rng.integers(n3)
+    B[ib, jb, kb] = -1e4 * np.abs(B[:, jb]).max()
+    A, B = A.astype(np.float32), B.astype(np.float32)
+    C = gpu_tprod(T, A, B)
+    assert np.isfinite(C).all()
+    ref = O.tprod_alg1(A.astype(np.float64), B.astype(np.float64))
+    # C(i, j, :) scales with row i of A and column j of B: compare each (i, j) tube block relative
+    # to its own size
+    for i in range(n1):
+        for j in range(0, n4, max(1, n4 // 4)):
+            num = np.linalg.norm(C[i, j] - ref[i, j])
+            den = np.linalg.norm(np.abs(A[i]).max() * np.abs(B[:, j]).max()) * np.sqrt(n2 * n3)
+            assert num <= 1e-5 * den, (i, j, num / den)
+
+
 def test_determinism_and_w_invariance(T):
     """Bitwise-repeatable, and lateral-slice shards equal the matching columns of the full
     result bitwise (no split-K; K order independent of n4) -- the multi-GPU partition run
