@@ -189,6 +189,15 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
   const int64_t p0 = (blockIdx.x - q * pblocks) * TUB;
   const int64_t PQ = P * Q;
   const float* x = X + P * q + p0;
+  // A (ROLE 0): each tube's exact row scale is applied as it is loaded, before two tubes share one
+  // complex FFT (neither tube's rounding is then large relative to the other's scale); B's pair
+  // shares its column scale, applied after the FFT
+  __shared__ float rsc[256];                      // TUB = 2F <= 256 (F * N <= FFT_POINTS, N > 64)
+  if (ROLE == 0) {
+    for (int t = threadIdx.x; t < TUB; t += FFT_THREADS)
+      rsc[t] = p0 + t < P ? pow2f(scale_exp(__ldg(maxbits + p0 + t), N)) : 1.f;
+    __syncthreads();
+  }
   // ---- load: tube t = p0 + t, element k -> buffer t/2, real (t even) / imaginary (t odd) part
   if (vec) {   // TUB % 4 == 0, P % TUB == 0, 16-byte aligned
     const int V = TUB >> 2;                         // float4 per row
@@ -196,14 +205,21 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
 #pragma unroll 8
     for (int idx = threadIdx.x; idx < total; idx += FFT_THREADS) {
       const int vv = idx % V, k = idx / V;
-      const float4 a = __ldg(reinterpret_cast<const float4*>(x + PQ * k) + vv);
+      float4 a = __ldg(reinterpret_cast<const float4*>(x + PQ * k) + vv);
+      if (ROLE == 0) {
+        a.x *= rsc[4 * vv];
+        a.y *= rsc[4 * vv + 1];
+        a.z *= rsc[4 * vv + 2];
+        a.w *= rsc[4 * vv + 3];
+      }
       z[(2 * vv) * Np + pad(k)] = make_float2(a.x, a.y);
       z[(2 * vv + 1) * Np + pad(k)] = make_float2(a.z, a.w);
     }
   } else {
     for (int idx = threadIdx.x; idx < TUB * N; idx += FFT_THREADS) {
       const int t = idx % TUB, k = idx / TUB;
-      const float v = (p0 + t < P) ? __ldg(x + PQ * k + t) : 0.f;
+      float v = (p0 + t < P) ? __ldg(x + PQ * k + t) : 0.f;
+      if (ROLE == 0) v *= rsc[t];
       reinterpret_cast<float*>(z + (t >> 1) * Np + pad(k))[t & 1] = v;
     }
   }
@@ -230,7 +246,7 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
       if (p0 == 0 && c == 0) unscale[q] = pow2f(-e0);
     }
   }
-  const float s0 = pow2f(e0), s1 = pow2f(e1);
+  const float s0 = ROLE == 0 ? 1.f : pow2f(e0), s1 = ROLE == 0 ? 1.f : pow2f(e1);   // A: applied at load
   if (p >= P) return;
   for (int idx = threadIdx.x; idx < H * F; idx += FFT_THREADS) {
     const int f = idx / F;

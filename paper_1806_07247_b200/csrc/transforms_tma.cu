@@ -313,11 +313,15 @@ __host__ __device__ constexpr int tube_toff(int log, int i) {
   return i <= 1 ? 0 : tube_toff(log, i - 1) + (tube_R(log, i - 1) - 1) * tube_Ns(i - 1);
 }
 
-template <int N, int F, int R, int Ns, int DIR, int NT = TUBE_NT>
-__device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp) {
+// PRE: multiply the loaded values by `pre` (the thread's column c = threadIdx.x % F is the same for
+// all its butterflies since NT % F == 0): per-tube exact scales applied before two real tubes share
+// one complex FFT, so neither tube's rounding error is large relative to the other's scale.
+template <int N, int F, int R, int Ns, int DIR, int NT = TUBE_NT, bool PRE = false>
+__device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp, float2 pre = make_float2(1.f, 1.f)) {
   constexpr int NB = N / R;
   constexpr int BPT = F * NB / NT;
   static_assert(F * NB % NT == 0, "butterflies must divide evenly");
+  static_assert(!PRE || NT % F == 0, "pre-scale needs a fixed column per thread");
   float2 v[BPT][R];
 #pragma unroll
   for (int u = 0; u < BPT; ++u) {
@@ -325,6 +329,10 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
     const int c = b % F, j = b / F, k = j % Ns;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[u][r] = z[(j + r * NB) * F + c];
+    if (PRE) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[u][r] = make_float2(v[u][r].x * pre.x, v[u][r].y * pre.y);
+    }
     if (Ns > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twN<DIR>(tp, (r - 1) * Ns + k));
@@ -342,10 +350,10 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
   __syncthreads();
 }
 
-template <int N, int DIR, int F = TubeCfg<N>::F, int NT = TUBE_NT>
-__device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st) {
+template <int N, int DIR, int F = TubeCfg<N>::F, int NT = TUBE_NT, bool PRE = false>
+__device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st, float2 pre = make_float2(1.f, 1.f)) {
   using C = TubeCfg<N>;
-  tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT>(z, st);
+  tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT, PRE>(z, st, pre);
   if constexpr (C::NP > 1) tube_pass<N, F, tube_R(C::LOG, 1), tube_Ns(1), DIR, NT>(z, st + tube_toff(C::LOG, 1));
 }
 
@@ -366,7 +374,6 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
   const int c = threadIdx.x % F;                    // TUBE_NT % F == 0: fixed tube pair per thread
   tma_pipeline<BUF, TUB>(&mX, P, Q, smem, full, [&](const Item& cur, float* s) {
     float2* z = reinterpret_cast<float2*>(s);       // z[k][c] = (x_{2c}[k], x_{2c+1}[k])
-    tube_fft<N, -1>(z, st);
     const int64_t q = cur.q, p = cur.p0 + 2 * c;
     const bool in0 = p < P, in1 = p + 1 < P;
     int e0 = 0, e1 = 0;
@@ -381,7 +388,13 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
       e0 = e1 = scale_exp(__ldg(maxbits + q), N);
       if (cur.p0 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
     }
-    const float s0 = pow2f(e0), s1 = pow2f(e1);
+    // A's two tubes of a pair have their own row scales: applied before the shared FFT (exact
+    // powers of two); B's pair shares its column scale, applied after
+    const float s0 = ROLE == 0 ? 1.f : pow2f(e0), s1 = ROLE == 0 ? 1.f : pow2f(e1);
+    if (ROLE == 0)
+      tube_fft<N, -1, F, TUBE_NT, true>(z, st, make_float2(pow2f(e0), pow2f(e1)));
+    else
+      tube_fft<N, -1>(z, st);
     if (threadIdx.x == 0) bulk_wait_read();         // the previous item's stores have read stg
     __syncthreads();
 #pragma unroll 4
@@ -465,7 +478,8 @@ template <int N2, int TUB>
 __global__ void __launch_bounds__(2 * TUB) fwd4_pass1_kernel(const __grid_constant__ CUtensorMap mX4,
                                                             const __grid_constant__ CUtensorMap mW4, int64_t P,
                                                             int64_t Q, int N1, const float2* __restrict__ st2,
-                                                            const float2* __restrict__ twN) {
+                                                            const float2* __restrict__ twN,
+                                                            const unsigned* __restrict__ rowmax) {
   constexpr int F = TUB / 2, NT = 2 * TUB;
   extern __shared__ __align__(128) float smem[];
   __shared__ uint64_t full;
@@ -492,7 +506,16 @@ __global__ void __launch_bounds__(2 * TUB) fwd4_pass1_kernel(const __grid_consta
           : "memory");
     }
     bar_wait(&full, ph);
-    tube_fft<N2, -1, F, NT>(z, st2);                 // over k2 -> z[f2][c]
+    if (rowmax) {
+      // A (row scales): the pair's own exact scales before the shared FFT (pass 2 then skips them)
+      const int64_t p = p0 + 2 * (threadIdx.x % F);
+      const int N = N1 * N2;
+      const float s0 = p < P ? pow2f(scale_exp(__ldg(rowmax + p), N)) : 1.f;
+      const float s1 = p + 1 < P ? pow2f(scale_exp(__ldg(rowmax + p + 1), N)) : 1.f;
+      tube_fft<N2, -1, F, NT, true>(z, st2, make_float2(s0, s1));   // over k2 -> z[f2][c]
+    } else {
+      tube_fft<N2, -1, F, NT>(z, st2);
+    }
     for (int idx = threadIdx.x; idx < N2 * F; idx += NT) {
       const int f2 = idx / F;
       const float2 t = __ldg(twN + k1 * f2);          // w_N^{k1 f2} = (cos, -sin), k1 f2 < N
@@ -569,7 +592,7 @@ __global__ void __launch_bounds__(2 * TUB) fwd4_pass2_kernel(const __grid_consta
         e0 = e1 = scale_exp(__ldg(maxbits + q), N);
         if (p0 == 0 && f2 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
       }
-      const float s0 = pow2f(e0), s1 = pow2f(e1);
+      const float s0 = ROLE == 0 ? 1.f : pow2f(e0), s1 = ROLE == 0 ? 1.f : pow2f(e1);   // A: applied in pass 1
       __half* o = out + q * ld + p;
       for (int t = 0; t < (two ? 2 : 1); ++t) {
         const float2* zt = t == 0 ? za : zb;
@@ -958,7 +981,8 @@ bool launch_fwd4_t(const float* X, int64_t P, int64_t Q, int role, const unsigne
   const float2* st1 = tw.st_n1;
   const float2* st2 = tw.st_n2;
   const float2* twn = tw.tw;
-  void* a1[] = {(void*)&mx, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn};
+  const unsigned* rowmax = role == 0 ? maxbits : nullptr;   // A: row scales applied in pass 1
+  void* a1[] = {(void*)&mx, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn, (void*)&rowmax};
   if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
   void* a2[] = {(void*)&mw2, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&maxbits, (void*)&st1, (void*)&out, (void*)&ld,
                 (void*)&unscale};

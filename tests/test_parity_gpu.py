@@ -399,7 +399,10 @@ def test_identity_shift_transpose_fp32(T):
 
 
 @pytest.mark.parametrize("dims", [(64, 64, 33, 48), (16, 8, 5, 12), (36, 100, 7, 20), (256, 160, 31, 40),
-                                  (4, 12, 16, 8), (33, 17, 9, 10)], ids=lambda d: "x".join(map(str, d)))
+                                  (4, 12, 16, 8), (33, 17, 9, 10),
+                                  # pair-packed FFT paths: tube (64, 128, 256), mixed radix, four-step
+                                  (64, 64, 64, 48), (64, 32, 128, 16), (64, 64, 256, 16), (64, 16, 250, 8),
+                                  (32, 8, 4096, 4)], ids=lambda d: "x".join(map(str, d)))
 def test_operand_scales_follow_rows_and_columns(T, dims):
     """K0's exact power-of-two scales are per row of A and per column of B (the fp16 split keeps
     fp32 accuracy only if every row / column is scaled by its own maximum): rows and columns
@@ -419,14 +422,47 @@ def test_operand_scales_follow_rows_and_columns(T, dims):
     A, B = A.astype(np.float32), B.astype(np.float32)
     C = gpu_tprod(T, A, B)
     assert np.isfinite(C).all()
-    ref = O.tprod_alg1(A.astype(np.float64), B.astype(np.float64))
-    # C(i, j, :) scales with row i of A and column j of B: compare each (i, j) tube block relative
-    # to its own size
+    js = list(range(0, n4, max(1, n4 // 4)))
+    if n3 <= 256:
+        ref = O.tprod_alg1(A.astype(np.float64), B.astype(np.float64))
+    else:                                               # long tubes: the sampled columns only
+        ref = np.zeros((n1, n4, n3))
+        ref[:, js] = O.tprod_columns(A.astype(np.float64), B.astype(np.float64), js)
+    # C(i, j, :) scales with rows i of A and column j of B.  The inverse transforms share one
+    # complex FFT between output tubes i and i ^ 1 (R18), so tube (i, j) is accurate relative to the
+    # larger of the two rows' scales
+    ra = np.abs(A).max(axis=(1, 2))
     for i in range(n1):
-        for j in range(0, n4, max(1, n4 // 4)):
+        for j in js:
             num = np.linalg.norm(C[i, j] - ref[i, j])
-            den = np.linalg.norm(np.abs(A[i]).max() * np.abs(B[:, j]).max()) * np.sqrt(n2 * n3)
+            den = max(ra[i], ra[min(i ^ 1, n1 - 1)]) * np.abs(B[:, j]).max() * np.sqrt(n2 * n3)
             assert num <= 1e-5 * den, (i, j, num / den)
+
+
+@pytest.mark.parametrize("dims", [(40, 24, 31, 36), (64, 64, 64, 64), (20, 12, 2048, 8)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_zero_rows_columns_and_tensors(T, dims):
+    """Degenerate operands: a zero row of A and a zero lateral slice of B take the max = 0 scale
+    path (2^0, no division by zero); the zero lateral slice gives exactly zero columns of C, the
+    zero row gives a row of C at the rounding level of its FFT partner row 2 (R18: the inverse
+    shares one complex FFT between output tubes i and i ^ 1); an all-zero A gives an exactly zero C;
+    the rest matches the oracle."""
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 81 + n3)
+    B = normal((n2, n4, n3), 82 + n3)
+    A[3] = 0.0
+    B[:, 5] = 0.0
+    C = gpu_tprod(T, A, B)
+    assert np.all(C[:, 5] == 0.0)
+    assert np.abs(C[3]).max() <= 1e-5 * np.abs(C[2]).max()
+    ref = O.tprod_alg1(A.astype(np.float64), B.astype(np.float64)) if n3 <= 64 else None
+    if ref is not None:
+        assert O.rel_err(C, ref) <= TOL32
+    else:                                               # long tubes: sampled columns (Eq. (9))
+        cols = [0, n4 - 1]
+        assert O.rel_err(C[:, cols], O.tprod_columns(A, B, cols)) <= TOL32
+    Z = gpu_tprod(T, np.zeros_like(A), B)
+    assert np.all(Z == 0.0) and np.isfinite(Z).all()
 
 
 def test_determinism_and_w_invariance(T):
