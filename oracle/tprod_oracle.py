@@ -18,8 +18,10 @@ Conventions (DESIGN.md "Readings"):
 
 Pins: every function below is checked by ``tests/test_oracle.py`` against something other than
 itself (the paper's printed structural examples, SPEC's hand-derived worked examples in
-``tests/golden/``, closed forms, numpy.fft as a library special case, and brute-force loops).
-No function here is "parity unpinned".
+``tests/golden/``, closed forms, numpy.fft as a library special case, and brute-force loops),
+including the parity metric ``rel_err`` and ``inner`` (hand-evaluated values,
+``test_rel_err_hand_values`` / ``test_inner_hand_values``).  No function here is "parity
+unpinned".
 """
 from __future__ import annotations
 
@@ -332,9 +334,18 @@ def inner(A: np.ndarray, B: np.ndarray) -> complex:
 
 
 def rel_err(X: np.ndarray, Ref: np.ndarray) -> float:
-    """Parity metric (BASELINE.json north_star): ||X - Ref||_F / ||Ref||_F, evaluated in fp64."""
+    """Parity metric (BASELINE.json north_star): ||X - Ref||_F / ||Ref||_F, evaluated in fp64.
+
+    Both arguments must be real (the t-product of real tensors is real):
+    a complex argument raises TypeError instead of being cast silently, so a caller holding
+    ``tprod_alg1``'s complex result takes ``.real`` explicitly.  A zero reference returns the
+    absolute error ||X||_F."""
+    if np.iscomplexobj(X) or np.iscomplexobj(Ref):
+        raise TypeError("rel_err takes real arrays; take .real of a complex oracle result explicitly")
     X = np.asarray(X, dtype=np.float64)
     Ref = np.asarray(Ref, dtype=np.float64)
+    if X.shape != Ref.shape:
+        raise ValueError(f"rel_err: shape mismatch {X.shape} vs {Ref.shape}")
     den = float(np.linalg.norm(Ref.ravel()))
     num = float(np.linalg.norm((X - Ref).ravel()))
     return num / den if den > 0 else num

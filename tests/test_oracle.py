@@ -88,6 +88,40 @@ def test_teye_and_frobenius(golden):
     assert O.frobenius(tube(g["tube"])) == pytest.approx(g["norm"], abs=0)
 
 
+def test_rel_err_hand_values():
+    """The parity gate itself (BASELINE.json north_star: ||X - Ref||_F / ||Ref||_F), pinned to
+    values worked by hand: a mutation that returned 0, dropped the square root, used the max
+    norm, normalised by ||X|| or ignored trailing dimensions fails one of these."""
+    assert O.rel_err([4.0, 4.0], [3.0, 4.0]) == pytest.approx(0.2, abs=1e-15)          # |(1,0)| / 5
+    assert O.rel_err([4.0, 5.0], [3.0, 4.0]) == pytest.approx(np.sqrt(2.0) / 5.0, abs=1e-15)  # not max norm 1/4
+    assert O.rel_err([3.0, 4.0], [4.0, 5.0]) == pytest.approx(np.sqrt(2.0) / np.sqrt(41.0), abs=1e-15)
+    assert O.rel_err([3.0, 4.0], [3.0, 4.0]) == 0.0
+    assert O.rel_err([3.0, 4.0], [0.0, 0.0]) == pytest.approx(5.0, abs=0)                # zero reference: absolute
+    X = np.zeros((2, 2, 2))
+    R = np.ones((2, 2, 2))
+    X[1, 1, 1] = 1.0                                   # 7 entries off by 1 out of ||R|| = sqrt(8)
+    assert O.rel_err(X, R) == pytest.approx(np.sqrt(7.0 / 8.0), abs=1e-15)
+    with pytest.raises(TypeError):                     # complex results must be reduced explicitly
+        O.rel_err(np.array([1.0 + 1e-3j]), np.array([1.0]))
+    with pytest.raises(ValueError):
+        O.rel_err(np.zeros(3), np.zeros(4))
+
+
+def test_inner_hand_values():
+    """<A, B> = sum_k Tr(A^(k)* B^(k)), worked by hand on a complex tube pair
+    (checks the conjugate sits on the first argument) and on a 2 x 2 x 1 pair (checks the trace
+    pairs equal indices, not a transposed product)."""
+    A = np.array([1 + 2j, 3.0]).reshape(1, 1, 2)
+    B = np.array([2.0, 1 - 1j]).reshape(1, 1, 2)
+    # conj(1+2i)*2 + conj(3)*(1-i) = (2-4i) + (3-3i)
+    assert O.inner(A, B) == pytest.approx(5 - 7j, abs=1e-15)
+    assert O.inner(B, A) == pytest.approx(5 + 7j, abs=1e-15)
+    M = np.array([[1.0, 2.0], [3.0, 4.0]]).reshape(2, 2, 1)
+    N = np.array([[5.0, 6.0], [7.0, 8.0]]).reshape(2, 2, 1)
+    assert O.inner(M, N) == pytest.approx(1 * 5 + 2 * 6 + 3 * 7 + 4 * 8, abs=0)   # 70, not Tr(MN) = 69
+    assert O.inner(M, M) == pytest.approx(O.frobenius(M) ** 2, abs=1e-12)
+
+
 # ---------------------------------------------------------------- DFT machinery
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 10, 31, 32, 64])
 def test_dft_matrix_vs_library_and_eq1(n):
