@@ -14,8 +14,8 @@ that fits one GPU.  The global problem is fixed ("scaling": "strong"): with N ra
 per GPU) rank r owns the contiguous lateral-slice block r of B and C (synth.lateral_shard) and the
 same A, broadcast once from rank 0 with the library's NCCL broadcast (setup, untimed).  Lateral
 slices are independent (Eq. (9)), so the timed region has no collective.
-At N = 1 the line also carries config 3 (the north star's >= 60 %-of-roofline target config) in
-"c3", measured with the same protocol.
+At N = 1 the line also carries configs 3 (the north star's >= 60 %-of-roofline target config), 4
+and 2 as the extra keys "c3", "c4", "c2", measured with the same protocol.
 
 Metric flops (BASELINE.json / SURVEY.md 8(d)):  F = 8*n1*n2*n4*h + 2.5*n3*log2(n3)*(n1n2+n2n4+n1n4)
 with h = ceil((n3+1)/2).  value = F / (max over ranks of the mean device time per step).
@@ -215,16 +215,38 @@ def run_reference(args, wl, rank, world):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _allmax(dist, world, vals, dev):
+    """Max over ranks of a list of floats (the job's time is the slowest rank's).  NCCL reduces a
+    device tensor; gloo (the multi-rank test on one GPU) a host tensor."""
+    import torch
+    if world == 1:
+        return [float(v) for v in vals]
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def stage_bytes(n1, n2, n3, n4):
+    """Algorithmic bytes of the memory-bound stages: K0 reads A and B once (4 B per
+    element); K1 reads a tube (4 n3 B) and writes its Hermitian half as 4 fp16 planes (8 h B); K3
+    reads a C-bar tube (re, im fp32: 8 h B) and writes the real tube (4 n3 B)."""
+    h = h_slices(n3)
+    return {"K0": 4.0 * n3 * (n1 * n2 + n2 * n4),
+            "K1": (4.0 * n3 + 8.0 * h) * (n1 * n2 + n2 * n4),
+            "K3": (8.0 * h + 4.0 * n3) * (n1 * n4)}
+
+
 def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, stream, label):
     """Set up one workload (global n4 sharded over the ranks), time K steps on the device and
-    end to end; returns a dict of measurements (rank-0 values are the max over ranks)."""
+    end to end; returns a dict of measurements (timings are the max over ranks)."""
     import numpy as np
     from synth import lateral_shard, normal, normal_lateral
     n1, n2, n3, n4g = wl["n1"], wl["n2"], wl["n3"], wl["n4"]
     j0, j1 = lateral_shard(n4g, world, rank)
     n4 = j1 - j0
 
-    # ---- inputs: A on rank 0 then one NCCL broadcast (setup, untimed); B = this rank's shard
+    # ---- inputs: A on rank 0 then one broadcast (setup, untimed); B = this rank's shard
     A_host = torch.from_numpy(normal((n1, n2, n3), wl["seedA"])) if rank == 0 else None
     if world == 1:
         B_np = normal((n2, n4g, n3), wl["seedB"])
@@ -237,15 +259,21 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
     if rank == 0:
         A.copy_(A_host)
     if world > 1:
+        from paper_1806_07247_b200 import dist as tpdist
         torch.cuda.synchronize()
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        from paper_1806_07247_b200 import dist as tpdist
-        tpdist.replicate(A, root=0, handle=handle)        # one ncclBroadcast, setup only
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t_bcast = e0.elapsed_time(e1)
+        if dist.get_backend() == "nccl":                   # one ncclBroadcast through the C ABI
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            tpdist.replicate(A, root=0, handle=handle)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_bcast = e0.elapsed_time(e1)
+        else:                                              # gloo (tests): the host copy
+            Ah = A.cpu() if rank == 0 else tp.matlab_empty(n1, n2, n3, torch.float32, "cpu")
+            tpdist.replicate(Ah, root=0, handle=None)
+            A.copy_(Ah)
+            torch.cuda.synchronize()
         if rank != 0:
             A_host = A.cpu()
     C = tp.matlab_empty(n1, n4, n3, torch.float32, dev)
@@ -277,7 +305,7 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         for i in range(args.steps):
             l2_flush()
             ev[i][0].record(stream)
@@ -290,16 +318,16 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
         dist.barrier()
     handle.set_option(tp._lib.TPROD_OPT_TIMING, 0)
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    t = torch.tensor([statistics.mean(step_ms), statistics.mean(s[2] for s in stage_ms)],
-                     dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, gemm_ms = float(t[0]), float(t[1])
+    st_mean = [statistics.mean(s[i] for s in stage_ms) for i in range(4)]
+    ms, *st_max = _allmax(dist, world, [statistics.mean(step_ms)] + st_mean, dev)
+    gemm_ms = st_max[2]
     F = metric_flops(n1, n2, n3, n4g)
     out = {"label": label, "n1": n1, "n2": n2, "n3": n3, "n4": n4g, "n4_local": n4,
            "ms": ms, "ms_min": min(step_ms), "value": F / (ms * 1e-3) / 1e12,
            "gemm_ms": gemm_ms, "gemm_flops_local": gemm_flops(n1, n2, n3, n4),
-           "stage_ms": [round(statistics.mean(s[i] for s in stage_ms), 5) for i in range(4)],
+           "metric_flops_local": metric_flops(n1, n2, n3, n4),
+           "stage_ms": [round(x, 5) for x in st_max], "stage_bytes_local": stage_bytes(n1, n2, n3, n4),
+           "compulsory_bytes_local": 4.0 * n3 * (n1 * n2 + n2 * n4 + n1 * n4),
            "launches": launches, "clocks": clk.summary(), "bcast_ms": t_bcast}
 
     # ---- NEXT-1 prepared left operand: A's scales + forward DFT once (untimed), then K steps of the
@@ -318,13 +346,11 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
         tp.tprod_prepared(B, out=Cp_dev, handle=handle, stream=stream)
         evp[i][1].record(stream)
     torch.cuda.synchronize()
-    tpm = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in evp)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tpm, op=dist.ReduceOp.MAX)
+    (tpm,) = _allmax(dist, world, [statistics.mean(a.elapsed_time(b) for a, b in evp)], dev)
     same = bool(torch.equal(Cp_dev, C))
     handle.release_a()
     del Cp_dev
-    out["prepared_a"] = {"ms_per_step": float(tpm), "value": F / (float(tpm) * 1e-3) / 1e12, "unit": "TFLOP/s",
+    out["prepared_a"] = {"ms_per_step": tpm, "value": F / (tpm * 1e-3) / 1e12, "unit": "TFLOP/s",
                          "bitwise_equal_to_full_path": same,
                          "note": "A prepared once per A (tprod_prepare_a_f32, untimed); each step runs K0/K1 of B, "
                                  "the GEMM and the inverse; value credits the full metric flops"}
@@ -344,25 +370,26 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
         tp.tprod_f32_host(Ap, Bp, out=Cp, handle=handle, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    out["e2e"] = {"value": F / (float(e2e_ms) * 1e-3) / 1e12, "unit": "TFLOP/s",
+    (e2e_ms,) = _allmax(dist, world, [e0.elapsed_time(e1) / e2e_steps], dev)
+    out["e2e"] = {"value": F / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                   "h2d_bytes_per_step": 4 * (n1 * n2 * n3 + n2 * n4g * n3),
                   "d2h_bytes_per_step": 4 * n1 * n4g * n3, "steps": e2e_steps}
     del Ap, Bp, Cp
 
-    # ---- parity spot check of the timed output on rank 0: sampled lateral (and, for long tubes,
-    # frontal) slices vs the fp64 oracle
+    # ---- parity spot check of the timed output on every rank: sampled lateral (and, for long
+    # tubes, frontal) slices of the rank's shard vs the fp64 oracle; the line reports the max
+    import oracle as O
+    Jl = np.unique(np.array([0, 1, n4 // 2, n4 - 1]))
+    big = n1 * n2 * n3 > (1 << 27) or n3 > 64          # the oracle gathers A once per slice
+    Tl = np.array([0, 1, n3 // 2, n3 - 1]) if big else np.arange(n3)
+    Cj = C[:, torch.from_numpy(Jl).to(dev), :][:, :, torch.from_numpy(Tl).to(dev)].cpu().numpy()
+    ref = O.tprod_blockrow(A_host.numpy(), B_np[:, Jl, :], Tl, np.arange(len(Jl)))
+    (err,) = _allmax(dist, world, [O.rel_err(Cj, ref)], dev)
+    out["parity_rel_err_sampled"] = err
+    out["parity_sample"] = (f"C(:, {Jl.tolist()}, {Tl.tolist() if big else 'all'}) of every rank's shard "
+                            f"(global columns {j0}+...), max over ranks")
+    out["shard"] = [j0, j1]
     if rank == 0:
-        import oracle as O
-        Jl = np.unique(np.array([0, 1, n4 // 2, n4 - 1]))
-        big = n1 * n2 * n3 > (1 << 27) or n3 > 64          # the oracle gathers A once per slice
-        Tl = np.array([0, 1, n3 // 2, n3 - 1]) if big else np.arange(n3)
-        Cj = C[:, torch.from_numpy(Jl).to(dev), :][:, :, torch.from_numpy(Tl).to(dev)].cpu().numpy()
-        ref = O.tprod_blockrow(A_host.numpy(), B_np[:, Jl, :], Tl, np.arange(len(Jl)))
-        out["parity_rel_err_sampled"] = O.rel_err(Cj, ref)
-        out["parity_sample"] = f"C(:, {Jl.tolist()}, {Tl.tolist() if big else 'all'}) of rank 0's shard"
         out["A_host"] = A_host
         out["B_cols"] = np.asfortranarray(B_np[:, :16, :])
     del A, B, C, flush, flush_rd
@@ -371,19 +398,48 @@ def time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, st
 
 
 def roofline(meas, peaks, src, workload, sustained):
+    """The dominant kernel's roofline (K2 GEMM, tensor-bound) plus SURVEY 8(d)'s whole-call
+    fraction T_roof / T (T_roof = max(F / P_tc, B / BW) for this rank's share) and each
+    memory-bound stage's achieved algorithmic GB/s against the measured HBM peak."""
     P = peaks["bf16_tflops_sustained" if sustained else "bf16_tflops"] / 3.0
+    BW = peaks["hbm_gbs"]
     achieved = meas["gemm_flops_local"] / (meas["gemm_ms"] * 1e-3) / 1e12
     tr = load_traffic(workload)
+    t_roof_ms = max(meas["metric_flops_local"] / (P * 1e12), meas["compulsory_bytes_local"] / (BW * 1e9)) * 1e3
+    sb = meas["stage_bytes_local"]
+    k0, k1, k2, k3 = meas["stage_ms"]
+
+    def gbs(b, t):
+        return b / (t * 1e-3) / 1e9 if t > 0 else None
+    stages = {
+        "K0 scales": {"ms": k0, "bytes": sb["K0"], "GB/s": gbs(sb["K0"], k0), "frac": gbs(sb["K0"], k0) / BW},
+        "K1 forward DFT (A, B)": {"ms": k1, "bytes": sb["K1"], "GB/s": gbs(sb["K1"], k1),
+                                  "frac": gbs(sb["K1"], k1) / BW},
+        "K2 GEMM": {"ms": k2, "TFLOP/s": achieved, "frac": achieved / P},
+        "K3 fill + inverse DFT": {"ms": k3, "bytes": sb["K3"], "GB/s": gbs(sb["K3"], k3),
+                                  "frac": gbs(sb["K3"], k3) / BW},
+    }
     return {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
             "frac": achieved / P, "traffic": tr,
-            "kernel": "K2 per-frequency complex GEMM (gemm_tc_kernel)",
+            "kernel": "K2 per-frequency complex GEMM (gemm_tc2_kernel / gemm_tc_kernel)",
+            "call_frac": t_roof_ms / meas["ms"], "call_t_roof_ms": t_roof_ms,
             "note": (f"achieved = the GEMM's algorithmic flops (8*n1*n2*n4 per complex slice, 2*n1*n2*n4 "
                      f"per real DC/Nyquist slice) / mean K2 time (CUDA events on the "
                      f"launching stream, every timed step); peak = {src} bf16 "
                      f"{'sustained' if sustained else 'burst'} / 3: an fp32-accurate product costs 3 "
-                     f"fp16 tensor-core products (hi*hi + hi*lo + lo*hi)"),
-            "gemm_ms": meas["gemm_ms"], "stage_ms": meas["stage_ms"],
-            "stages": ["K0 scales", "K1 forward DFT (A, B)", "K2 GEMM", "K3 fill + inverse DFT"]}
+                     f"fp16 tensor-core products (hi*hi + hi*lo + lo*hi).  call_frac = T_roof / ms_per_step "
+                     f"with T_roof = max(metric flops / peak, compulsory bytes (A, B read, C written) / "
+                     f"{src} HBM {BW:.0f} GB/s) (SURVEY 8(d))"),
+            "gemm_ms": meas["gemm_ms"], "stage_ms": meas["stage_ms"], "stages": stages}
+
+
+def side_line(m, peaks, src, workload, steps):
+    """A secondary workload measured with the same protocol, reported as an extra key."""
+    return {"value": m["value"], "unit": "TFLOP/s", "ms_per_step": m["ms"],
+            "config": {k: m[k] for k in ("n1", "n2", "n3", "n4")},
+            "roofline": roofline(m, peaks, src, workload, m["ms"] * steps > 500.0),
+            "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": m["clocks"],
+            "prepared_a": m["prepared_a"], "parity_rel_err_sampled": m.get("parity_rel_err_sampled")}
 
 
 def main():
@@ -393,11 +449,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--extra", default="c3,c4,c2",
+                    help="secondary workloads measured at N = 1 with the same protocol (extra keys)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c3", action="store_true", help="skip the secondary config-3 measurement")
+    ap.add_argument("--no-c3", action="store_true", help="no secondary workloads (same as --extra '')")
     ap.add_argument("--engine", type=int, default=0, help="0 tcgen05 (default), 1 SIMT reference")
     ap.add_argument("--bn", type=int, default=0, help="force the GEMM N tile (0 = library heuristic)")
     ap.add_argument("--cn", type=int, default=0, help="force GEMM cluster width 1/2 (0 = heuristic)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (gloo: the multi-rank test on one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -416,27 +476,35 @@ def main():
     import paper_1806_07247_b200 as tp
     from paper_1806_07247_b200 import build as tpbuild
 
-    tpbuild.build()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if rank == 0 or world == 1:
+        tpbuild.build()
+    ngpu = torch.cuda.device_count()
+    gpu = local % max(ngpu, 1)           # one rank per GPU; the gloo test runs 2 ranks on one GPU
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    handle = tp.Handle(local)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+        dist.barrier()                   # rank 0 has built the library before anyone loads it
+    handle = tp.Handle(gpu)
     handle.set_option(tp._lib.TPROD_OPT_ENGINE, args.engine)
     if args.bn:
         handle.set_option(tp._lib.TPROD_OPT_GEMM_BN, args.bn)
     if args.cn:
         handle.set_option(tp._lib.TPROD_OPT_GEMM_CLUSTER, args.cn)
-    if world > 1:
+    if world > 1 and args.dist_backend == "nccl":
         from paper_1806_07247_b200 import dist as tpdist
         handle.set_world(rank, world, tpdist.exchange_uid(tp.nccl_unique_id))
     stream = torch.cuda.current_stream(dev)
 
     meas = time_workload(tp, torch, dist, handle, wl, args, rank, world, local, dev, stream, args.workload)
-    c3 = None
-    if world == 1 and args.workload != "c3" and not args.no_c3:
-        c3 = time_workload(tp, torch, dist, handle, dict(WORKLOADS["c3"]), args, rank, world, local, dev,
-                           stream, "c3")
+    extras = {}
+    if world == 1 and not args.no_c3:
+        for name in [x for x in args.extra.split(",") if x and x != args.workload]:
+            extras[name] = time_workload(tp, torch, dist, handle, dict(WORKLOADS[name]), args, rank, world, local,
+                                         dev, stream, name)
 
     if rank == 0:
         peaks, src = load_peaks()
@@ -450,7 +518,7 @@ def main():
             "config": {"workload": args.workload, "n1": n1, "n2": n2, "n3": n3, "n4": n4,
                        "h": h_slices(n3), "n4_per_gpu": meas["n4_local"],
                        "parallelism": f"lateral-slice shards x{world} (no collective in the step), "
-                                      f"A broadcast once (NCCL)",
+                                      f"A broadcast once ({args.dist_backend})",
                        "l2": "flushed between timed steps (write 2x L2 then read 2x L2, outside the step events)",
                        "engine": "tcgen05" if args.engine == 0 else "simt-reference"},
             "roofline": roofline(meas, peaks, src, args.workload, sustained),
@@ -464,12 +532,8 @@ def main():
         }
         if meas["bcast_ms"] is not None:
             line["setup_bcast_ms"] = meas["bcast_ms"]
-        if c3 is not None:
-            line["c3"] = {"value": c3["value"], "unit": "TFLOP/s", "ms_per_step": c3["ms"],
-                          "config": {"n1": 1024, "n2": 1024, "n3": 31, "n4": 512},
-                          "roofline": roofline(c3, peaks, src, "c3", False),
-                          "e2e": c3["e2e"], "gpu_launches": c3["launches"], "clocks": c3["clocks"],
-                          "parity_rel_err_sampled": c3.get("parity_rel_err_sampled")}
+        for name, m in extras.items():
+            line[name] = side_line(m, peaks, src, name, args.steps)
         if not args.no_cpu_baseline and world == 1:      # rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(wl, meas["A_host"].numpy(), meas["B_cols"])
         print(json.dumps(line), flush=True)

@@ -149,6 +149,18 @@ def _shapes(A, B):
     return int(n1), int(n2), int(n3), int(B.shape[1])
 
 
+def _check_out(out, shape, dtype, device, name="out"):
+    """A caller-supplied output must match exactly what the kernels will write: shape, dtype,
+    device (CUDA index or CPU) and the Matlab layout -- anything else would be an out-of-bounds
+    or wrong-device write inside the library."""
+    if tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != device:
+        raise ValueError(f"{name} must be a {tuple(shape)} {dtype} tensor on {device}, got "
+                         f"{tuple(out.shape)} {out.dtype} on {out.device}")
+    if not is_matlab_layout(out):
+        raise ValueError(f"{name} must have the Matlab layout (strides (1, n1, n1*n2)); use matlab_empty()")
+    return out
+
+
 def _call(fn_name, A, B, out=None, handle=None, stream=None):
     import torch
     n1, n2, n3, n4 = _shapes(A, B)
@@ -161,8 +173,8 @@ def _call(fn_name, A, B, out=None, handle=None, stream=None):
     dev = A.device.index
     if out is None:
         out = matlab_empty(n1, n4, n3, A.dtype, A.device)
-    elif tuple(out.shape) != (n1, n4, n3) or not is_matlab_layout(out) or out.dtype != A.dtype:
-        raise ValueError("out must be a Matlab-layout n1 x n4 x n3 tensor of A's dtype")
+    else:
+        _check_out(out, (n1, n4, n3), A.dtype, A.device)
     h = handle or _default_handle(dev)
     s = stream if stream is not None else torch.cuda.current_stream(A.device)
     st = getattr(lib(), fn_name)(A.data_ptr(), B.data_ptr(), out.data_ptr(), n1, n2, n3, n4,
@@ -185,8 +197,8 @@ def tprod_prepared(B, out=None, handle=None, stream=None):
     n4 = int(B.shape[1])
     if out is None:
         out = matlab_empty(n1, n4, n3, torch.float32, B.device)
-    elif tuple(out.shape) != (n1, n4, n3) or not is_matlab_layout(out) or out.dtype != torch.float32:
-        raise ValueError("out must be a Matlab-layout n1 x n4 x n3 float32 tensor")
+    else:
+        _check_out(out, (n1, n4, n3), torch.float32, B.device)
     s = stream if stream is not None else torch.cuda.current_stream(B.device)
     check(lib().tprod_f32_prepared(B.data_ptr(), out.data_ptr(), n4, C.c_void_p(s.cuda_stream), h.ptr),
           "tprod_f32_prepared")
@@ -208,6 +220,8 @@ def tran(A, out=None, handle=None, stream=None):
     n1, n2, n3 = (int(x) for x in A.shape)
     if out is None:
         out = matlab_empty(n2, n1, n3, A.dtype, A.device)
+    else:
+        _check_out(out, (n2, n1, n3), A.dtype, A.device)
     fn = {torch.float32: lib().tprod_tran_f32, torch.float64: lib().tprod_tran_f64}.get(A.dtype)
     if fn is None:
         raise TypeError(f"tran: unsupported dtype {A.dtype}")
@@ -240,6 +254,8 @@ def tinv(A, out=None, handle=None, stream=None):
     n, _, n3 = (int(x) for x in A.shape)
     if out is None:
         out = matlab_empty(n, n, n3, torch.float32, A.device)
+    else:
+        _check_out(out, (n, n, n3), torch.float32, A.device)
     h, s = _h_s(A, handle, stream)
     check(lib().tprod_tinv_f32(A.data_ptr(), out.data_ptr(), n, n3, s, h.ptr), "tprod_tinv_f32")
     return out
@@ -253,6 +269,8 @@ def tsvt(Y, tau: float, out=None, handle=None, stream=None):
     n1, n2, n3 = (int(x) for x in Y.shape)
     if out is None:
         out = matlab_empty(n1, n2, n3, torch.float32, Y.device)
+    else:
+        _check_out(out, (n1, n2, n3), torch.float32, Y.device)
     h, s = _h_s(Y, handle, stream)
     check(lib().tprod_tsvt_f32(Y.data_ptr(), out.data_ptr(), n1, n2, n3, C.c_float(tau), s, h.ptr),
           "tprod_tsvt_f32")
@@ -316,16 +334,23 @@ def tprod(A, B, out=None, handle=None, stream=None):
     raise TypeError(f"unsupported dtype {A.dtype}")
 
 
-def _host_call(fn_name, A, B, out, handle, stream, device):
-    """End-to-end call on HOST tensors (pinned recommended): H2D, t-product, D2H, synchronise."""
+def _host_call(fn_name, dtype, A, B, out, handle, stream, device):
+    """End-to-end call on HOST tensors (pinned recommended): H2D, t-product, D2H, synchronise.
+    The library copies sizeof(dtype) bytes per element from A, B and into out, so all three are
+    checked for exactly that dtype, shape and layout (a mismatch would be a host over-read /
+    overflow inside the library)."""
     import torch
     n1, n2, n3, n4 = _shapes(A, B)
     if A.is_cuda or B.is_cuda:
         raise ValueError("*_host entry points take CPU tensors")
+    if A.dtype != dtype or B.dtype != dtype:
+        raise TypeError(f"{fn_name} needs {dtype} tensors, got {A.dtype} and {B.dtype}")
     if not (is_matlab_layout(A) and is_matlab_layout(B)):
         raise ValueError("A and B must have the Matlab layout")
     if out is None:
-        out = matlab_empty(n1, n4, n3, A.dtype, "cpu")
+        out = matlab_empty(n1, n4, n3, dtype, "cpu")
+    else:
+        _check_out(out, (n1, n4, n3), dtype, torch.device("cpu"))
     h = handle or _default_handle(device if device is not None else torch.cuda.current_device())
     s = stream if stream is not None else torch.cuda.current_stream(h.device)
     check(getattr(lib(), fn_name)(A.data_ptr(), B.data_ptr(), out.data_ptr(), n1, n2, n3, n4,
@@ -334,11 +359,13 @@ def _host_call(fn_name, A, B, out, handle, stream, device):
 
 
 def tprod_f32_host(A, B, out=None, handle=None, stream=None, device=None):
-    return _host_call("tprod_f32_host", A, B, out, handle, stream, device)
+    import torch
+    return _host_call("tprod_f32_host", torch.float32, A, B, out, handle, stream, device)
 
 
 def tprod_f64_host(A, B, out=None, handle=None, stream=None, device=None):
-    return _host_call("tprod_f64_host", A, B, out, handle, stream, device)
+    import torch
+    return _host_call("tprod_f64_host", torch.float64, A, B, out, handle, stream, device)
 
 
 def dft_f32(X, role: int = 0, handle=None):

@@ -430,15 +430,17 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
   if (tc) {
-    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB, n3 % 2 == 0 ? 1 : 0,
+    st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3 % 2 == 0 ? 1 : 0,
                               h->force_bn, h->force_cn, h->num_sms, s);
     if (st) return st;
   } else {
-    launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, uA, uB, s);
+    launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, s);
   }
   ++launches;                                                     // Alg.1 step 2
   mark(3);
-  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, C, h->num_sms, s); ++launches;     // Alg.1 step 2b + 3
+  // Alg.1 step 2b + 3; each output tube (i, j) unscaled by uA[i] uB[j] after the inverse (R18)
+  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, OutUnscale{uA, uB}, C, h->num_sms, s);
+  ++launches;
   mark(4);
   h->timed_last = h->timing;
   h->last_launches = launches;
@@ -790,7 +792,7 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   launch_absmax_planes(re, im, hh * nn, amax, s);
   const float rtol = (float)n * 9.5367431640625e-07f;                        // n * 2^-20
   if (launch_slice_inverse(re, im, xre, xim, n, hh, nn, rtol, amax, flag, s)) return TPROD_ECUDA;
-  launch_inv_f32(xre, xim, n, nn, n, n, n3, T, X, h->num_sms, s);            // fill + inverse DFT
+  launch_inv_f32(xre, xim, n, nn, n, n, n3, T, OutUnscale{}, X, h->num_sms, s);            // fill + inverse DFT
   if ((st = launch_status())) return st;
   int host_flag = 0;
   CK(cudaMemcpyAsync(&host_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -817,7 +819,7 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   float* wre = (float*)extra;
   float* wim = wre + hh * mn;
   if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, s)) return TPROD_ECUDA;   // step 2
-  launch_inv_f32(wre, wim, n1, mn, n1, n2, n3, T, X, h->num_sms, s);         // step 2b + 3
+  launch_inv_f32(wre, wim, n1, mn, n1, n2, n3, T, OutUnscale{}, X, h->num_sms, s);         // step 2b + 3
   h->last_launches = 5;
   return launch_status();
 }
@@ -846,9 +848,9 @@ int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int
   CK(cudaMemsetAsync(sim, 0, 4 * (size_t)(hh * ns), s));                                  // S-bar is real
   if (launch_slice_svd_factors(re, im, n1, n2, hh, n1 * n2, ure, uim, sre, vre, vim, s)) return TPROD_ECUDA;  // step 2
   // step 2b + 3: conjugate fill + inverse DFT of each factor (S-bar's copy rule = conj of a real slice)
-  launch_inv_f32(ure, uim, n1, nu, n1, r, n3, T, U, h->num_sms, s);
-  launch_inv_f32(sre, sim, r, ns, r, r, n3, T, S, h->num_sms, s);
-  launch_inv_f32(vre, vim, n2, nv, n2, r, n3, T, V, h->num_sms, s);
+  launch_inv_f32(ure, uim, n1, nu, n1, r, n3, T, OutUnscale{}, U, h->num_sms, s);
+  launch_inv_f32(sre, sim, r, ns, r, r, n3, T, OutUnscale{}, S, h->num_sms, s);
+  launch_inv_f32(vre, vim, n2, nv, n2, r, n3, T, OutUnscale{}, V, h->num_sms, s);
   h->last_launches = 8;
   return launch_status();
 }
@@ -985,7 +987,7 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
   cudaStream_t s = (cudaStream_t)stream;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, T, X, h->num_sms, s);
+  launch_inv_f32(Xre, Xim, p, p * q, p, q, n3, T, OutUnscale{}, X, h->num_sms, s);
   h->last_launches = 1;
   return launch_status();
 }

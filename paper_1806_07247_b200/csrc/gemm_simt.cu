@@ -18,8 +18,7 @@ constexpr int TS = 16;
 
 __global__ void gemm_simt_split_kernel(const __half* __restrict__ Ab, int64_t lda,
                                        const __half* __restrict__ Bb, int64_t ldb,
-                                       float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4,
-                                       const float* __restrict__ uA, const float* __restrict__ uB) {
+                                       float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4) {
   __shared__ float sAr[TS][TS + 1], sAi[TS][TS + 1], sBr[TS][TS + 1], sBi[TS][TS + 1];
   const int f = blockIdx.z;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -63,20 +62,18 @@ __global__ void gemm_simt_split_kernel(const __half* __restrict__ Ab, int64_t ld
     __syncthreads();
   }
   if (i < n1 && j < n4) {
-    const float ua = uA[i], ub = uB[j];
     int64_t o = (int64_t)j * ldc + i;
     int64_t pc = (int64_t)n4 * ldc;
-    Cb[(int64_t)(2 * f) * pc + o] = (cr * ua) * ub;
-    Cb[(int64_t)(2 * f + 1) * pc + o] = (ci * ua) * ub;
+    Cb[(int64_t)(2 * f) * pc + o] = cr;          // at the operands' scales (unscaled in K3, R18)
+    Cb[(int64_t)(2 * f + 1) * pc + o] = ci;
   }
 }
 
 void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
-                            int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                            const float* uA, const float* uB, cudaStream_t s) {
+                            int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, cudaStream_t s) {
   dim3 grid((unsigned)((n1 + TS - 1) / TS), (unsigned)((n4 + TS - 1) / TS), (unsigned)h);
   gemm_simt_split_kernel<<<grid, dim3(TS, TS), 0, s>>>(Ab, lda, Bb, ldb, Cb, ldc, (int)n1, (int)n2,
-                                                      (int)n4, uA, uB);
+                                                      (int)n4);
 }
 
 __global__ void gemm_simt_f64_kernel(const double* __restrict__ Ab, int64_t lda,

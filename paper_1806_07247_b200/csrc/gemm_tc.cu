@@ -8,8 +8,9 @@
 // rounding), with the complex product in the 4M form
 //   Cr = Ar.Br - Ai.Bi,   Ci = Ar.Bi + Ai.Br        (-Ai via the instruction descriptor's negate-A bit)
 // i.e. 12 tcgen05.mma.kind::f16 per K step, all accumulating in fp32 in TMEM (Cr in columns
-// [0, BN), Ci in [BN, 2 BN)).  The epilogue multiplies by 2^-(e_i + e_j) (exact) and stores fp32
-// planes [f][re|im][j][i] coalesced along i.
+// [0, BN), Ci in [BN, 2 BN)).  The epilogue stores the accumulators as they are -- C-bar at the
+// operands' exact scales 2^(e_i + e_j), unscaled per output tube after the inverse transform
+// (R18) -- as fp32 planes [f][re|im][j][i] coalesced along i.
 //
 // Kernel structure (one 128 x BN output tile of one frequency per CTA, 128 threads):
 //   warp 0 / lane 0 : TMA producer -- per K block of BK=32: 8 boxes of A (4 planes x 2 M-halves,
@@ -251,7 +252,6 @@ template <int BN, int CN>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
-                   const float* __restrict__ uA, const float* __restrict__ uB,
                    long long* __restrict__ dbg, int nyq) {
   using G = Cfg<BN>;
   const long long t_start = clock64();
@@ -426,15 +426,13 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       const long long ts0 = dbg ? clock64() : 0;
       const int i = ti.m0 + q * 32 + lane;
       if (i < n1) {
-        const float ua = __ldg(uA + i);
         float* Cr = Cb + (int64_t)(2 * ti.f) * plane + (int64_t)n0 * ldc + i;
         float* Ci = Cr + plane;
 #pragma unroll
         for (int x = 0; x < CPT; ++x) {
           if (n0 + x < n4) {
-            const float ub = __ldg(uB + n0 + x);      // exact 2^-(e_i + e_j) unscaling
-            Cr[(int64_t)x * ldc] = (accr[x] * ua) * ub;
-            Ci[(int64_t)x * ldc] = (acci[x] * ua) * ub;
+            Cr[(int64_t)x * ldc] = accr[x];
+            Ci[(int64_t)x * ldc] = acci[x];
           }
         }
       }
@@ -537,8 +535,7 @@ __device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
 template <int SEGKB>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h,
-                    const float* __restrict__ uA, const float* __restrict__ uB, int nyq) {
+                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h, int nyq) {
   constexpr int BN = 128;
   constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
   constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
@@ -723,15 +720,13 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
       }
       const int i = m0 + BM * (int)rank + q * 32 + lane;
       if (i < n1) {
-        const float ua = __ldg(uA + i);
         float* Cr = Cb + (int64_t)(2 * f) * plane + (int64_t)n0 * ldc + i;
         float* Ci = Cr + plane;
 #pragma unroll
         for (int x = 0; x < CPT; ++x) {
           if (n0 + x < n4) {
-            const float ub = __ldg(uB + n0 + x);
-            Cr[(int64_t)x * ldc] = (accr[x] * ua) * ub;
-            Ci[(int64_t)x * ldc] = (acci[x] * ua) * ub;
+            Cr[(int64_t)x * ldc] = accr[x];
+            Ci[(int64_t)x * ldc] = acci[x];
           }
         }
       }
@@ -781,7 +776,7 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 
 template <int BN, int CN>
 int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
-              int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int nyq, int num_sms,
+              int64_t n2, int64_t n4, int64_t h, int nyq, int num_sms,
               cudaStream_t s) {
   using G = Cfg<BN>;
   CUtensorMap mb;
@@ -817,7 +812,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
     cudaMemsetAsync(dbg_buf, 0, 8 * sizeof(long long), s);
     dbg = dbg_buf;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, dbg, nyq) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, dbg, nyq) != cudaSuccess)
     return 4;
   if (dbg) {
     long long hv[8];
@@ -833,7 +828,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
 
 template <int SEGKB>
 int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
-                int64_t n2, int64_t n4, int64_t h, const float* uA, const float* uB, int nyq, int num_sms,
+                int64_t n2, int64_t n4, int64_t h, int nyq, int num_sms,
                 cudaStream_t s) {
   constexpr int BN = 128;
   constexpr int STAGE = NPLANES * (BK * BM * 2 + (BN / 2) * BK * 2);
@@ -861,7 +856,7 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, uA, uB, nyq) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -870,8 +865,7 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
 bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
 
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
-                         int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int nyq, int force_bn, int force_cn,
+                         int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, int nyq, int force_bn, int force_cn,
                          int num_sms, cudaStream_t s) {
   CUtensorMap ma;
   if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
@@ -890,14 +884,14 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   const bool pair_ok = bn == 128 || force_bn == 0;
   if (cn == 3 || (cn == 0 && force_bn == 0 && n1 > 128 &&
                   ((n1 + 255) / 256) * ((n4 + 127) / 128) * h >= num_sms / 2)) {
-    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
   }
   if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
   if (bn == 128)
-    return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s)
-                   : tc::launch_bn<128, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
-  return cn == 2 ? tc::launch_bn<64, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s)
-                 : tc::launch_bn<64, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, uA, uB, nyq, num_sms, s);
+    return cn == 2 ? tc::launch_bn<128, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s)
+                   : tc::launch_bn<128, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
+  return cn == 2 ? tc::launch_bn<64, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s)
+                 : tc::launch_bn<64, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
 }
 
 }  // namespace tprod

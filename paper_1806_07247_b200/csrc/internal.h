@@ -50,11 +50,11 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int64_t n3, int role,
                          const float* unscale, float* re, float* im, cudaStream_t s);
 
-// K2 (reference SIMT engine): C-bar_f = A-bar_f B-bar_f on split operands; epilogue multiplies
-// by uA[i] * uB[j] (exact powers of two).
+// K2 (reference SIMT engine): C-bar_f = A-bar_f B-bar_f on split operands, stored at the operands'
+// exact scales (the inverse transform unscales per output tube, R18).
 void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                             float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                            const float* uA, const float* uB, cudaStream_t s);
+                            cudaStream_t s);
 
 // K2 (tcgen05 engine).  Returns false if the shape/device is not supported by the kernel.
 bool gemm_tc_supported();
@@ -62,21 +62,25 @@ bool gemm_tc_supported();
 // Im planes and run only the Ar.Br products.
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
-                         const float* uA, const float* uB, int nyq, int force_bn, int force_cn,
+                         int nyq, int force_bn, int force_cn,
                          int num_sms, cudaStream_t s);
 
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
-// Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).
+// Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).  Output tube
+// (p, q) is multiplied by urow[p] * ucol[q] (exact powers of two or 0; nullptr = 1) after the
+// inverse FFT (R18: the t-product's C-bar arrives at the operands' scales).
+struct OutUnscale {
+  const float* row = nullptr;
+  const float* col = nullptr;
+};
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, int num_sms, cudaStream_t s);
+                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s);
 
 // TMA-staged persistent dense transforms for n3 <= 64 (transforms_tma.cu); false = not handled
 // (unaligned shapes fall back to the register kernels of transforms_dense.cu).  The inverse
 // requires C-bar in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld).
 bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
-bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
-                    cudaStream_t s);
 
 // Tube-parallel TMA-staged Stockham transforms for power-of-two 32 <= n3 <= 256 (transforms_tma.cu);
 // `st` = Stockham table of host_stockham_table.  false = not handled.  The inverse requires C-bar
@@ -87,12 +91,12 @@ void fourstep_factors(int64_t n3, int* n1, int* n2);
 bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                       const Twiddles32& tw, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
 // inverse: C-bar in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld)
-bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw, float* X,
-                      int num_sms, cudaStream_t s);
+bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw,
+                      OutUnscale u, float* X, int num_sms, cudaStream_t s);
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
-bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
-                     int num_sms, cudaStream_t s);
+bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st,
+                     OutUnscale u, float* X, int num_sms, cudaStream_t s);
 
 // ------------------------------------------------------------------ NEXT-4 (tensor_ops.cu)
 template <typename T>
@@ -127,7 +131,7 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
                       const unsigned* maxbits, __half* out, int64_t ld, float* unscale,
                       cudaStream_t s);
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                      int64_t Q, int64_t n3, float* X, cudaStream_t s);
+                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s);
 
 // In-smem mixed-radix (16/8/4/2, 3, 5) Stockham FFT transforms for 5-smooth 64 < n3 <= 16384
 // (transforms_fft.cu).
@@ -136,7 +140,7 @@ bool fft_supported(int64_t n3);
 bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s);
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
-                    int64_t n3, const float2* st, float* X, cudaStream_t s);
+                    int64_t n3, const float2* st, OutUnscale u, float* X, cudaStream_t s);
 // Per-pass twiddles of the mixed-radix Stockham FFT, laid out [pass][r-1][k] so that a warp's
 // lookups are coalesced: entry (r, k) of the pass with span Ns and radix R is
 // (cos, sin)(2 pi r k / (Ns R)), taken from the fp64 table cs (2n doubles) and rounded to fp32.

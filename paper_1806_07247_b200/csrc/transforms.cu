@@ -231,25 +231,44 @@ void launch_absmax(const float* X, int64_t P, int64_t Q, int64_t n3, int role, u
   }
 }
 
+// Dynamic shared memory for a kernel's staged twiddle table of `bytes`: the table size when the
+// kernel can be opted in to it (up to 96 KB, leaving room for co-resident CTAs), else 0 (the
+// kernel then reads the table from global memory).
+static size_t tw_smem_bytes(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return bytes;
+  if (bytes > 96 * 1024) return 0;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return bytes;
+}
+
 // ------------------------------------------------------------------------------------ K1 (fp32)
 // Generic fallback (any n3; O(n3^2) per tube).  n3 <= 64 runs transforms_dense.cu instead.
+// The twiddle table is staged in shared memory when it fits (tw_smem = 1), else read through L1/L2.
 template <int ROLE>
 __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t Q, int n3, int h,
                                  const unsigned* __restrict__ maxbits,
-                                 const float2* __restrict__ tw, __half* __restrict__ out,
+                                 const float2* __restrict__ tw, int tw_smem, __half* __restrict__ out,
                                  int64_t ld, float* __restrict__ unscale) {
-  extern __shared__ float2 stw[];
-  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw[m] = tw[m];
-  __syncthreads();
+  extern __shared__ float2 stw_buf[];
+  const float2* stw = tw;
+  if (tw_smem) {
+    for (int m = threadIdx.x; m < n3; m += blockDim.x) stw_buf[m] = tw[m];
+    __syncthreads();
+    stw = stw_buf;
+  }
   int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
   int64_t q = blockIdx.x / pblocks;
   int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const int64_t PQ = P * Q;
   const float* x = X + p + P * q;
-  const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), n3);
+  const unsigned mb = __ldg(maxbits + (ROLE == 0 ? p : q));
+  const int e = scale_exp(mb, n3);
   const float sc = pow2f(e);
-  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = pow2f(-e);
+  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = unscale_of(mb, e);
   const int64_t plane = Q * ld;
   __half* o = out + q * ld + p;
   for (int f = 0; f < h; ++f) {
@@ -288,12 +307,14 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
   if (tw.st && launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
-  size_t smem = sizeof(float2) * (size_t)n3;
   int h = (int)h_slices(n3);
+  const void* k = role == 0 ? (const void*)fwd_split_kernel<0> : (const void*)fwd_split_kernel<1>;
+  const size_t smem = tw_smem_bytes(k, sizeof(float2) * (size_t)n3);
+  const int ts = smem > 0;
   if (role == 0)
-    fwd_split_kernel<0><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld, unscale);
+    fwd_split_kernel<0><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, ts, out, ld, unscale);
   else
-    fwd_split_kernel<1><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, out, ld, unscale);
+    fwd_split_kernel<1><<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, h, maxbits, tw.tw, ts, out, ld, unscale);
 }
 
 __global__ void decode_split_kernel(const __half* __restrict__ in, int64_t ld, int64_t P, int64_t Q,
@@ -323,11 +344,15 @@ void launch_decode_split(const __half* in, int64_t ld, int64_t P, int64_t Q, int
 template <typename T, typename T2>
 __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim, int64_t ld,
                            int64_t fstride, int64_t P, int64_t Q, int n3, int h,
-                           const T2* __restrict__ tw, T* __restrict__ X) {
+                           const T2* __restrict__ tw, int tw_smem, OutUnscale u, T* __restrict__ X) {
   extern __shared__ unsigned char smem_raw[];
-  T2* stw = reinterpret_cast<T2*>(smem_raw);
-  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw[m] = tw[m];
-  __syncthreads();
+  const T2* stw = tw;
+  if (tw_smem) {
+    T2* b = reinterpret_cast<T2*>(smem_raw);
+    for (int m = threadIdx.x; m < n3; m += blockDim.x) b[m] = tw[m];
+    __syncthreads();
+    stw = b;
+  }
   int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
   int64_t q = blockIdx.x / pblocks;
   int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
@@ -335,6 +360,7 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
   const T* cr = Cre + q * ld + p;
   const T* ci = Cim + q * ld + p;
   const T inv_n = T(1) / T(n3);
+  const float2 sc = out_scale(u.row, p, u.col, q, 1.f);      // R18 (fp64 path: nullptr, exactly 1)
   for (int t = 0; t < n3; ++t) {
     T acc = cr[0];                      // Re C-bar_0 (Im of DC discarded)
     int m = 0;
@@ -346,33 +372,37 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
       T v = r * w.x - i * w.y;          // Re(C-bar_f e^{+i theta})
       acc += (2 * f == n3) ? v : T(2) * v;
     }
-    X[p + P * q + P * Q * (int64_t)t] = acc * inv_n;
+    X[p + P * q + P * Q * (int64_t)t] = ((acc * inv_n) * (T)sc.x) * (T)sc.y;
   }
 }
 
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                    int64_t Q, int64_t n3, Twiddles32 tw, float* X, int num_sms, cudaStream_t s) {
+                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s) {
   const bool prod_layout = tw.staged && Cim == Cre + Q * ld && fstride == 2 * Q * ld;
-  if (prod_layout && launch_inv_tma(Cre, ld, P, Q, n3, X, num_sms, s)) return;
+  if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, u, X, num_sms, s)) return;
   cudaGetLastError();
-  if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, X, num_sms, s)) return;
+  if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, u, X, num_sms, s)) return;
   cudaGetLastError();
-  if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, X, num_sms, s)) return;
-  cudaGetLastError();
-  if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, X, s)) return;
-  if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, X, s)) return;
+  if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, u, X, s)) return;
+  if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, u, X, s)) return;
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
-  inv_kernel<float, float2><<<(unsigned)blocks, threads, sizeof(float2) * n3, s>>>(
-      Cre, Cim, ld, fstride, P, Q, (int)n3, (int)h_slices(n3), tw.tw, X);
+  const size_t smem = tw_smem_bytes((const void*)inv_kernel<float, float2>, sizeof(float2) * (size_t)n3);
+  inv_kernel<float, float2><<<(unsigned)blocks, threads, smem, s>>>(
+      Cre, Cim, ld, fstride, P, Q, (int)n3, (int)h_slices(n3), tw.tw, smem > 0, u, X);
 }
 
 // ------------------------------------------------------------------------------------ fp64 path
 __global__ void fwd_f64_kernel(const double* __restrict__ X, int64_t P, int64_t Q, int n3, int h,
-                               const double2* __restrict__ tw, double* __restrict__ out, int64_t ld) {
-  extern __shared__ double2 stw64[];
-  for (int m = threadIdx.x; m < n3; m += blockDim.x) stw64[m] = tw[m];
-  __syncthreads();
+                               const double2* __restrict__ tw, int tw_smem, double* __restrict__ out,
+                               int64_t ld) {
+  extern __shared__ double2 stw64_buf[];
+  const double2* stw64 = tw;
+  if (tw_smem) {
+    for (int m = threadIdx.x; m < n3; m += blockDim.x) stw64_buf[m] = tw[m];
+    __syncthreads();
+    stw64 = stw64_buf;
+  }
   int64_t pblocks = (P + blockDim.x - 1) / blockDim.x;
   int64_t q = blockIdx.x / pblocks;
   int64_t p = (blockIdx.x % pblocks) * blockDim.x + threadIdx.x;
@@ -401,16 +431,18 @@ void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles6
                     int64_t ld, cudaStream_t s) {
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
-  fwd_f64_kernel<<<(unsigned)blocks, threads, sizeof(double2) * n3, s>>>(
-      X, P, Q, (int)n3, (int)h_slices(n3), tw.tw, out, ld);
+  const size_t smem = tw_smem_bytes((const void*)fwd_f64_kernel, sizeof(double2) * (size_t)n3);
+  fwd_f64_kernel<<<(unsigned)blocks, threads, smem, s>>>(X, P, Q, (int)n3, (int)h_slices(n3), tw.tw, smem > 0, out,
+                                                         ld);
 }
 
 void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
                     double* X, cudaStream_t s) {
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
-  inv_kernel<double, double2><<<(unsigned)blocks, threads, sizeof(double2) * n3, s>>>(
-      Cb, Cb + Q * ld, ld, 2 * Q * ld, P, Q, (int)n3, (int)h_slices(n3), tw.tw, X);
+  const size_t smem = tw_smem_bytes((const void*)inv_kernel<double, double2>, sizeof(double2) * (size_t)n3);
+  inv_kernel<double, double2><<<(unsigned)blocks, threads, smem, s>>>(
+      Cb, Cb + Q * ld, ld, 2 * Q * ld, P, Q, (int)n3, (int)h_slices(n3), tw.tw, smem > 0, OutUnscale{}, X);
 }
 
 }  // namespace tprod

@@ -164,9 +164,10 @@ __global__ void __launch_bounds__(128) fwd_dense_kernel(const float* __restrict_
       Xf[f] = make_float2(re, im);
     }
   }
-  const int e = scale_exp(__ldg(maxbits + (ROLE == 0 ? p : q)), N);
+  const unsigned mb = __ldg(maxbits + (ROLE == 0 ? p : q));
+  const int e = scale_exp(mb, N);
   const float sc = pow2f(e);
-  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = pow2f(-e);
+  if (ROLE == 0 ? q == 0 : p == 0) unscale[ROLE == 0 ? p : q] = unscale_of(mb, e);
   const int64_t plane = Q * ld;
   __half* o = out + q * ld + p;
 #pragma unroll
@@ -185,7 +186,7 @@ template <int N>
 __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict__ Cre,
                                                         const float* __restrict__ Cim, int64_t ld,
                                                         int64_t fstride, int64_t P, int64_t Q,
-                                                        float* __restrict__ X) {
+                                                        OutUnscale u, float* __restrict__ X) {
   constexpr int H = N / 2 + 1;
   const int64_t pblocks = (P + 127) >> 7;
   const int64_t q = blockIdx.x / pblocks;
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
   const int64_t PQ = P * Q;
   float* xo = X + p + P * q;
   if constexpr (is_pow2(N) && N >= 8) {
+    const float2 sc = out_scale(u.row, p, u.col, q, 1.f);      // R18 (irfft_half applies 1/N)
     float2 Xf[H];
 #pragma unroll
     for (int f = 0; f < H; ++f) {
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
     float xt[N];
     irfft_half<N>(Xf, xt);
 #pragma unroll
-    for (int t = 0; t < N; ++t) xo[PQ * t] = xt[t];
+    for (int t = 0; t < N; ++t) xo[PQ * t] = apply_scale(xt[t], sc);
     return;
   }
   float R[H], I[H];
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
     R[f] = wf * __ldg(cr + fstride * f);
     I[f] = (f == 0 || 2 * f == N) ? 0.f : wf * __ldg(ci + fstride * f);  // Im of DC/Nyquist dropped
   }
-  const float inv_n = 1.f / (float)N;
+  const float2 sc = out_scale(u.row, p, u.col, q, 1.f / (float)N);   // 1/N and R18 unscale
 #pragma unroll
   for (int t = 0; t <= N / 2; ++t) {
     float a = R[0], b = 0.f;
@@ -225,8 +227,8 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
       a = fmaf(R[f], tw.x, a);
       b = fmaf(-I[f], tw.y, b);
     }
-    xo[PQ * t] = (a + b) * inv_n;
-    if (t > 0 && 2 * t != N) xo[PQ * (N - t)] = (a - b) * inv_n;
+    xo[PQ * t] = apply_scale(a + b, sc);
+    if (t > 0 && 2 * t != N) xo[PQ * (N - t)] = apply_scale(a - b, sc);
   }
 }
 
@@ -290,15 +292,17 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
   }
   int e0, e1;
   if (ROLE == 0) {
-    e0 = scale_exp(__ldg(maxbits + p), N);
-    e1 = scale_exp(__ldg(maxbits + p + 1), N);
+    const unsigned m0 = __ldg(maxbits + p), m1 = __ldg(maxbits + p + 1);
+    e0 = scale_exp(m0, N);
+    e1 = scale_exp(m1, N);
     if (q == 0) {
-      unscale[p] = pow2f(-e0);
-      unscale[p + 1] = pow2f(-e1);
+      unscale[p] = unscale_of(m0, e0);
+      unscale[p + 1] = unscale_of(m1, e1);
     }
   } else {
-    e0 = e1 = scale_exp(__ldg(maxbits + q), N);
-    if (p == 0) unscale[q] = pow2f(-e0);
+    const unsigned mq = __ldg(maxbits + q);
+    e0 = e1 = scale_exp(mq, N);
+    if (p == 0) unscale[q] = unscale_of(mq, e0);
   }
   const float s0 = pow2f(e0), s1 = pow2f(e1);
   const int64_t plane = Q * ld;
@@ -321,7 +325,7 @@ template <int N>
 __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict__ Cre,
                                                          const float* __restrict__ Cim, int64_t ld,
                                                          int64_t fstride, int64_t P, int64_t Q,
-                                                         float* __restrict__ X) {
+                                                         OutUnscale u, float* __restrict__ X) {
   constexpr int H = N / 2 + 1;
   const int64_t pblocks = (P + 255) >> 8;
   const int64_t q = blockIdx.x / pblocks;
@@ -333,6 +337,7 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
   const int64_t PQh = (P * Q) >> 1;
   float2* xo = reinterpret_cast<float2*>(X + p + P * q);
   if constexpr (is_pow2(N) && N >= 8) {
+    const float2 s0 = out_scale(u.row, p, u.col, q, 1.f), s1 = out_scale(u.row, p + 1, u.col, q, 1.f);
     float2 X0[H], X1[H];
 #pragma unroll
     for (int f = 0; f < H; ++f) {
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
     irfft_half<N>(X0, x0);
     irfft_half<N>(X1, x1);
 #pragma unroll
-    for (int t = 0; t < N; ++t) xo[PQh * t] = make_float2(x0[t], x1[t]);
+    for (int t = 0; t < N; ++t) xo[PQh * t] = make_float2(apply_scale(x0[t], s0), apply_scale(x1[t], s1));
     return;
   }
   float2 R[H], I[H];
@@ -364,6 +369,7 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
     }
   }
   const float inv_n = 1.f / (float)N;
+  const float2 s0 = out_scale(u.row, p, u.col, q, inv_n), s1 = out_scale(u.row, p + 1, u.col, q, inv_n);
 #pragma unroll
   for (int t = 0; t <= N / 2; ++t) {
     float2 a = R[0], b = make_float2(0.f, 0.f);
@@ -375,14 +381,15 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
       b.x = fmaf(-I[f].x, tw.y, b.x);
       b.y = fmaf(-I[f].y, tw.y, b.y);
     }
-    xo[PQh * t] = make_float2((a.x + b.x) * inv_n, (a.y + b.y) * inv_n);
-    if (t > 0 && 2 * t != N) xo[PQh * (N - t)] = make_float2((a.x - b.x) * inv_n, (a.y - b.y) * inv_n);
+    xo[PQh * t] = make_float2(apply_scale(a.x + b.x, s0), apply_scale(a.y + b.y, s1));
+    if (t > 0 && 2 * t != N)
+      xo[PQh * (N - t)] = make_float2(apply_scale(a.x - b.x, s0), apply_scale(a.y - b.y, s1));
   }
 }
 
 // ------------------------------------------------------------------------------ dispatch tables
 using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
-using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, float*);
+using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, OutUnscale, float*);
 
 template <int N>
 struct DenseTable {
@@ -464,13 +471,13 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 }
 
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                      int64_t Q, int64_t n3, float* X, cudaStream_t s) {
+                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s) {
   if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
   const bool pair = n3 <= PAIR_MAX && P % 2 == 0 && ld % 2 == 0 && fstride % 2 == 0 &&
                     ((uintptr_t)X & 7) == 0 && ((uintptr_t)Cre & 7) == 0 && ((uintptr_t)Cim & 7) == 0;
   InvFn fn = pair ? dense_fns().invp[n3] : dense_fns().inv[n3];
   int64_t blocks = (P + (pair ? 255 : 127)) / (pair ? 256 : 128) * Q;
-  void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&X};
+  void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&u, (void*)&X};
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
 }
 

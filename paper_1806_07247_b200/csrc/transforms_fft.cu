@@ -238,12 +238,12 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
       e0 = scale_exp(__ldg(maxbits + p), N);
       e1 = two ? scale_exp(__ldg(maxbits + p + 1), N) : 0;
       if (q == 0) {
-        unscale[p] = pow2f(-e0);
-        if (two) unscale[p + 1] = pow2f(-e1);
+        unscale[p] = unscale_of(__ldg(maxbits + p), e0);
+        if (two) unscale[p + 1] = unscale_of(__ldg(maxbits + p + 1), e1);
       }
     } else {
       e0 = e1 = scale_exp(__ldg(maxbits + q), N);
-      if (p0 == 0 && c == 0) unscale[q] = pow2f(-e0);
+      if (p0 == 0 && c == 0) unscale[q] = unscale_of(__ldg(maxbits + q), e0);
     }
   }
   const float s0 = ROLE == 0 ? 1.f : pow2f(e0), s1 = ROLE == 0 ? 1.f : pow2f(e1);   // A: applied at load
@@ -285,9 +285,10 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
                                                                  const float* __restrict__ Cim, int64_t ld,
                                                                  int64_t fstride, int64_t P, int64_t Q,
                                                                  int N, int F, const __grid_constant__ FftPlan pl,
-                                                                 const float2* __restrict__ st,
+                                                                 const float2* __restrict__ st, OutUnscale u,
                                                                  float* __restrict__ X, int vec) {
   extern __shared__ float2 z[];
+  __shared__ float2 ssc[2 * (FFT_POINTS / 64)];   // per-tube output scale (1/N and R18), TUB <= 256
   const int TUB = 2 * F;
   const int Np = bstride(N, F);
   const int64_t pblocks = (P + TUB - 1) / TUB;
@@ -313,9 +314,10 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
     z[c * Np + pad(f)] = make_float2(xr - yi, xi + yr);                 // X_f + i Y_f
     if (!self) z[c * Np + pad(N - f)] = make_float2(xr + yi, yr - xi);  // conj X_f + i conj Y_f
   }
+  for (int t = threadIdx.x; t < TUB; t += IFFT_THREADS)
+    ssc[t] = p0 + t < P ? out_scale(u.row, p0 + t, u.col, q, 1.f / (float)N) : make_float2(0.f, 0.f);
   __syncthreads();
   fft_smem<+1, IFFT_THREADS>(z, N, F, Np, pl, st);
-  const float inv_n = 1.f / (float)N;
   const int64_t PQ = P * Q;
   float* xo = X + P * q + p0;
   if (vec && (TUB % 4) == 0 && p0 + TUB <= P && (P % 4) == 0 && (((uintptr_t)X) & 15) == 0) {
@@ -325,14 +327,16 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
     for (int idx = threadIdx.x; idx < total; idx += IFFT_THREADS) {
       const int vv = idx % V, k = idx / V;
       const float2 a = z[(2 * vv) * Np + pad(k)], b = z[(2 * vv + 1) * Np + pad(k)];
-      reinterpret_cast<float4*>(xo + PQ * k)[vv] = make_float4(a.x * inv_n, a.y * inv_n, b.x * inv_n, b.y * inv_n);
+      reinterpret_cast<float4*>(xo + PQ * k)[vv] =
+          make_float4(apply_scale(a.x, ssc[4 * vv]), apply_scale(a.y, ssc[4 * vv + 1]),
+                      apply_scale(b.x, ssc[4 * vv + 2]), apply_scale(b.y, ssc[4 * vv + 3]));
     }
   } else {
     for (int idx = threadIdx.x; idx < TUB * N; idx += IFFT_THREADS) {
       const int t = idx % TUB, k = idx / TUB;
       if (p0 + t >= P) continue;
       const float2 v = z[(t >> 1) * Np + pad(k)];
-      xo[PQ * k + t] = ((t & 1) == 0 ? v.x : v.y) * inv_n;
+      xo[PQ * k + t] = apply_scale((t & 1) == 0 ? v.x : v.y, ssc[t]);
     }
   }
 }
@@ -400,7 +404,7 @@ bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
 }
 
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
-                    int64_t n3, const float2* st, float* X, cudaStream_t s) {
+                    int64_t n3, const float2* st, OutUnscale u, float* X, cudaStream_t s) {
   if (!fft_supported(n3)) return false;
   FftPlan pl;
   make_plan((int)n3, &pl);
@@ -412,7 +416,7 @@ bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   const int vec = (P % TUB == 0) && (ld % 2 == 0) && (fstride % 2 == 0) && (((uintptr_t)Cre) & 7) == 0 &&
                   (((uintptr_t)Cim) & 7) == 0;
   if (!fft_smem_ok((const void*)fft_inv_kernel, N)) return false;
-  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, F, pl, st, X, vec);
+  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, F, pl, st, u, X, vec);
   return cudaGetLastError() == cudaSuccess;
 }
 

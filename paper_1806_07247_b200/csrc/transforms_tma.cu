@@ -1,6 +1,7 @@
-// TMA-staged, persistent dense mode-3 transforms for n3 <= 64 (the production K1/K3 of configs
-// 2, 3, 5).  Same arithmetic as transforms_dense.cu (conjugate-pair folding, compile-time twiddle
-// indices into a constant-bank table), different data movement:
+// TMA-staged mode-3 transforms.  (1) Persistent dense forward DFT for non-power-of-two
+// 32 < n3 <= 64 (fwd_tma_kernel; the inverse of those sizes runs the register kernels of
+// transforms_dense.cu, measured faster).  Same arithmetic as transforms_dense.cu (conjugate-pair
+// folding, compile-time twiddle indices into a constant-bank table), different data movement:
 //
 //   * a work item is 256 consecutive tubes p0..p0+255 of one q;
 //   * one thread TMA-loads the item's whole tile  X(p0:p0+256, q, 0:n3)  (a 3-D box, the
@@ -8,8 +9,9 @@
 //     persistent loop, so HBM latency overlaps the arithmetic of the previous item without
 //     holding the tile in registers;
 //   * each thread reads its TPT adjacent tubes from smem (conflict-free) and writes half2/__half
-//     (K1) or float2/float (K3) results, warp-coalesced along p.  TPT = 2 for n3 <= 32, else 1
-//     (register budget).
+//     results, warp-coalesced along p.  TPT = 2 for n3 <= 32, else 1 (register budget).
+// (2) Tube-parallel Stockham FFTs for power-of-two n3 (K1 and K3) and (3) the four-step long-tube
+// transforms, described at their kernels below.
 //
 // K1: Alg. 1 step 1, Eq. (2), Hermitian half (Eq. (8)).
 // K3: Alg. 1 step 2 second branch + step 3 (L177-179): fused conjugate fill + inverse DFT.
@@ -183,10 +185,10 @@ __global__ void __launch_bounds__(TP / tpt_of(N)) fwd_tma_kernel(const __grid_co
       int e = 0;
       if (ROLE == 0) {
         if (p + t < P) e = scale_exp(__ldg(maxbits + p + t), N);
-        if (q == 0 && p + t < P) unscale[p + t] = pow2f(-e);
+        if (q == 0 && p + t < P) unscale[p + t] = unscale_of(__ldg(maxbits + p + t), e);
       } else {
         e = scale_exp(__ldg(maxbits + q), N);
-        if (p == 0 && t == 0) unscale[q] = pow2f(-e);
+        if (p == 0 && t == 0) unscale[q] = unscale_of(__ldg(maxbits + q), e);
       }
       sc[t] = pow2f(e);
     }
@@ -217,64 +219,6 @@ __global__ void __launch_bounds__(TP / tpt_of(N)) fwd_tma_kernel(const __grid_co
       __half* of = o + (int64_t)(4 * f) * plane;
       store_split<TPT>(of + PL_RE_HI * plane, of + PL_RE_LO * plane, re, pair);
       store_split<TPT>(of + PL_IM_HI * plane, of + PL_IM_LO * plane, im, pair);
-    }
-  });
-}
-
-template <int N>
-__global__ void __launch_bounds__(TP / tpt_of(N)) inv_tma_kernel(const __grid_constant__ CUtensorMap mC,
-                                                                int64_t P, int64_t Q, float* __restrict__ X) {
-  constexpr int H = N / 2 + 1;
-  constexpr int TPT = tpt_of(N);
-  constexpr int BUF = TP * 2 * H;                  // floats per buffer: [f][re|im][256]
-  extern __shared__ __align__(128) float smem[];
-  __shared__ uint64_t full[2];
-  const int tid = threadIdx.x;
-  const float inv_n = 1.f / (float)N;
-  const int64_t PQ = P * Q;
-  tma_pipeline<BUF>(&mC, P, Q, smem, full, [&](const Item& cur, const float* s) {
-    const int64_t p = cur.p0 + TPT * tid;
-    if (p >= P) return;
-    float R[H][TPT], I[H][TPT];
-#pragma unroll
-    for (int f = 0; f < H; ++f) {
-      const bool self = (f == 0 || 2 * f == N);
-      const float wf = self ? 1.f : 2.f;             // conjugate fill weight
-      lds<TPT>(s, 2 * f, tid, R[f]);
-      lds<TPT>(s, 2 * f + 1, tid, I[f]);
-#pragma unroll
-      for (int t = 0; t < TPT; ++t) {
-        R[f][t] *= wf;
-        I[f][t] = self ? 0.f : I[f][t] * wf;       // Im of DC/Nyquist dropped (C2R)
-      }
-    }
-    float* xo = X + p + P * cur.q;
-#pragma unroll
-    for (int tt = 0; tt <= N / 2; ++tt) {
-      float a[TPT], bb[TPT];
-#pragma unroll
-      for (int t = 0; t < TPT; ++t) {
-        a[t] = R[0][t];
-        bb[t] = 0.f;
-      }
-#pragma unroll
-      for (int f = 1; f < H; ++f) {
-        const float2 tw = c_tw2[toff(N) + (f * tt) % N];
-#pragma unroll
-        for (int t = 0; t < TPT; ++t) {
-          a[t] = fmaf(R[f][t], tw.x, a[t]);
-          bb[t] = fmaf(-I[f][t], tw.y, bb[t]);
-        }
-      }
-      if constexpr (TPT == 2) {
-        *reinterpret_cast<float2*>(xo + PQ * tt) = make_float2((a[0] + bb[0]) * inv_n, (a[1] + bb[1]) * inv_n);
-        if (tt > 0 && 2 * tt != N)
-          *reinterpret_cast<float2*>(xo + PQ * (N - tt)) =
-              make_float2((a[0] - bb[0]) * inv_n, (a[1] - bb[1]) * inv_n);
-      } else {
-        xo[PQ * tt] = (a[0] + bb[0]) * inv_n;
-        if (tt > 0 && 2 * tt != N) xo[PQ * (N - tt)] = (a[0] - bb[0]) * inv_n;
-      }
     }
   });
 }
@@ -316,8 +260,11 @@ __host__ __device__ constexpr int tube_toff(int log, int i) {
 // PRE: multiply the loaded values by `pre` (the thread's column c = threadIdx.x % F is the same for
 // all its butterflies since NT % F == 0): per-tube exact scales applied before two real tubes share
 // one complex FFT, so neither tube's rounding error is large relative to the other's scale.
-template <int N, int F, int R, int Ns, int DIR, int NT = TUBE_NT, bool PRE = false>
-__device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp, float2 pre = make_float2(1.f, 1.f)) {
+// POST: multiply the results by post1 then post2 (per tube of the pair, same fixed column) before
+// they are stored: the inverse's per-output-tube unscale of DESIGN.md R18.
+template <int N, int F, int R, int Ns, int DIR, int NT = TUBE_NT, bool PRE = false, bool POST = false>
+__device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ tp, float2 pre = make_float2(1.f, 1.f),
+                                          float2 post1 = make_float2(1.f, 1.f), float2 post2 = make_float2(1.f, 1.f)) {
   constexpr int NB = N / R;
   constexpr int BPT = F * NB / NT;
   static_assert(F * NB % NT == 0, "butterflies must divide evenly");
@@ -338,6 +285,11 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
       for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twN<DIR>(tp, (r - 1) * Ns + k));
     }
     dft_reg<R, DIR>(v[u]);
+    if (POST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        v[u][r] = make_float2((v[u][r].x * post1.x) * post2.x, (v[u][r].y * post1.y) * post2.y);
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -350,11 +302,18 @@ __device__ __forceinline__ void tube_pass(float2* z, const float2* __restrict__ 
   __syncthreads();
 }
 
-template <int N, int DIR, int F = TubeCfg<N>::F, int NT = TUBE_NT, bool PRE = false>
-__device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st, float2 pre = make_float2(1.f, 1.f)) {
+template <int N, int DIR, int F = TubeCfg<N>::F, int NT = TUBE_NT, bool PRE = false, bool POST = false>
+__device__ __forceinline__ void tube_fft(float2* z, const float2* __restrict__ st, float2 pre = make_float2(1.f, 1.f),
+                                         float2 post1 = make_float2(1.f, 1.f), float2 post2 = make_float2(1.f, 1.f)) {
   using C = TubeCfg<N>;
-  tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT, PRE>(z, st, pre);
-  if constexpr (C::NP > 1) tube_pass<N, F, tube_R(C::LOG, 1), tube_Ns(1), DIR, NT>(z, st + tube_toff(C::LOG, 1));
+  static_assert(C::NP <= 2, "tube FFTs have at most two passes");
+  if constexpr (C::NP == 1) {
+    tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT, PRE, POST>(z, st, pre, post1, post2);
+  } else {
+    tube_pass<N, F, tube_R(C::LOG, 0), tube_Ns(0), DIR, NT, PRE>(z, st, pre);
+    tube_pass<N, F, tube_R(C::LOG, 1), tube_Ns(1), DIR, NT, false, POST>(z, st + tube_toff(C::LOG, 1),
+                                                                          make_float2(1.f, 1.f), post1, post2);
+  }
 }
 
 // K1 epilogue staged in shared memory: the item's 4h output rows (f, plane) of TUB halves are
@@ -381,12 +340,12 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
       if (in0) e0 = scale_exp(__ldg(maxbits + p), N);
       if (in1) e1 = scale_exp(__ldg(maxbits + p + 1), N);
       if (q == 0 && threadIdx.x < F) {
-        if (in0) unscale[p] = pow2f(-e0);
-        if (in1) unscale[p + 1] = pow2f(-e1);
+        if (in0) unscale[p] = unscale_of(__ldg(maxbits + p), e0);
+        if (in1) unscale[p + 1] = unscale_of(__ldg(maxbits + p + 1), e1);
       }
     } else {
       e0 = e1 = scale_exp(__ldg(maxbits + q), N);
-      if (cur.p0 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
+      if (cur.p0 == 0 && threadIdx.x == 0) unscale[q] = unscale_of(__ldg(maxbits + q), e0);
     }
     // A's two tubes of a pair have their own row scales: applied before the shared FFT (exact
     // powers of two); B's pair shares its column scale, applied after
@@ -423,13 +382,13 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
-// K3: the 1/N of the inverse is applied while Z is built (a power of two: exact), and the
-// transformed tile z[k][c] -- which read as floats IS the output rows X(p0:p0+TUB, q, k) -- leaves
-// by one TMA bulk tensor store.
+// K3: the 1/N of the inverse is applied while Z is built (a power of two: exact), the per-tube
+// unscale (R18) by the last FFT pass, and the transformed tile z[k][c] -- which read as floats IS
+// the output rows X(p0:p0+TUB, q, k) -- leaves by one TMA bulk tensor store.
 template <int N>
 __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant__ CUtensorMap mC,
                                                           const __grid_constant__ CUtensorMap mXo, int64_t P,
-                                                          int64_t Q, const float2* __restrict__ st) {
+                                                          int64_t Q, const float2* __restrict__ st, OutUnscale u) {
   using C = TubeCfg<N>;
   constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
   constexpr int BUF = TUB * 2 * H;                  // C-bar tile: rows [f][re|im], TUB floats each
@@ -451,7 +410,13 @@ __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant
       if (!self) z[(N - f) * F + c] = make_float2((re.x + im.y) * inv_n, (re.y - im.x) * inv_n);
     }
     __syncthreads();
-    tube_fft<N, +1>(z, st);
+    {
+      const int64_t p = cur.p0 + 2 * (threadIdx.x % F);         // this thread's tube pair (TUBE_NT % F == 0)
+      const float2 a = p < P ? out_scale(u.row, p, u.col, cur.q, 1.f) : make_float2(0.f, 0.f);
+      const float2 b = p + 1 < P ? out_scale(u.row, p + 1, u.col, cur.q, 1.f) : make_float2(0.f, 0.f);
+      tube_fft<N, +1, F, TUBE_NT, false, true>(z, st, make_float2(1.f, 1.f), make_float2(a.x, b.x),
+                                               make_float2(a.y, b.y));
+    }
     fence_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -585,12 +550,12 @@ __global__ void __launch_bounds__(2 * TUB) fwd4_pass2_kernel(const __grid_consta
         e0 = scale_exp(__ldg(maxbits + p), N);
         if (in1) e1 = scale_exp(__ldg(maxbits + p + 1), N);
         if (q == 0 && f2 == 0 && threadIdx.x < F) {
-          unscale[p] = pow2f(-e0);
-          if (in1) unscale[p + 1] = pow2f(-e1);
+          unscale[p] = unscale_of(__ldg(maxbits + p), e0);
+          if (in1) unscale[p + 1] = unscale_of(__ldg(maxbits + p + 1), e1);
         }
       } else {
         e0 = e1 = scale_exp(__ldg(maxbits + q), N);
-        if (p0 == 0 && f2 == 0 && threadIdx.x == 0) unscale[q] = pow2f(-e0);
+        if (p0 == 0 && f2 == 0 && threadIdx.x == 0) unscale[q] = unscale_of(__ldg(maxbits + q), e0);
       }
       const float s0 = ROLE == 0 ? 1.f : pow2f(e0), s1 = ROLE == 0 ? 1.f : pow2f(e1);   // A: applied in pass 1
       __half* o = out + q * ld + p;
@@ -738,7 +703,8 @@ __global__ void __launch_bounds__(2 * TUB) inv4_pass1_kernel(const __grid_consta
 template <int N1, int TUB>
 __global__ void __launch_bounds__(2 * TUB) inv4_pass2_kernel(const __grid_constant__ CUtensorMap mW4,
                                                             const __grid_constant__ CUtensorMap mX4t, int64_t P,
-                                                            int64_t Q, int N2, const float2* __restrict__ st1) {
+                                                            int64_t Q, int N2, const float2* __restrict__ st1,
+                                                            OutUnscale u) {
   constexpr int F = TUB / 2, NT = 2 * TUB;
   extern __shared__ __align__(128) float smem[];
   __shared__ uint64_t full;
@@ -766,8 +732,14 @@ __global__ void __launch_bounds__(2 * TUB) inv4_pass2_kernel(const __grid_consta
           : "memory");
     }
     bar_wait(&full, ph);
-    tube_fft<N1, +1, F, NT>(z, st1);                          // over f1 -> z[k1][c]
-    for (int idx = threadIdx.x; idx < N1 * F; idx += NT) z[idx] = make_float2(z[idx].x * inv_n, z[idx].y * inv_n);
+    {
+      // 1/N and the per-tube unscale (R18), folded into the last pass; NT % F == 0: fixed pair
+      const int64_t p = p0 + 2 * (threadIdx.x % F);
+      const float2 a = p < P ? out_scale(u.row, p, u.col, q, inv_n) : make_float2(0.f, 0.f);
+      const float2 b = p + 1 < P ? out_scale(u.row, p + 1, u.col, q, inv_n) : make_float2(0.f, 0.f);
+      tube_fft<N1, +1, F, NT, false, true>(z, st1, make_float2(1.f, 1.f), make_float2(a.x, b.x),
+                                           make_float2(a.y, b.y));   // over f1 -> z[k1][c]
+    }
     fence_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -783,7 +755,6 @@ __global__ void __launch_bounds__(2 * TUB) inv4_pass2_kernel(const __grid_consta
 
 // ------------------------------------------------------------------------------ tables / launch
 using FwdFn = void (*)(CUtensorMap, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
-using InvFn = void (*)(CUtensorMap, int64_t, int64_t, float*);
 
 // Measured (config 3, n3 = 31): the register kernels of transforms_dense.cu (direct warp-coalesced
 // loads, ~14 warps/SM) already run K1 at ~5.5 TB/s and K3 faster than the TMA-staged variants, so
@@ -793,21 +764,20 @@ constexpr int TMIN = 33;
 
 template <int N>
 struct Tab {
-  static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
+  static void fill(FwdFn* f0, FwdFn* f1) {
     f0[N] = fwd_tma_kernel<N, 0>;
     f1[N] = fwd_tma_kernel<N, 1>;
-    Tab<N - 1>::fill(f0, f1, inv);
+    Tab<N - 1>::fill(f0, f1);
   }
 };
 template <>
 struct Tab<TMIN - 1> {
-  static void fill(FwdFn*, FwdFn*, InvFn*) {}
+  static void fill(FwdFn*, FwdFn*) {}
 };
 
 struct Fns {
   FwdFn f0[TMAX + 1] = {}, f1[TMAX + 1] = {};
-  InvFn inv[TMAX + 1] = {};
-  Fns() { Tab<TMAX>::fill(f0, f1, inv); }
+  Fns() { Tab<TMAX>::fill(f0, f1); }
 };
 const Fns& fns() {
   static Fns t;
@@ -923,8 +893,8 @@ bool launch_fwd_tube_n(const float* X, int64_t P, int64_t Q, int role, const uns
 }
 
 template <int N>
-bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const float2* st, float* X, int num_sms,
-                       cudaStream_t s) {
+bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const float2* st, OutUnscale u, float* X,
+                       int num_sms, cudaStream_t s) {
   using C = TubeCfg<N>;
   constexpr int H = N / 2 + 1;
   CUtensorMap m, mo;
@@ -937,7 +907,7 @@ bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
   const int grid = grid_occ(fn, items, smem, num_sms);
-  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&st};
+  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&st, (void*)&u};
   return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
 }
 
@@ -1005,8 +975,8 @@ bool map_cbar_5d(CUtensorMap* m, const void* base, uint64_t P, uint64_t ld, uint
 }
 
 template <int N1, int N2, int TUB>
-bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twiddles32& tw, float* X, int num_sms,
-                   cudaStream_t s) {
+bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twiddles32& tw, OutUnscale u, float* X,
+                   int num_sms, cudaStream_t s) {
   CUtensorMap mc, mw1, mw2, mx;
   if (!map_cbar_5d(&mc, Cre, P, ld, Q, N1, N2 / 2 + 1, TUB) ||
       !map_f32_4d(&mw1, tw.scratch, P, Q, N1, N2, TUB, 1, N2) ||
@@ -1032,7 +1002,7 @@ bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twi
   const float2* twn = tw.tw;
   void* a1[] = {(void*)&mc, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn};
   if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
-  void* a2[] = {(void*)&mw2, (void*)&mx, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&st1};
+  void* a2[] = {(void*)&mw2, (void*)&mx, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&st1, (void*)&u};
   return cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) == cudaSuccess;
 }
 }  // namespace
@@ -1046,8 +1016,8 @@ void fourstep_factors(int64_t n3, int* n1, int* n2) {
   else if (n3 == 16384) { *n1 = 128; *n2 = 128; }
 }
 
-bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw, float* X,
-                      int num_sms, cudaStream_t s) {
+bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw,
+                      OutUnscale u, float* X, int num_sms, cudaStream_t s) {
   int N1, N2;
   fourstep_factors(n3, &N1, &N2);
   if (!N1 || !tw.st_n1 || !tw.st_n2 || !tw.scratch || tw.scratch_bytes < (size_t)(4 * P * Q * n3) || P % 4 != 0 ||
@@ -1055,13 +1025,13 @@ bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_
     return false;
   const bool wide = P >= 128;
   if (N1 == 64 && N2 == 64)
-    return wide ? launch_inv4_t<64, 64, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
-                : launch_inv4_t<64, 64, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
+    return wide ? launch_inv4_t<64, 64, 128>(Cre, ld, P, Q, tw, u, X, num_sms, s)
+                : launch_inv4_t<64, 64, 64>(Cre, ld, P, Q, tw, u, X, num_sms, s);
   if (N1 == 128 && N2 == 64)
-    return wide ? launch_inv4_t<128, 64, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
-                : launch_inv4_t<128, 64, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
-  return wide ? launch_inv4_t<128, 128, 128>(Cre, ld, P, Q, tw, X, num_sms, s)
-              : launch_inv4_t<128, 128, 64>(Cre, ld, P, Q, tw, X, num_sms, s);
+    return wide ? launch_inv4_t<128, 64, 128>(Cre, ld, P, Q, tw, u, X, num_sms, s)
+                : launch_inv4_t<128, 64, 64>(Cre, ld, P, Q, tw, u, X, num_sms, s);
+  return wide ? launch_inv4_t<128, 128, 128>(Cre, ld, P, Q, tw, u, X, num_sms, s)
+              : launch_inv4_t<128, 128, 64>(Cre, ld, P, Q, tw, u, X, num_sms, s);
 }
 
 bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
@@ -1102,14 +1072,14 @@ bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
   }
 }
 
-bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st, float* X,
-                     int num_sms, cudaStream_t s) {
+bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st,
+                     OutUnscale u, float* X, int num_sms, cudaStream_t s) {
   if (!st || !tube_inv_pick(n3) || P % 4 != 0 || ((uintptr_t)X & 15) != 0 || (ld * 4) % 16 != 0) return false;
   switch (n3) {
-    case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, X, num_sms, s);
-    case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, X, num_sms, s);
-    case 128: return launch_inv_tube_n<128>(Cre, ld, P, Q, st, X, num_sms, s);
-    default: return launch_inv_tube_n<256>(Cre, ld, P, Q, st, X, num_sms, s);
+    case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, u, X, num_sms, s);
+    case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, u, X, num_sms, s);
+    case 128: return launch_inv_tube_n<128>(Cre, ld, P, Q, st, u, X, num_sms, s);
+    default: return launch_inv_tube_n<256>(Cre, ld, P, Q, st, u, X, num_sms, s);
   }
 }
 
@@ -1127,27 +1097,6 @@ bool launch_fwd_tma(const float* X, int64_t P, int64_t Q, int64_t n3, int role, 
   const int thr = threads_of(n3);
   const int grid = grid_for(items, smem, thr, num_sms);
   void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld, (void*)&unscale};
-  return cudaLaunchKernel((const void*)fn, dim3(grid), dim3(thr), args, smem, s) == cudaSuccess;
-}
-
-bool launch_inv_tma(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, float* X, int num_sms,
-                    cudaStream_t s) {
-  // C-bar planes [f][re|im][q][ld] as a 3-D map {P (pitch ld), Q, 2h}
-  if (n3 < TMIN || n3 > TMAX || fns().inv[n3] == nullptr || !ensure_tw() || ((uintptr_t)X & 7) != 0 ||
-      P % 2 != 0)
-    return false;
-  const int64_t h = n3 / 2 + 1;
-  CUtensorMap m;
-  if (!map_f32(&m, Cre, (uint64_t)P, (uint64_t)ld, (uint64_t)Q, (uint64_t)(2 * h), (uint32_t)(2 * h)))
-    return false;
-  InvFn fn = fns().inv[n3];
-  const size_t smem = 2 * sizeof(float) * TP * 2 * (size_t)h;
-  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return false;
-  const int64_t items = (P + TP - 1) / TP * Q;
-  const int thr = threads_of(n3);
-  const int grid = grid_for(items, smem, thr, num_sms);
-  void* args[] = {(void*)&m, (void*)&P, (void*)&Q, (void*)&X};
   return cudaLaunchKernel((const void*)fn, dim3(grid), dim3(thr), args, smem, s) == cudaSuccess;
 }
 

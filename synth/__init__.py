@@ -14,6 +14,9 @@ from __future__ import annotations
 
 import numpy as np
 
+# the lateral-slice partition (pure index arithmetic, one definition): re-exported for tests/bench
+from paper_1806_07247_b200.dist import lateral_shard  # noqa: F401
+
 # BASELINE.json configs (shape tuples (n1, n2, n3, n4), dtype, seeds)
 CONFIGS = {
     "c1": dict(n1=20, n2=30, n3=10, n4=15, dtype="f64", seedA=0, seedB=1, seedD=2),
@@ -68,17 +71,6 @@ def normal_lateral(shape, seed: int, j0: int, j1: int, dtype=np.float32) -> np.n
                 flat[d:d + (b - a)] = vals[a - pos:b - pos]
         pos = e
     return out
-
-
-def lateral_shard(n4: int, world: int, rank: int) -> tuple[int, int]:
-    """Balanced contiguous block [start, stop) of lateral slices owned by ``rank``.
-
-    Pure index arithmetic (no t-product math): used by bench.py and tests for the
-    lateral-slice partition of B and C."""
-    base, extra = divmod(n4, world)
-    start = rank * base + min(rank, extra)
-    stop = start + base + (1 if rank < extra else 0)
-    return start, stop
 
 
 def sample_columns(n4: int, count: int = 64, seed: int = 42) -> np.ndarray:

@@ -80,3 +80,60 @@ def test_sass_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([exe, "--list-elf", lib], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_sass_summary_matches_build(L):
+    """Per-kernel SASS evidence of the tcgen05 / TMEM / TMA path, recomputed from the built library
+    (scripts/sass_summary.py) and compared with the committed profiles/sass_summary.json: the GEMM
+    kernels issue UTCHMMA (2-CTA in the pair kernel), load operands with UTMALDG and read TMEM
+    with LDTM; the tube / four-step transforms move tiles with UTMALDG / UTMASTG."""
+    import json
+    import shutil
+    import sys
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    import sass_summary
+    got = sass_summary.summary(os.path.join(ROOT, "paper_1806_07247_b200", "libtprod.so"))
+    assert got["arch"] == ["sm_100a"]
+
+    def fam(name, d):
+        return {k: v for k, v in d["kernels"].items() if name in k}
+    pair = fam("gemm_tc2_kernel", got)
+    assert pair and all(v.get("UTCHMMA.2CTA", 0) > 0 and v.get("LDTM.x16", 0) > 0 and
+                        v.get("UTMALDG.3D.2CTA", 0) > 0 for v in pair.values())
+    single = fam("gemm_tc_kernel", got)
+    assert single and all(v.get("UTCHMMA", 0) > 0 and v.get("LDTM.x16", 0) > 0 for v in single.values())
+    for name in ("fwd_tube_kernel", "inv_tube_kernel"):
+        ks = fam(name, got)
+        assert ks and all(v.get("UTMALDG.3D", 0) > 0 and v.get("UTMASTG.3D", 0) > 0 for v in ks.values()), name
+    for name in ("fwd4_pass1_kernel", "inv4_pass2_kernel"):
+        ks = fam(name, got)
+        assert ks and all(v.get("UTMALDG.4D", 0) > 0 and v.get("UTMASTG.4D", 0) > 0 for v in ks.values()), name
+    with open(os.path.join(ROOT, "profiles", "sass_summary.json")) as f:
+        committed = json.load(f)
+    assert committed["kernels"] == got["kernels"], "profiles/sass_summary.json is stale: rerun scripts/sass_summary.py"
+
+
+def test_binding_rejects_mismatched_host_and_out_arguments():
+    """The host entry points copy sizeof(dtype) bytes per element from A and B and into out: the
+    binding rejects any dtype / shape / device / layout mismatch before the library is reached
+    (a float32 tensor passed to tprod_f64_host was a host over-read / overflow)."""
+    import torch
+    import paper_1806_07247_b200 as T
+    A32 = T.matlab_empty(4, 3, 5, torch.float32, "cpu").zero_()
+    B32 = T.matlab_empty(3, 2, 5, torch.float32, "cpu").zero_()
+    with pytest.raises(TypeError):
+        T.tprod_f64_host(A32, B32)
+    with pytest.raises(TypeError):
+        T.tprod_f32_host(A32.double(), B32.double())
+    with pytest.raises(TypeError):
+        T.tprod_f32_host(A32, B32.double())
+    with pytest.raises(ValueError):                    # wrong shape
+        T.tprod_f32_host(A32, B32, out=T.matlab_empty(4, 3, 5, torch.float32, "cpu"))
+    with pytest.raises(ValueError):                    # wrong dtype
+        T.tprod_f32_host(A32, B32, out=T.matlab_empty(4, 2, 5, torch.float64, "cpu"))
+    with pytest.raises(ValueError):                    # not the Matlab layout
+        T.tprod_f32_host(A32, B32, out=torch.empty((4, 2, 5), dtype=torch.float32))
+    with pytest.raises(ValueError):                    # shape mismatch of the operands
+        T.tprod_f32_host(A32, T.matlab_empty(4, 2, 5, torch.float32, "cpu"))

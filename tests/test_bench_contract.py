@@ -37,3 +37,30 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "c2"
+
+
+def test_roofline_call_frac_and_stage_rates():
+    """The bench line's roofline: GEMM fraction against bf16/3, SURVEY 8(d)'s whole-call fraction
+    T_roof / T with T_roof = max(F / P, B / BW), and the memory-bound stages' algorithmic GB/s."""
+    sys.path.insert(0, ROOT)
+    import bench
+    n1, n2, n3, n4 = 1024, 1024, 31, 512
+    peaks = {"hbm_gbs": 6000.0, "bf16_tflops": 1500.0, "bf16_tflops_sustained": 1200.0}
+    meas = {"gemm_flops_local": bench.gemm_flops(n1, n2, n3, n4), "gemm_ms": 0.2,
+            "metric_flops_local": bench.metric_flops(n1, n2, n3, n4),
+            "compulsory_bytes_local": 4.0 * n3 * (n1 * n2 + n2 * n4 + n1 * n4),
+            "stage_bytes_local": bench.stage_bytes(n1, n2, n3, n4),
+            "stage_ms": [0.05, 0.1, 0.2, 0.05], "ms": 0.5}
+    r = bench.roofline(meas, peaks, "test", "c3", sustained=False)
+    P = 1500.0 / 3
+    assert abs(r["peak"] - P) < 1e-9
+    assert abs(r["achieved"] - bench.gemm_flops(n1, n2, n3, n4) / 0.2e-3 / 1e12) < 1e-9
+    t_roof = max(bench.metric_flops(n1, n2, n3, n4) / (P * 1e12),
+                 4.0 * n3 * (n1 * n2 + n2 * n4 + n1 * n4) / 6000e9)
+    assert abs(r["call_frac"] - t_roof * 1e3 / 0.5) < 1e-12
+    h = n3 // 2 + 1
+    k1 = (4 * n3 + 8 * h) * (n1 * n2 + n2 * n4) / 0.1e-3 / 1e9
+    assert abs(r["stages"]["K1 forward DFT (A, B)"]["GB/s"] - k1) < 1e-6
+    assert abs(r["stages"]["K3 fill + inverse DFT"]["frac"] - (8 * h + 4 * n3) * n1 * n4 / 0.05e-3 / 1e9 / 6000) < 1e-9
+    rs = bench.roofline(meas, peaks, "test", "c3", sustained=True)
+    assert abs(rs["peak"] - 400.0) < 1e-9
