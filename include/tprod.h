@@ -15,7 +15,9 @@
  *
  * Ownership: all tensor pointers are caller-owned; the library never frees or retains them past
  * the call.  The handle owns its plan cache, DFT tables and workspace (device memory, grown on
- * demand, freed by tprod_destroy) and an optional NCCL communicator.
+ * demand, freed by tprod_destroy) and an optional NCCL communicator.  Workspace growth is stream
+ * ordered (cudaMallocAsync / cudaFreeAsync on the call's stream): it never synchronises the device,
+ * so a handle must be used from one stream at a time (or the caller orders the streams).
  *
  * Errors: every entry point returns an int status (0 = TPROD_OK).  Argument errors are detected
  * synchronously, BEFORE anything is enqueued.  Device-side faults of enqueued kernels surface at
@@ -188,7 +190,11 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
-       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6 };
+       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7 };
+/* TPROD_OPT_POISON: 1 = before every call the handle fills the workspace it will use (and a prepared
+ * operand's buffers) with 0xFF bytes -- NaN in fp16 / fp32 / fp64 -- on the call's stream, so that any
+ * kernel reading workspace it has not written first turns the result into NaN (a test-time stand-in
+ * for compute-sanitizer's initcheck).  Results are unchanged when the kernels are correct. */
 /* TPROD_OPT_GRAPHS (tprod_f32 / tprod_f64 / tprod_f32_prepared): 1 (default) = the second and later
  * calls with the same operand pointers, shapes and options replay the call's launch sequence as
  * one CUDA graph (captured on a private stream at the second call, launched on the caller's
@@ -196,12 +202,16 @@ enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_
  * graph only removes per-kernel host work and launch gaps.  Bypassed while TPROD_OPT_TIMING is on
  * (stage events between direct launches) and when the caller's stream is being captured.  The handle keeps at most 64 graphs (all are
  * dropped, after a device synchronisation, when a 65th key arrives or the workspace grows). */
-/* TPROD_OPT_TRANSFORM (fp32 path): 0 = auto (TMA-staged / tube-parallel transform kernels where
- * they apply), 1 = register-resident transform kernels only.  Same arithmetic up to rounding
- * order of the DFT sums (both within the stage tolerances). */
+/* TPROD_OPT_TRANSFORM (fp32 path): 0 = auto (the TMA-staged / tube-parallel / four-step transform
+ * kernels where they apply, else the register-resident / mixed-radix / generic ones), 1 =
+ * register-resident and generic transform kernels only, 2 = for 2 <= n3 <= 64 the tensor-core
+ * DFT-matrix kernels (Eq. (2) as a tcgen05 3xTF32 contraction, transforms_tc.cu; measured slower
+ * than auto on B200), else auto.  Same result up to the rounding of the DFT sums (all
+ * within the stage tolerances). */
 /* TPROD_OPT_GEMM_CLUSTER: 0 = auto, 1 = independent CTAs, 2 = 2-CTA clusters along N sharing the
  * A tile by TMA multicast, 3 = CTA pairs issuing tcgen05.mma.cta_group::2 (256 x 128 tiles over two
- * SMs; requires the 128 N tile).  None of the options changes the arithmetic (results are bitwise
+ * SMs; requires the 128 N tile), 4 = 4-CTA clusters of two such pairs stacked along M sharing the B
+ * tile by TMA multicast (512 x 128 cluster tiles).  None of the options changes the arithmetic (results are bitwise
  * identical for every option value except TPROD_OPT_ENGINE). */
 int tprod_set_option(tprod_handle h, int option, int64_t value);
 

@@ -14,7 +14,7 @@ TPROD_OK, TPROD_EINVAL, TPROD_EALIAS, TPROD_ENOMEM, TPROD_ECUDA, TPROD_ENCCL, \
     TPROD_EUNSUPPORTED, TPROD_ENOWORLD, TPROD_ESINGULAR = range(9)
 TPROD_DTYPE_F32, TPROD_DTYPE_F64 = 0, 1
 (TPROD_OPT_ENGINE, TPROD_OPT_GEMM_BN, TPROD_OPT_TIMING, TPROD_OPT_GEMM_CLUSTER, TPROD_OPT_TRANSFORM,
- TPROD_OPT_GRAPHS) = 1, 2, 3, 4, 5, 6
+ TPROD_OPT_GRAPHS, TPROD_OPT_POISON) = 1, 2, 3, 4, 5, 6, 7
 
 # name -> (restype, argtypes); the full list of symbols include/tprod.h declares
 _i64, _vp, _int = C.c_int64, C.c_void_p, C.c_int

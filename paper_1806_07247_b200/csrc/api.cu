@@ -62,6 +62,7 @@ struct tprod_ctx {
   // CUDA-graph cache of the launch sequence (TPROD_OPT_GRAPHS): key = everything the kernels'
   // parameters derive from (operand / workspace / table pointers, shapes, options)
   bool graphs = true;
+  bool poison = false;                                 // TPROD_OPT_POISON: NaN-fill the workspace before each call
   cudaStream_t cap = nullptr;                          // private capture stream
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -69,6 +70,10 @@ struct tprod_ctx {
     int64_t launches = 0;
   };
   std::map<std::vector<int64_t>, GraphEntry> graph_cache;
+  // buffers from cudaMallocAsync (released with cudaFreeAsync); buffers replaced while a stream was
+  // being captured are kept in `retired` until tprod_destroy
+  std::map<void*, bool> async_buf;
+  std::vector<void*> retired;
 };
 
 namespace {
@@ -128,10 +133,12 @@ Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = 
   L.off_Ab = o;  if (with_A) o = align_up(o + 2 * (size_t)(L.h * NPLANES * n2 * L.lda), 1024);
   L.off_Bb = o;   o = align_up(o + 2 * (size_t)(L.h * NPLANES * n4 * L.ldb), 1024);
   L.off_Cb = o;   o = align_up(o + 4 * (size_t)(L.h * 2 * n4 * L.ldc), 1024);
-  // four-step long-tube forward: intermediate the size of the larger operand
+  // four-step long-tube transforms: intermediate the size of the largest tensor they transform
+  // (A and B forward, C inverse -- without C's size a prepared-operand call with n1 > n2 fell back
+  // to the mixed-radix inverse and differed from the one-shot call in the last bits)
   int f1 = 0, f2 = 0;
   fourstep_factors(n3, &f1, &f2);
-  L.W_bytes = f1 ? 4 * (size_t)(std::max(with_A ? n1 * n2 : 0, n2 * n4) * n3) : 0;
+  L.W_bytes = f1 ? 4 * (size_t)(std::max({with_A ? n1 * n2 : (int64_t)0, n2 * n4, n1 * n4}) * n3) : 0;
   L.off_W = o;    o = align_up(o + L.W_bytes, 1024);
   L.total = o;
   return L;
@@ -154,35 +161,77 @@ Layout64 layout64(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
 
 void clear_graphs(tprod_ctx* h);
 
-int ensure_ws(tprod_ctx* h, size_t bytes) {
+// Stream-ordered device buffers of the handle (workspace, host-path buffers, prepared operands):
+// allocated with cudaMallocAsync on the call's stream and released with cudaFreeAsync on the stream
+// of the call that outgrows them, so growing a buffer never synchronises the device (work already
+// enqueued on that stream finishes with the old buffer first; a handle is used from one stream at a
+// time, include/tprod.h).  While the stream is being captured into a graph, plain cudaMalloc is
+// used and an outgrown buffer is kept until tprod_destroy.
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) { cudaGetLastError(); return true; }
+  return cs != cudaStreamCaptureStatusNone;
+}
+int dev_alloc(tprod_ctx* h, void** p, size_t bytes, cudaStream_t s) {
+  *p = nullptr;
+  if (!capturing(s) && cudaMallocAsync(p, bytes, s) == cudaSuccess) {
+    h->async_buf[*p] = true;
+    return TPROD_OK;
+  }
+  cudaGetLastError();
+  if (cudaMalloc(p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return TPROD_ENOMEM;
+  }
+  h->async_buf[*p] = false;
+  return TPROD_OK;
+}
+void dev_release(tprod_ctx* h, void* p, cudaStream_t s) {
+  if (!p) return;
+  auto it = h->async_buf.find(p);
+  const bool async = it != h->async_buf.end() && it->second;
+  if (async && !capturing(s) && cudaFreeAsync(p, s) == cudaSuccess) {
+    h->async_buf.erase(it);
+    return;
+  }
+  cudaGetLastError();
+  h->retired.push_back(p);
+}
+
+// Grow-only workspace; the cached graphs address the old buffer and are dropped (an executable
+// graph still in flight is released by the driver when it completes).
+int ensure_ws(tprod_ctx* h, size_t bytes, cudaStream_t s) {
   if (h->ws_bytes >= bytes) return TPROD_OK;
   if (h->ws) {
-    CK(cudaDeviceSynchronize());
-    clear_graphs(h);                                   // their kernels address the old workspace
-    cudaFree(h->ws);
+    clear_graphs(h);
+    dev_release(h, h->ws, s);
     h->ws = nullptr;
     h->ws_bytes = 0;
   }
-  if (cudaMalloc(&h->ws, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return TPROD_ENOMEM;
-  }
+  int st = dev_alloc(h, &h->ws, bytes, s);
+  if (st) return st;
   h->ws_bytes = bytes;
   return TPROD_OK;
 }
 
-int ensure_hbuf(tprod_ctx* h, int which, size_t bytes) {
+// TPROD_OPT_POISON: fill `bytes` of the workspace with 0xFF (a NaN pattern in fp32 / fp64 / fp16)
+// on the call's stream, so that a kernel reading workspace it did not write first shows up as NaN
+// in the result (the stand-in for initcheck, which is not available on the GPU pool).
+int poison_ws(tprod_ctx* h, size_t bytes, cudaStream_t s) {
+  if (!h->poison || !bytes) return TPROD_OK;
+  CK(cudaMemsetAsync(h->ws, 0xFF, std::min(bytes, h->ws_bytes), s));
+  return TPROD_OK;
+}
+
+int ensure_hbuf(tprod_ctx* h, int which, size_t bytes, cudaStream_t s) {
   if (h->hbuf_bytes[which] >= bytes) return TPROD_OK;
   if (h->hbuf[which]) {
-    CK(cudaDeviceSynchronize());
-    cudaFree(h->hbuf[which]);
+    dev_release(h, h->hbuf[which], s);
     h->hbuf[which] = nullptr;
     h->hbuf_bytes[which] = 0;
   }
-  if (cudaMalloc(&h->hbuf[which], bytes) != cudaSuccess) {
-    cudaGetLastError();
-    return TPROD_ENOMEM;
-  }
+  if (int st = dev_alloc(h, &h->hbuf[which], bytes, s)) return st;
   h->hbuf_bytes[which] = bytes;
   return TPROD_OK;
 }
@@ -286,25 +335,27 @@ int prepare_into(tprod_ctx* h, PreparedA& P, const float* A, int64_t n1, int64_t
   const size_t bytes = off_Ab + 2 * (size_t)(hh * NPLANES * n2 * lda);
   if (P.bytes < bytes) {
     if (P.buf) {
-      CK(cudaDeviceSynchronize());
-      cudaFree(P.buf);
+      dev_release(h, P.buf, s);
       P.buf = nullptr;
       P.bytes = 0;
     }
-    if (cudaMalloc(&P.buf, bytes) != cudaSuccess) { cudaGetLastError(); P.valid = false; return TPROD_ENOMEM; }
+    if ((st = dev_alloc(h, &P.buf, bytes, s))) { P.valid = false; return st; }
     P.bytes = bytes;
   }
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
+  T.staged = h->transform != 1;
+  T.tc = h->transform == 2;
   int f1 = 0, f2 = 0;
   fourstep_factors(n3, &f1, &f2);
   if (f1) {
     const size_t w = 4 * (size_t)(n1 * n2 * n3);
-    if ((st = ensure_ws(h, w))) return st;
+    if ((st = ensure_ws(h, w, s))) return st;
     T.scratch = (float*)h->ws;
     T.scratch_bytes = w;
   }
+  if (h->poison) CK(cudaMemsetAsync(P.buf, 0xFF, bytes, s));
+  if ((st = poison_ws(h, T.scratch_bytes, s))) return st;
   P.maxA = (unsigned*)P.buf;
   P.uA = (float*)((char*)P.buf + off_u);
   P.Ab = (__half*)((char*)P.buf + off_Ab);
@@ -342,10 +393,8 @@ int graph_run(tprod_ctx* h, std::vector<int64_t>&& key, cudaStream_t s, Body&& b
   if (cs != cudaStreamCaptureStatusNone) return body(s);
   auto it = h->graph_cache.find(key);
   if (it == h->graph_cache.end()) {
-    if (h->graph_cache.size() >= GRAPH_CACHE_MAX) {   // rare: drop the lot (an exec may be in flight)
-      CK(cudaDeviceSynchronize());
-      clear_graphs(h);
-    }
+    if (h->graph_cache.size() >= GRAPH_CACHE_MAX)     // rare: drop the lot (in-flight execs are
+      clear_graphs(h);                                 // released by the driver on completion)
     it = h->graph_cache.emplace(std::move(key), tprod_ctx::GraphEntry{}).first;
   }
   tprod_ctx::GraphEntry& e = it->second;
@@ -384,7 +433,7 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
 int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2,
             int64_t n3, int64_t n4, cudaStream_t s, const PreparedA* pa = nullptr) {
   Layout32 L = layout32(n1, n2, n3, n4, pa == nullptr);
-  int st = ensure_ws(h, L.total);
+  int st = ensure_ws(h, L.total, s);
   if (st) return st;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
@@ -399,7 +448,8 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
 int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
                int64_t n4, cudaStream_t s, const PreparedA* pa, const Layout32& L, Twiddles32 T) {
   int st = 0;
-  T.staged = h->transform == 0;
+  T.staged = h->transform != 1;
+  T.tc = h->transform == 2;
   char* ws = (char*)h->ws;
   T.scratch = L.W_bytes ? (float*)(ws + L.off_W) : nullptr;
   T.scratch_bytes = L.W_bytes;
@@ -414,6 +464,7 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
 
   auto mark = [&](int i) { if (h->timing) cudaEventRecord(h->ev[i], s); };
   h->timed_last = false;
+  if ((st = poison_ws(h, L.total, s))) return st;
   mark(0);
   CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_uA - L.off_maxA, s));
   const float* A0 = pa ? nullptr : A;
@@ -450,7 +501,7 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
 int run_f64(tprod_ctx* h, const double* A, const double* B, double* C, int64_t n1, int64_t n2,
             int64_t n3, int64_t n4, cudaStream_t s) {
   Layout64 L = layout64(n1, n2, n3, n4);
-  int st = ensure_ws(h, L.total);
+  int st = ensure_ws(h, L.total, s);
   if (st) return st;
   const double2* tw = nullptr;
   if ((st = get_tw64(h, (int)n3, &tw))) return st;
@@ -462,6 +513,7 @@ int run_f64(tprod_ctx* h, const double* A, const double* B, double* C, int64_t n
   std::vector<int64_t> key = {2, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
                               (int64_t)(uintptr_t)h->ws};
   return graph_run(h, std::move(key), s, [&](cudaStream_t ls) {
+    if (int ps = poison_ws(h, L.total, ls)) return ps;
     launch_fwd_f64(A, n1, n2, n3, T, Ab, n1, ls);
     launch_fwd_f64(B, n2, n4, n3, T, Bb, n2, ls);
     launch_gemm_simt_f64(Ab, n1, Bb, n2, Cb, n1, n1, n2, n4, L.h, ls);
@@ -503,7 +555,7 @@ int host_call_f32_pipelined(const float* A, const float* B, float* C, int64_t n1
     }
   }
   const size_t bA = 4 * (size_t)(n1 * n2 * n3), bBc = 4 * (size_t)(n2 * w * n3), bCc = 4 * (size_t)(n1 * w * n3);
-  if ((st = ensure_hbuf(h, 0, bA)) || (st = ensure_hbuf(h, 1, 2 * bBc)) || (st = ensure_hbuf(h, 2, 2 * bCc))) return st;
+  if ((st = ensure_hbuf(h, 0, bA, s)) || (st = ensure_hbuf(h, 1, 2 * bBc, s)) || (st = ensure_hbuf(h, 2, 2 * bCc, s))) return st;
   float* dA = (float*)h->hbuf[0];
   float* dB[2] = {(float*)h->hbuf[1], (float*)((char*)h->hbuf[1] + bBc)};
   float* dC[2] = {(float*)h->hbuf[2], (float*)((char*)h->hbuf[2] + bCc)};
@@ -559,7 +611,7 @@ int host_call(const T* A, const T* B, T* C, int64_t n1, int64_t n2, int64_t n3, 
   cudaStream_t s = (cudaStream_t)stream;
   size_t bA = sizeof(T) * (size_t)(n1 * n2 * n3), bB = sizeof(T) * (size_t)(n2 * n4 * n3),
          bC = sizeof(T) * (size_t)(n1 * n4 * n3);
-  if ((st = ensure_hbuf(h, 0, bA)) || (st = ensure_hbuf(h, 1, bB)) || (st = ensure_hbuf(h, 2, bC))) return st;
+  if ((st = ensure_hbuf(h, 0, bA, s)) || (st = ensure_hbuf(h, 1, bB, s)) || (st = ensure_hbuf(h, 2, bC, s))) return st;
   CK(cudaMemcpyAsync(h->hbuf[0], A, bA, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(h->hbuf[1], B, bB, cudaMemcpyHostToDevice, s));
   if (sizeof(T) == 4)
@@ -612,11 +664,12 @@ int spectral_planes(tprod_ctx* h, const float* Y, int64_t n1, int64_t n2, int64_
   const size_t off_re = o;   o = align_up(o + 4 * (size_t)(2 * hh * mn), 1024);
   const size_t off_x = o;    o = align_up(o + extra, 1024);
   const size_t off_w = o;    o = align_up(o + wb, 1024);
-  if ((st = ensure_ws(h, o))) return st;
+  if ((st = ensure_ws(h, o, s)) || (st = poison_ws(h, o, s))) return st;
   char* ws = (char*)h->ws;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
+  T.staged = h->transform != 1;
+  T.tc = 0;   // NEXT rows decode the spectrum to fp32: the FFT forward kernels (more accurate than 3xTF32)
   T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
   T.scratch_bytes = wb;
   unsigned* mx = (unsigned*)(ws + off_max);
@@ -676,6 +729,7 @@ int tprod_destroy(tprod_handle h) {
   clear_graphs(h);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->ws) cudaFree(h->ws);
+  for (void* p : h->retired) cudaFree(p);
   delete h;
   return TPROD_OK;
 }
@@ -726,10 +780,11 @@ int tprod_f32_prepared(const float* B, float* C, int64_t n4, void* stream, tprod
 
 int tprod_release_a(tprod_handle h) {
   if (!h) return TPROD_EINVAL;
-  if (h->prep.buf) {
+  if (h->prep.buf) {                                 // synchronous by contract (include/tprod.h)
     CK(cudaSetDevice(h->device));
     CK(cudaDeviceSynchronize());
     cudaFree(h->prep.buf);
+    h->async_buf.erase(h->prep.buf);
   }
   h->prep = PreparedA();
   return TPROD_OK;
@@ -768,11 +823,12 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   const size_t off_sp = o;   o = align_up(o + 2 * (size_t)(hh * NPLANES * n * ld), 1024);
   const size_t off_re = o;   o = align_up(o + 4 * (size_t)(4 * hh * nn), 1024);  // re, im, xre, xim
   const size_t off_w = o;    o = align_up(o + (f1 ? b : 0), 1024);
-  if ((st = ensure_ws(h, o))) return st;
+  if ((st = ensure_ws(h, o, s)) || (st = poison_ws(h, o, s))) return st;
   char* ws = (char*)h->ws;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
+  T.staged = h->transform != 1;
+  T.tc = 0;   // NEXT rows decode the spectrum to fp32: the FFT forward kernels (more accurate than 3xTF32)
   T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
   T.scratch_bytes = f1 ? b : 0;
   int* flag = (int*)(ws + off_flag);
@@ -961,10 +1017,11 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   fourstep_factors(n3, &f1, &f2);
   const size_t w_bytes = f1 ? 4 * (size_t)(p * q * n3) : 0;            // four-step intermediate
   const size_t off_w = align_up(off_sp + 2 * (size_t)(hh * NPLANES * q * ld), 1024);
-  if ((st = ensure_ws(h, off_w + w_bytes))) return st;
+  if ((st = ensure_ws(h, off_w + w_bytes, s)) || (st = poison_ws(h, off_w + w_bytes, s))) return st;
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
-  T.staged = h->transform == 0;
+  T.staged = h->transform != 1;
+  T.tc = h->transform == 2;
   T.scratch = w_bytes ? (float*)((char*)h->ws + off_w) : nullptr;
   T.scratch_bytes = w_bytes;
   unsigned* mx = (unsigned*)h->ws;
@@ -1008,11 +1065,11 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       h->timing = value != 0;
       return TPROD_OK;
     case TPROD_OPT_GEMM_CLUSTER:
-      if (value < 0 || value > 3) return TPROD_EINVAL;
+      if (value < 0 || value > 4) return TPROD_EINVAL;
       h->force_cn = (int)value;
       return TPROD_OK;
     case TPROD_OPT_TRANSFORM:
-      if (value != 0 && value != 1) return TPROD_EINVAL;
+      if (value < 0 || value > 2) return TPROD_EINVAL;
       h->transform = (int)value;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:
@@ -1022,6 +1079,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
     case TPROD_OPT_GRAPHS:
       if (value != 0 && value != 1) return TPROD_EINVAL;
       h->graphs = value != 0;
+      return TPROD_OK;
+    case TPROD_OPT_POISON:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->poison = value != 0;
       return TPROD_OK;
     default:
       return TPROD_EINVAL;

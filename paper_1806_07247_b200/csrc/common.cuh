@@ -46,8 +46,9 @@ __device__ __forceinline__ float unscale_of(unsigned maxbits, int e) {
 // with c the transform's own factor (e.g. 1/n3).  urow / ucol hold 2^-e or 0 (nullptr = 1).  The
 // exponent sum is split in two multipliers so that neither leaves the fp32 range and the
 // intermediate lies between x and the result (no spurious overflow / underflow).
-__device__ __forceinline__ float2 out_scale(const float* urow, int64_t p, const float* ucol, int64_t q, float c) {
-  int F = 0;
+__device__ __forceinline__ float2 out_scale(const float* urow, int64_t p, const float* ucol, int64_t q, float c,
+                                            int extra_exp = 0) {
+  int F = extra_exp;                   // an additional exact 2^extra_exp (the tensor-core inverse's own scale)
   if (urow) {
     const float u = __ldg(urow + p);
     if (u == 0.f) return make_float2(0.f, 0.f);
@@ -58,6 +59,13 @@ __device__ __forceinline__ float2 out_scale(const float* urow, int64_t p, const 
     if (u == 0.f) return make_float2(0.f, 0.f);
     F += ((__float_as_int(u) >> 23) & 0xff) - 127;
   }
+  const int F1 = F < -100 ? -100 : (F > 100 ? 100 : F);
+  return make_float2(c * pow2f(F1), pow2f_ext(F - F1));
+}
+// out_scale from already-loaded factors ua = urow[p], ub = ucol[q] (1 where there is none).
+__device__ __forceinline__ float2 out_scale_of(float ua, float ub, float c, int extra_exp = 0) {
+  if (ua == 0.f || ub == 0.f) return make_float2(0.f, 0.f);
+  const int F = extra_exp + ((__float_as_int(ua) >> 23) & 0xff) - 127 + ((__float_as_int(ub) >> 23) & 0xff) - 127;
   const int F1 = F < -100 ? -100 : (F > 100 ? 100 : F);
   return make_float2(c * pow2f(F1), pow2f_ext(F - F1));
 }

@@ -22,6 +22,7 @@
 // Deterministic: fixed K order, no split-K, no atomics (C column j independent of n4).
 #include "internal.h"
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -33,171 +34,13 @@ namespace tprod {
 
 namespace tc {
 
+using namespace ptx;
+
 constexpr int BM = 128;
 constexpr int BK = 32;            // K elements per stage (two MMA K-steps; 64 B rows of B)
 constexpr int B_ROW = BK * 2;     // bytes per K-major B row in smem
 constexpr uint32_t B_SWZ = (BK == 32) ? 4u : 6u;   // smem-descriptor swizzle code: 64B / 32B
 constexpr CUtensorMapSwizzle B_TMA_SWZ = (BK == 32) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
-constexpr int NTHREADS = 128;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-// elected lane of a converged warp only (see mma_f16)
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(bytes)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// elected lane of a converged warp only (see mma_f16)
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                            int c1, int c2) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4, %5}], [%2];\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-// Same box, written to the same smem offset of every CTA in `mask` (and completing the mbarrier
-// at the same offset in each of them).
-__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                               int c1, int c2, uint16_t mask) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%3, %4, %5}], [%2], %6;\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-
-// Shared-memory matrix descriptor (tcgen05 "version 1"): start, leading/stride byte offsets,
-// swizzle mode in bits 61-63 (2 = 128B, 4 = 64B, 6 = 32B).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t swz) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)swz << 61;
-  return d;
-}
-
-// Instruction descriptor, kind::f16: D f32, A/B f16, A MN-major, B K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int negA) {
-  return (1u << 4)                      // c_format = F32
-         | (0u << 7) | (0u << 10)       // a_format = b_format = F16
-         | ((uint32_t)negA << 13)       // negate A
-         | (1u << 15)                   // A MN-major
-         | (0u << 16)                   // B K-major
-         | ((uint32_t)(N >> 3) << 17)   // N / 8
-         | ((uint32_t)(M >> 4) << 24);  // M / 16
-}
-
-// The single-thread tcgen05/TMA instructions below are executed by a whole converged warp and
-// predicated on `elect.sync` inside the asm: the operands stay warp-uniform, so ptxas keeps them
-// in uniform registers.  (Issuing from an `if (lane == 0)` region made ptxas wrap every UTCHMMA
-// in a uniformising loop -- ~75 cycles per MMA, slower than the 64-cycle MMA itself.)
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe, p;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-      "}\n" ::"r"(smem_u32(bar))
-      : "memory");
-}
-
-// Arrive (on completion of this thread's prior MMAs) on the mbarrier at the same offset in every
-// CTA of `mask`.
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// 16 consecutive fp32 columns of this thread's TMEM lane; caller issues tmem_wait() before use.
-__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------- kernel
 // Persistent warp-specialised kernel, 1 CTA per SM, (2 + 8) warps:
@@ -475,64 +318,14 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
 //   seg_full[b]  both CTAs'; multicast commit after the last MMA of a promoted segment
 //   seg_empty[b] leader's; all 2 x 8 epilogue warps of the pair arrive (the peer's remotely)
 // Same arithmetic, K order and epilogue as gemm_tc_kernel<128, *>: results are bitwise identical.
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// TMA load into this CTA's smem whose completion is counted on the mbarrier at shared::cluster
-// address `bar_cl` (the leader's).
-__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl, int c0,
-                                                 int c1, int c2) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4, %5}], [%2];\n"
-      "}\n" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma2_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe, p;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "@pe tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n"
-      ".reg .pred pe;\n"
-      "elect.sync _|pe, 0xffffffff;\n"
-      "@pe tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-template <int SEGKB>
+//
+// CM = 2: clusters of 2 CM = 4 CTAs, two pairs stacked along M (cluster tile 512 x 128).  Both pairs
+// need the same B tile, so CTA r of pair j loads only rows (64 / CM) j .. of its 64-row B half and
+// multicasts them to CTA r of every pair: each B-bar panel is read from L2 / DRAM once per 512 A
+// rows instead of once per 256 (the panels of a frequency do not fit the L2, so this halves the
+// GEMM's DRAM traffic on config 5).  empty[s] then counts the commits of all CM pair leaders (a
+// slot is refilled only after every pair's MMAs have read the multicast data in it).
+template <int SEGKB, int CM>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h, int nyq) {
@@ -553,19 +346,26 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   uint32_t* tmem_slot = (uint32_t*)(seg_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1, pr = crank >> 1, lead = crank & ~1u;   // role in the pair, pair, its leader
+  constexpr int BSUB = (BN / 2) / CM;               // B rows each CTA loads (and multicasts) per plane
+  constexpr uint16_t ALL = (uint16_t)((1u << (2 * CM)) - 1);
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
+  uint16_t same_role = 0;                           // CTA `rank` of every pair
+#pragma unroll
+  for (int j = 0; j < CM; ++j) same_role |= (uint16_t)(1u << (2 * j + rank));
   const int nk = (n2 + BK - 1) / BK;
   const int nseg = (nk + SEGKB - 1) / SEGKB;
-  const int mt = (n1 + 2 * BM - 1) / (2 * BM), nt = (n4 + BN - 1) / BN;
+  const int mt = (n1 + 2 * CM * BM - 1) / (2 * CM * BM), nt = (n4 + BN - 1) / BN;
   const int64_t ntiles = (int64_t)mt * nt * h;
-  const int64_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int64_t cid = blockIdx.x / (2 * CM), ncl = gridDim.x / (2 * CM);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CM);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(seg_full + b, 1);
@@ -589,16 +389,17 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   // 6 m-tiles per n sweep 180 GB -- the pairs drift apart in K by up to a tile, longer than an L2
   // residency, so no raster order recovers the reuse; the plain order stays.)
   const int64_t tpf = (int64_t)mt * nt;
-  auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {
+  auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {   // m0: this pair's first row
     f = (int)(t / tpf);
     const int r = (int)(t - (int64_t)f * tpf);
     n0 = (r % nt) * BN;
-    m0 = (r / nt) * (2 * BM);
+    m0 = (r / nt) * (2 * CM * BM) + 2 * BM * (int)pr;
   };
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer (both CTAs)
-    const uint32_t full_cl = mapa_u32(smem_u32(full), 0);      // leader's full[0]
+    const uint32_t full_cl = mapa_u32(smem_u32(full), lead);   // the pair leader's full[0]
+    const uint32_t full_mc = smem_u32(full) & 0xFEFFFFFFu;       // multicast: each destination's pair leader
     uint32_t it = 0;
     for (int64_t t = cid; t < ntiles; t += ncl) {
       int f, m0, n0;
@@ -614,20 +415,24 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         if (rank == 0) mbar_expect_tx(full + s, 2 * (STAGE / NPLANES) * np);
         const uint32_t bar = full_cl + s * 8;
         const int k0 = kb * BK;
-        const int mr = m0 + BM * (int)rank, nr = n0 + (BN / 2) * (int)rank;
+        const int mr = m0 + BM * (int)rank, nr = n0 + (BN / 2) * (int)rank + BSUB * (int)pr;
 #pragma unroll
         for (int p = 0; p < NPLANES; ++p) {
           if (p >= np) break;
           uint8_t* a = st + p * A_PLANE;
           tma_load_3d_pair(a, &tmA, bar, mr, k0, 4 * f + p);
           tma_load_3d_pair(a + BK * 128, &tmA, bar, mr + 64, k0, 4 * f + p);
-          tma_load_3d_pair(st + NPLANES * A_PLANE + p * B_PLANE, &tmB, bar, k0, nr, 4 * f + p);
+          uint8_t* bdst = st + NPLANES * A_PLANE + p * B_PLANE;
+          if (CM == 1)
+            tma_load_3d_pair(bdst, &tmB, bar, k0, nr, 4 * f + p);
+          else
+            tma_load_3d_pair_mc(bdst + BSUB * pr * B_ROW, &tmB, full_mc + s * 8, k0, nr, 4 * f + p, same_role);
         }
       }
     }
   } else if (warp == 1) {
     if (rank == 0) {
-      // -------------------------------------------------------------- MMA issuer (leader only)
+      // -------------------------------------------------------------- MMA issuer (pair leaders only)
       constexpr uint32_t ID_POS = idesc_f16(2 * BM, BN, 0);
       constexpr uint32_t ID_NEG = idesc_f16(2 * BM, BN, 1);
       uint32_t it = 0, g = 0;
@@ -673,9 +478,9 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
                 mma2_f16(tCi, a[PL_IM_LO], bd[PL_RE_HI], ID_POS, 1);
               }
             }
-            mma2_commit_mc(empty + s, (uint16_t)3);     // slot s free in both CTAs
+            mma2_commit_mc(empty + s, ALL);              // slot s read by this pair (every CTA counts CM)
           }
-          mma2_commit_mc(seg_full + b, (uint16_t)3);    // segment accumulators complete (both)
+          mma2_commit_mc(seg_full + b, pair_mask);      // segment accumulators complete (both of the pair)
         }
       }
     }
@@ -685,7 +490,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
     const int half = (warp - 2) >> 2;
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     const int64_t plane = (int64_t)n4 * ldc;
-    const uint32_t segE_cl = mapa_u32(smem_u32(seg_empty), 0);   // leader's seg_empty[0]
+    const uint32_t segE_cl = mapa_u32(smem_u32(seg_empty), lead);   // the pair leader's seg_empty[0]
     uint32_t g = 0;
     for (int64_t t = cid; t < ntiles; t += ncl) {
       int f, m0, n0t;
@@ -826,7 +631,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
-template <int SEGKB>
+template <int SEGKB, int CM>
 int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
                 int64_t n2, int64_t n4, int64_t h, int nyq, int num_sms,
                 cudaStream_t s) {
@@ -835,22 +640,36 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   constexpr int STAGES = (227 * 1024 - 2048) / STAGE;
   constexpr int SMEM = STAGES * STAGE + 1024 + 256;
   CUtensorMap mb;
-  if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN / 2,
+  if (!make_map(&mb, Bb, (uint64_t)n2, (uint64_t)n4, (uint64_t)(NPLANES * h), (uint64_t)ldb, BK, BN / 2 / CM,
                 B_TMA_SWZ))
     return 4;
-  auto kern = gemm_tc2_kernel<SEGKB>;
+  auto kern = gemm_tc2_kernel<SEGKB, CM>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess) return 4;
-  const int64_t nct = ((n1 + 2 * BM - 1) / (2 * BM)) * ((n4 + BN - 1) / BN) * h;
-  const int64_t max_cl = num_sms / 2;
-  const int grid = (int)((nct < max_cl ? nct : max_cl) * 2);
+  if (CM > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+  const int64_t nct = ((n1 + 2 * CM * BM - 1) / (2 * CM * BM)) * ((n4 + BN - 1) / BN) * h;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NTHREADS2);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = 2 * CM;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent grid: as many clusters as can be co-resident (GPC sizes need not be multiples of 2 CM)
+  int max_cl = num_sms / (2 * CM);
+  {
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3((unsigned)(2 * CM * max_cl));
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, kern, &q) == cudaSuccess && nclu > 0) max_cl = std::min(max_cl, nclu);
+    else cudaGetLastError();
+  }
+  const int grid = (int)((nct < max_cl ? nct : max_cl) * 2 * CM);
+  cfg.gridDim = dim3((unsigned)grid);
+  attr[0].val.clusterDim.x = 2 * CM;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -882,9 +701,15 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   int cn = force_cn;
   // cta_group::2 pairs: 256 x 128 tiles (enough of them to fill the SM pairs)
   const bool pair_ok = bn == 128 || force_bn == 0;
+  // 4-CTA clusters (two pairs sharing B by multicast) when A has at least 1024 rows and the 512 x 128
+  // cluster tiles still fill the GPU several times over (fewer, larger tiles would lengthen the tail)
+  if (cn == 4 || (cn == 0 && force_bn == 0 && n1 >= 1024 &&
+                  ((n1 + 511) / 512) * ((n4 + 127) / 128) * h >= 4 * (num_sms / 4))) {
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
+  }
   if (cn == 3 || (cn == 0 && force_bn == 0 && n1 > 128 &&
                   ((n1 + 255) / 256) * ((n4 + 127) / 128) * h >= num_sms / 2)) {
-    if (pair_ok) return tc::launch_pair<tc::SEG_KB>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
   }
   if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
   if (bn == 128)

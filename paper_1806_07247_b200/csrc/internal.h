@@ -23,6 +23,7 @@ struct Twiddles32 {
   int n3;
   const float2* st = nullptr;    // Stockham per-pass twiddle table (FFT path only), see transforms_fft.cu
   int staged = 1;                // 0: skip the TMA-staged / tube kernels (TPROD_OPT_TRANSFORM = 1)
+  int tc = 1;                    // tensor-core DFT-matrix kernels for n3 <= 64 (0: TPROD_OPT_TRANSFORM = 1, 2)
   // four-step long-tube forward (n3 = N1*N2 in {4096, 8192, 16384}): Stockham tables of the two
   // factors and a workspace the size of the larger operand
   const float2* st_n1 = nullptr;
@@ -124,6 +125,14 @@ void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64
                           cudaStream_t s);
 void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
                     double* X, cudaStream_t s);
+
+// Tensor-core (tcgen05) DFT-matrix transforms for 2 <= n3 <= 64 (transforms_tc.cu); false = not
+// handled (P % 4 != 0, unaligned pointers).  The inverse requires C-bar in the production layout.
+bool dft_tc_supported(int64_t n3);
+bool launch_fwd_dft_tc(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                       __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
+bool launch_inv_dft_tc(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, OutUnscale u, float* X,
+                       int num_sms, cudaStream_t s);
 
 // Register-resident dense transforms for n3 <= 64 (transforms_dense.cu); false = not handled.
 bool dense_supported(int64_t n3);

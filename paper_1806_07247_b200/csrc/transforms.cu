@@ -295,6 +295,8 @@ __global__ void fwd_split_kernel(const float* __restrict__ X, int64_t P, int64_t
 void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
                       const unsigned* maxbits, Twiddles32 tw, __half* out, int64_t ld,
                       float* unscale, int num_sms, cudaStream_t s) {
+  if (tw.staged && tw.tc && launch_fwd_dft_tc(X, P, Q, n3, role, maxbits, out, ld, unscale, num_sms, s)) return;
+  cudaGetLastError();
   if (tw.staged) {
     if (launch_fwd_tma(X, P, Q, n3, role, maxbits, out, ld, unscale, num_sms, s)) return;
     cudaGetLastError();
@@ -379,6 +381,8 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                     int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s) {
   const bool prod_layout = tw.staged && Cim == Cre + Q * ld && fstride == 2 * Q * ld;
+  if (prod_layout && tw.tc && launch_inv_dft_tc(Cre, ld, P, Q, n3, u, X, num_sms, s)) return;
+  cudaGetLastError();
   if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, u, X, num_sms, s)) return;
   cudaGetLastError();
   if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, u, X, num_sms, s)) return;

@@ -104,6 +104,10 @@ def test_sass_summary_matches_build(L):
                         v.get("UTMALDG.3D.2CTA", 0) > 0 for v in pair.values())
     single = fam("gemm_tc_kernel", got)
     assert single and all(v.get("UTCHMMA", 0) > 0 and v.get("LDTM.x16", 0) > 0 for v in single.values())
+    for name in ("fwd_dft_tc_kernel", "inv_dft_tc_kernel"):       # DFT-matrix contraction on tcgen05
+        ks = fam(name, got)
+        assert ks and all(v.get("UTCHMMA", 0) > 0 and v.get("UTMALDG.3D", 0) > 0 and v.get("LDTM.x8", 0) > 0
+                          for v in ks.values()), name
     for name in ("fwd_tube_kernel", "inv_tube_kernel"):
         ks = fam(name, got)
         assert ks and all(v.get("UTMALDG.3D", 0) > 0 and v.get("UTMASTG.3D", 0) > 0 for v in ks.values()), name

@@ -148,18 +148,21 @@ def test_simt_engine_cross_check(T):
     assert O.rel_err(C_tc, C_simt) <= TOL32
 
 
-@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (1000, 136, 3, 700), (129, 64, 7, 129)],
+@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (1000, 136, 3, 700), (129, 64, 7, 129),
+                                  (1100, 200, 8, 300), (520, 96, 5, 130)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
-    """GEMM N tile (64/128), 2-CTA A-multicast clusters and cta_group::2 CTA pairs (256-row tiles
-    across two SMs) change scheduling only: the K order of every output is fixed, so all variants
-    are bitwise identical (odd N-tile counts and a lone 128-row half-pair included)."""
+    """GEMM N tile (64/128), 2-CTA A-multicast clusters, cta_group::2 CTA pairs (256-row tiles
+    across two SMs) and 4-CTA clusters of two pairs sharing B by multicast (512-row cluster tiles)
+    change scheduling only: the K order of every output is fixed, so all variants are bitwise
+    identical (odd N-tile counts, a lone 128-row half-pair and ragged 512-row cluster tiles
+    included)."""
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 11)
     B = normal((n2, n4, n3), 12)
     ref = O.tprod_bcirc(A, B)
     outs = []
-    for bn, cn in ((64, 1), (64, 2), (128, 1), (128, 2), (128, 3), (0, 0)):
+    for bn, cn in ((64, 1), (64, 2), (128, 1), (128, 2), (128, 3), (128, 4), (0, 0)):
         h = T.Handle()
         h.set_option(T._lib.TPROD_OPT_GEMM_BN, bn)
         h.set_option(T._lib.TPROD_OPT_GEMM_CLUSTER, cn)
@@ -194,6 +197,49 @@ def test_stage_inverse_roundtrip(T, n3):
     assert np.linalg.norm(back - X) / np.linalg.norm(X) < 2e-6
 
 
+TC_N3 = [2, 3, 4, 5, 7, 8, 10, 15, 16, 17, 24, 31, 32, 33, 45, 48, 63, 64]
+
+
+@pytest.mark.parametrize("n3", TC_N3)
+def test_stage_forward_dft_tensor_core(T, n3):
+    """The tcgen05 DFT-matrix forward kernel (TPROD_OPT_TRANSFORM = 2; 2 <= n3 <= 64, P % 4 == 0;
+    the last 128-tube block ragged) vs numpy.fft.rfft for both operand roles, and vs the default
+    kernels within fp32 rounding."""
+    X = normal((132, 5, n3), 9 + n3)
+    ref = np.fft.rfft(X.astype(np.float64), axis=2)
+    htc = T.Handle()
+    htc.set_option(T._lib.TPROD_OPT_TRANSFORM, 2)
+    for role in (0, 1):
+        got = host(T.dft_f32(dev(X), role=role, handle=htc))
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err < 2e-6, (role, err)
+        old = host(T.dft_f32(dev(X), role=role))
+        assert np.linalg.norm(got - old) / np.linalg.norm(ref) < 2e-6
+
+
+@pytest.mark.parametrize("n3", TC_N3)
+def test_tprod_tensor_core_transforms(T, n3):
+    """End to end with the tcgen05 forward and inverse DFT kernels (TPROD_OPT_TRANSFORM = 2; n1, n2 %
+    4 == 0 so both operands and C take them), rows of A spread over 2^-20 .. 2^20 (per-tube scales in
+    the inverse): vs the oracle, and the default kernels too."""
+    n1, n2, n4 = 260, 48, 36
+    rng = np.random.default_rng(n3)
+    A = normal((n1, n2, n3), 19 + n3).astype(np.float64) * np.exp2(rng.integers(-20, 21, size=n1)).reshape(n1, 1, 1)
+    A = A.astype(np.float32)
+    B = normal((n2, n4, n3), 29 + n3)
+    ref = O.tprod_alg1(A.astype(np.float64), B.astype(np.float64)).real
+    h2 = T.Handle()
+    h2.set_option(T._lib.TPROD_OPT_TRANSFORM, 2)
+    C = gpu_tprod(T, A, B, handle=h2)
+    C2 = gpu_tprod(T, A, B)
+    ra = np.abs(A).max(axis=(1, 2))
+    for i in range(0, n1, 7):                           # every row to its own scale (R18)
+        num = np.linalg.norm(C[i] - ref[i])
+        assert num <= 1e-5 * ra[i] * np.abs(B).max() * np.sqrt(n2 * n3 * n4), (i, num)
+    assert O.rel_err(C, ref) <= TOL32
+    assert O.rel_err(C2, ref) <= TOL32
+
+
 @pytest.mark.parametrize("n3", [64, 128, 256])
 def test_tube_transforms_match_register_kernels(T, n3):
     """The TMA-staged tube-parallel Stockham kernels (picked for aligned shapes) and the register /
@@ -212,7 +258,8 @@ def test_tube_transforms_match_register_kernels(T, n3):
     assert O.rel_err(C0, C1) <= 1e-6
 
 
-@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (256, 128, 64, 96), (64, 40, 100, 24), (7, 5, 2, 3)],
+@pytest.mark.parametrize("dims", [(300, 260, 31, 200), (256, 128, 64, 96), (64, 40, 100, 24), (7, 5, 2, 3),
+                                  (16, 12, 4096, 8)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_prepared_operand_bitwise(T, dims):
     """NEXT-1 prepared left operand: tprod_prepare_a_f32 once, tprod_f32_prepared for several B --
