@@ -121,8 +121,92 @@ __global__ void gemm_simt_f64_kernel(const double* __restrict__ Ab, int64_t lda,
   }
 }
 
+// Register-tiled fp64 complex GEMM (the fp64 path's K2): a 64 x 64 output tile per CTA of 16 x 16
+// threads, each thread 4 x 4 outputs (rows tx + 16 a, columns ty + 16 b: conflict-free shared
+// reads), K blocks of 16 staged in shared memory (A as [l][i], B transposed to [l][j]), complex 4M
+// with fp64 FMAs: 64 DFMA per 16 shared loads.  Same K order for every output (deterministic).
+constexpr int T64 = 64, KB64 = 16;
+__global__ void __launch_bounds__(256) gemm_f64_tiled_kernel(const double* __restrict__ Ab, int64_t lda,
+                                                             const double* __restrict__ Bb, int64_t ldb,
+                                                             double* __restrict__ Cb, int64_t ldc, int n1, int n2,
+                                                             int n4) {
+  __shared__ double sA[2][KB64][T64];
+  __shared__ double sB[2][KB64][T64 + 1];
+  const int f = blockIdx.z;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.x * T64, j0 = blockIdx.y * T64;
+  const int64_t pa = (int64_t)n2 * lda, pb = (int64_t)n4 * ldb;
+  const double* A0 = Ab + (int64_t)(2 * f) * pa;
+  const double* B0 = Bb + (int64_t)(2 * f) * pb;
+  double cr[4][4], ci[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cr[a][b] = ci[a][b] = 0.0;
+  for (int l0 = 0; l0 < n2; l0 += KB64) {
+    // A tile: KB64 rows l x 64 columns i (coalesced along i); B tile: 64 rows j x KB64 l (coalesced
+    // along l), stored transposed
+#pragma unroll
+    for (int r = 0; r < (KB64 * T64) / 256; ++r) {
+      const int e = threadIdx.x + 256 * r;
+      const int ii = e % T64, l = e / T64;
+      const bool ok = l0 + l < n2 && i0 + ii < n1;
+      const int64_t o = (int64_t)(l0 + l) * lda + i0 + ii;
+      sA[0][l][ii] = ok ? A0[o] : 0.0;
+      sA[1][l][ii] = ok ? A0[pa + o] : 0.0;
+      const int ll = e % KB64, jj = e / KB64;
+      const bool okb = l0 + ll < n2 && j0 + jj < n4;
+      const int64_t ob = (int64_t)(j0 + jj) * ldb + l0 + ll;
+      sB[0][ll][jj] = okb ? B0[ob] : 0.0;
+      sB[1][ll][jj] = okb ? B0[pb + ob] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < KB64; ++kk) {
+      double ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ar[a] = sA[0][kk][tx + 16 * a];
+        ai[a] = sA[1][kk][tx + 16 * a];
+        br[a] = sB[0][kk][ty + 16 * a];
+        bi[a] = sB[1][kk][ty + 16 * a];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          cr[a][b] = fma(ar[a], br[b], cr[a][b]);
+          cr[a][b] = fma(-ai[a], bi[b], cr[a][b]);
+          ci[a][b] = fma(ar[a], bi[b], ci[a][b]);
+          ci[a][b] = fma(ai[a], br[b], ci[a][b]);
+        }
+    }
+    __syncthreads();
+  }
+  const int64_t pc = (int64_t)n4 * ldc;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int j = j0 + ty + 16 * b;
+    if (j >= n4) continue;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = i0 + tx + 16 * a;
+      if (i < n1) {
+        const int64_t o = (int64_t)j * ldc + i;
+        Cb[(int64_t)(2 * f) * pc + o] = cr[a][b];
+        Cb[(int64_t)(2 * f + 1) * pc + o] = ci[a][b];
+      }
+    }
+  }
+}
+
 void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64_t ldb, double* Cb,
                           int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, cudaStream_t s) {
+  if (n1 * n4 >= 64 * 64) {                          // register-tiled kernel once a tile is mostly full
+    dim3 g((unsigned)((n1 + T64 - 1) / T64), (unsigned)((n4 + T64 - 1) / T64), (unsigned)h);
+    gemm_f64_tiled_kernel<<<g, 256, 0, s>>>(Ab, lda, Bb, ldb, Cb, ldc, (int)n1, (int)n2, (int)n4);
+    return;
+  }
   dim3 grid((unsigned)((n1 + TS - 1) / TS), (unsigned)((n4 + TS - 1) / TS), (unsigned)h);
   gemm_simt_f64_kernel<<<grid, dim3(TS, TS), 0, s>>>(Ab, lda, Bb, ldb, Cb, ldc, (int)n1, (int)n2,
                                                     (int)n4);

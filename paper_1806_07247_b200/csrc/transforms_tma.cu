@@ -21,6 +21,7 @@
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <mutex>
 #include <algorithm>
 #include <vector>
@@ -502,7 +503,7 @@ template <int N1, int TUB, int ROLE>
 __global__ void __launch_bounds__(2 * TUB) fwd4_pass2_kernel(const __grid_constant__ CUtensorMap mW4, int64_t P,
                                                             int64_t Q, int N2, const unsigned* __restrict__ maxbits,
                                                             const float2* __restrict__ st1, __half* __restrict__ out,
-                                                            int64_t ld, float* __restrict__ unscale) {
+                                                            int64_t ld, int64_t plane, float* __restrict__ unscale) {
   constexpr int F = TUB / 2, NT = 2 * TUB;
   extern __shared__ __align__(128) float smem[];
   __shared__ uint64_t full;
@@ -517,7 +518,6 @@ __global__ void __launch_bounds__(2 * TUB) fwd4_pass2_kernel(const __grid_consta
   const int64_t pblocks = (P + TUB - 1) / TUB;
   const int half = N2 / 2;
   const int64_t items = pblocks * Q * (half + 1);
-  const int64_t plane = Q * ld;
   const int c = threadIdx.x % F;                                // NT % F == 0
   uint32_t ph = 0;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x, ph ^= 1) {
@@ -914,12 +914,14 @@ bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const
 
 // 4-D fp32 view {P, Q, N1, N2} of a Matlab-layout P x Q x (N1 N2) tensor (row k1 + N1 k2), box
 // {TUB, 1, b2, b3}
+// (Qs = the tensor's full lateral size for the strides, Q = the lateral slices of this view)
 bool map_f32_4d(CUtensorMap* m, const void* base, uint64_t P, uint64_t Q, uint64_t N1, uint64_t N2, uint32_t tub,
-                uint32_t b2, uint32_t b3) {
+                uint32_t b2, uint32_t b3, uint64_t Qs = 0) {
   auto fn = encode();
+  if (!Qs) Qs = Q;
   if (!fn || (P * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0) return false;
   cuuint64_t dims[4] = {P, Q, N1, N2};
-  cuuint64_t strides[3] = {P * 4, P * Q * 4, P * Q * N1 * 4};
+  cuuint64_t strides[3] = {P * 4, P * Qs * 4, P * Qs * N1 * 4};
   cuuint32_t box[4] = {tub, 1, b2, b3};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, es,
@@ -927,13 +929,26 @@ bool map_f32_4d(CUtensorMap* m, const void* base, uint64_t P, uint64_t Q, uint64
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Lateral-slice chunks of a four-step transform (measurement knob): with TPROD_4STEP_L2_MB = m > 0
+// the passes run chunk by chunk so that a chunk's intermediate (4 P Qc n3 bytes <= m MB) could stay
+// in L2 until pass 2 reads it.  Measured on config 4 (K1 + K3): one chunk 0.203 ms, 40 MB chunks
+// 0.240 ms, 24 MB chunks 0.275 ms -- the smaller grids per launch cost more than the DRAM re-read of
+// the intermediate saves -- so the default is one chunk.
+int64_t fourstep_chunk(int64_t P, int64_t Q, int64_t n3) {
+  static const int64_t budget = [] {
+    const char* e = getenv("TPROD_4STEP_L2_MB");
+    return (int64_t)(e ? atoi(e) : 0) << 20;
+  }();
+  if (budget <= 0) return Q;
+  const int64_t per_q = 4 * P * n3;
+  const int64_t qmax = std::max<int64_t>(1, budget / per_q);
+  const int64_t nch = (Q + qmax - 1) / qmax;
+  return (Q + nch - 1) / nch;
+}
+
 template <int N1, int N2, int TUB>
 bool launch_fwd4_t(const float* X, int64_t P, int64_t Q, int role, const unsigned* maxbits, const Twiddles32& tw,
                    __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
-  CUtensorMap mx, mw1, mw2;
-  if (!map_f32_4d(&mx, X, P, Q, N1, N2, TUB, 1, N2) || !map_f32_4d(&mw1, tw.scratch, P, Q, N1, N2, TUB, 1, N2) ||
-      !map_f32_4d(&mw2, tw.scratch, P, Q, N1, N2, TUB, N1, 1))
-    return false;
   const void* k1 = (const void*)fwd4_pass1_kernel<N2, TUB>;
   const void* k2 = role == 0 ? (const void*)fwd4_pass2_kernel<N1, TUB, 0> : (const void*)fwd4_pass2_kernel<N1, TUB, 1>;
   const size_t sm1 = sizeof(float) * TUB * N2, sm2 = 2 * sizeof(float) * TUB * N1;
@@ -944,29 +959,44 @@ bool launch_fwd4_t(const float* X, int64_t P, int64_t Q, int role, const unsigne
   int per1 = 1, per2 = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, 2 * TUB, sm1);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k2, 2 * TUB, sm2);
-  const int64_t it1 = pblocks * Q * N1, it2 = pblocks * Q * (N2 / 2 + 1);
-  const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
-  const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
-  int n1i = N1, n2i = N2;
-  const float2* st1 = tw.st_n1;
-  const float2* st2 = tw.st_n2;
-  const float2* twn = tw.tw;
-  const unsigned* rowmax = role == 0 ? maxbits : nullptr;   // A: row scales applied in pass 1
-  void* a1[] = {(void*)&mx, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn, (void*)&rowmax};
-  if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
-  void* a2[] = {(void*)&mw2, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&maxbits, (void*)&st1, (void*)&out, (void*)&ld,
-                (void*)&unscale};
-  return cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) == cudaSuccess;
+  const int64_t Qc = fourstep_chunk(P, Q, (int64_t)N1 * N2);
+  const int64_t plane = Q * ld;
+  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+    int64_t Qi = std::min(Qc, Q - q0);
+    CUtensorMap mx, mw1, mw2;
+    if (!map_f32_4d(&mx, X + P * q0, P, Qi, N1, N2, TUB, 1, N2, Q) ||
+        !map_f32_4d(&mw1, tw.scratch, P, Qi, N1, N2, TUB, 1, N2) || !map_f32_4d(&mw2, tw.scratch, P, Qi, N1, N2, TUB, N1, 1))
+      return false;
+    const int64_t it1 = pblocks * Qi * N1, it2 = pblocks * Qi * (N2 / 2 + 1);
+    const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
+    const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
+    int n1i = N1, n2i = N2;
+    const float2* st1 = tw.st_n1;
+    const float2* st2 = tw.st_n2;
+    const float2* twn = tw.tw;
+    const unsigned* rowmax = role == 0 ? maxbits : nullptr;   // A: row scales applied in pass 1
+    // B (role 1): the column maxima / unscale factors of this chunk's lateral slices
+    const unsigned* mb = role == 0 ? maxbits : maxbits + q0;
+    float* us = role == 0 ? unscale : unscale + q0;
+    __half* o = out + q0 * ld;
+    void* a1[] = {(void*)&mx, (void*)&mw1, (void*)&P, (void*)&Qi, (void*)&n1i, (void*)&st2, (void*)&twn, (void*)&rowmax};
+    if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
+    void* a2[] = {(void*)&mw2, (void*)&P, (void*)&Qi, (void*)&n2i, (void*)&mb, (void*)&st1, (void*)&o, (void*)&ld,
+                  (void*)&plane, (void*)&us};
+    if (cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) != cudaSuccess) return false;
+  }
+  return true;
 }
 
 // 5-D fp32 view {P (pitch ld), Q, 2, N1, R2} of C-bar planes [f][re|im][q][ld] with f = f1 + N1 f2,
 // box {tub, 1, 2, 1, R2}
 bool map_cbar_5d(CUtensorMap* m, const void* base, uint64_t P, uint64_t ld, uint64_t Q, uint64_t N1, uint64_t R2,
-                 uint32_t tub) {
+                 uint32_t tub, uint64_t Qs = 0) {
   auto fn = encode();
+  if (!Qs) Qs = Q;
   if (!fn || (ld * 4) % 16 != 0 || ((uintptr_t)base & 15) != 0) return false;
   cuuint64_t dims[5] = {P, Q, 2, N1, R2};
-  cuuint64_t strides[4] = {ld * 4, ld * Q * 4, 2 * ld * Q * 4, 2 * N1 * ld * Q * 4};
+  cuuint64_t strides[4] = {ld * 4, ld * Qs * 4, 2 * ld * Qs * 4, 2 * N1 * ld * Qs * 4};
   cuuint32_t box[5] = {tub, 1, 2, 1, (cuuint32_t)R2};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(base), dims, strides, box, es,
@@ -977,12 +1007,6 @@ bool map_cbar_5d(CUtensorMap* m, const void* base, uint64_t P, uint64_t ld, uint
 template <int N1, int N2, int TUB>
 bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twiddles32& tw, OutUnscale u, float* X,
                    int num_sms, cudaStream_t s) {
-  CUtensorMap mc, mw1, mw2, mx;
-  if (!map_cbar_5d(&mc, Cre, P, ld, Q, N1, N2 / 2 + 1, TUB) ||
-      !map_f32_4d(&mw1, tw.scratch, P, Q, N1, N2, TUB, 1, N2) ||
-      !map_f32_4d(&mw2, tw.scratch, P, Q, N1, N2, TUB, N1, 1) ||
-      !map_f32_4d(&mx, X, P, Q, N2, N1, TUB, 1, N1))
-    return false;
   const void* k1 = (const void*)inv4_pass1_kernel<N2, TUB>;
   const void* k2 = (const void*)inv4_pass2_kernel<N1, TUB>;
   const size_t sm1 = sizeof(float) * (2 * (N2 / 2 + 1) * 2 * TUB + 2 * TUB * N2), sm2 = sizeof(float) * TUB * N1;
@@ -993,17 +1017,29 @@ bool launch_inv4_t(const float* Cre, int64_t ld, int64_t P, int64_t Q, const Twi
   int per1 = 1, per2 = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k1, 2 * TUB, sm1);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k2, 2 * TUB, sm2);
-  const int64_t it1 = pblocks * Q * (N1 / 2 + 1), it2 = pblocks * Q * N2;
-  const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
-  const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
-  int n1i = N1, n2i = N2;
-  const float2* st1 = tw.st_n1;
-  const float2* st2 = tw.st_n2;
-  const float2* twn = tw.tw;
-  void* a1[] = {(void*)&mc, (void*)&mw1, (void*)&P, (void*)&Q, (void*)&n1i, (void*)&st2, (void*)&twn};
-  if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
-  void* a2[] = {(void*)&mw2, (void*)&mx, (void*)&P, (void*)&Q, (void*)&n2i, (void*)&st1, (void*)&u};
-  return cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) == cudaSuccess;
+  const int64_t Qc = fourstep_chunk(P, Q, (int64_t)N1 * N2);
+  for (int64_t q0 = 0; q0 < Q; q0 += Qc) {
+    int64_t Qi = std::min(Qc, Q - q0);
+    CUtensorMap mc, mw1, mw2, mx;
+    if (!map_cbar_5d(&mc, Cre + q0 * ld, P, ld, Qi, N1, N2 / 2 + 1, TUB, Q) ||
+        !map_f32_4d(&mw1, tw.scratch, P, Qi, N1, N2, TUB, 1, N2) ||
+        !map_f32_4d(&mw2, tw.scratch, P, Qi, N1, N2, TUB, N1, 1) ||
+        !map_f32_4d(&mx, X + P * q0, P, Qi, N2, N1, TUB, 1, N1, Q))
+      return false;
+    const int64_t it1 = pblocks * Qi * (N1 / 2 + 1), it2 = pblocks * Qi * N2;
+    const int g1 = (int)std::min<int64_t>(it1, (int64_t)num_sms * std::max(per1, 1));
+    const int g2 = (int)std::min<int64_t>(it2, (int64_t)num_sms * std::max(per2, 1));
+    int n1i = N1, n2i = N2;
+    const float2* st1 = tw.st_n1;
+    const float2* st2 = tw.st_n2;
+    const float2* twn = tw.tw;
+    OutUnscale uc{u.row, u.col ? u.col + q0 : nullptr};
+    void* a1[] = {(void*)&mc, (void*)&mw1, (void*)&P, (void*)&Qi, (void*)&n1i, (void*)&st2, (void*)&twn};
+    if (cudaLaunchKernel(k1, dim3(g1), dim3(2 * TUB), a1, sm1, s) != cudaSuccess) return false;
+    void* a2[] = {(void*)&mw2, (void*)&mx, (void*)&P, (void*)&Qi, (void*)&n2i, (void*)&st1, (void*)&uc};
+    if (cudaLaunchKernel(k2, dim3(g2), dim3(2 * TUB), a2, sm2, s) != cudaSuccess) return false;
+  }
+  return true;
 }
 }  // namespace
 

@@ -105,11 +105,13 @@ def test_sweep_fp64(T, dims):
     assert O.rel_err(gpu_tprod(T, A, B), O.tprod_bcirc(A, B)) <= TOL64
 
 
-@pytest.mark.parametrize("dims", [(24, 20, 32, 16), (17, 33, 64, 9), (40, 24, 100, 20), (6, 5, 4096, 4)],
+@pytest.mark.parametrize("dims", [(24, 20, 32, 16), (17, 33, 64, 9), (40, 24, 100, 20), (6, 5, 4096, 4),
+                                  (130, 70, 9, 100), (256, 96, 31, 200)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_fp64_longer_tubes(T, dims):
     """fp64 path beyond the sweep's n3 <= 31: power-of-two, 5-smooth and long tubes (n3 = 4096's
-    twiddle table no longer fits the default 48 KB of shared memory) vs the oracle at 1e-12."""
+    twiddle table no longer fits the default 48 KB of shared memory), and slices large enough for the
+    register-tiled fp64 GEMM (ragged 64 x 64 tiles) vs the oracle at 1e-12."""
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 500 + n3, np.float64)
     B = normal((n2, n4, n3), 600 + n3, np.float64)
