@@ -200,8 +200,9 @@ enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_
  * one CUDA graph (captured on a private stream at the second call, launched on the caller's
  * stream); 0 = always launch kernel by kernel.  Identical kernels and results either way; the
  * graph only removes per-kernel host work and launch gaps.  Bypassed while TPROD_OPT_TIMING is on
- * (stage events between direct launches) and when the caller's stream is being captured.  The handle keeps at most 64 graphs (all are
- * dropped, after a device synchronisation, when a 65th key arrives or the workspace grows). */
+ * (stage events between direct launches) and when the caller's stream is being captured.  The
+ * handle keeps at most 64 graphs (all are dropped when a 65th key arrives or the workspace grows;
+ * an executable graph still in flight is released by the driver when it completes). */
 /* TPROD_OPT_TRANSFORM (fp32 path): 0 = auto (the TMA-staged / tube-parallel / four-step transform
  * kernels where they apply, else the register-resident / mixed-radix / generic ones), 1 =
  * register-resident and generic transform kernels only, 2 = for 2 <= n3 <= 64 the tensor-core
