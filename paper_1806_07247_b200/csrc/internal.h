@@ -146,6 +146,9 @@ bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fs
 // (transforms_fft.cu).
 // `st` is the Stockham table of host_stockham_table (device copy).
 bool fft_supported(int64_t n3);
+// Not 5-smooth 64 < n3 <= 8192: Bluestein's chirp-z through a 5-smooth FFT of length >= 2 n3 - 1
+// (launch_fwd_fft / launch_inv_fft take that route themselves; `st` may then be null).
+bool bluestein_supported(int64_t n3);
 bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                     const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s);
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,

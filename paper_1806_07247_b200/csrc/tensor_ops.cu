@@ -352,8 +352,16 @@ __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float*
         // fp64 divisions / square roots are slow: the angle comes from fp32 estimates (an approximate
         // Jacobi angle still converges), and the quantities that must be exact to fp64 -- the unit
         // phase e and the rotation's c^2 + s^2 = 1 -- get one Newton step of rsqrt in fp64
-        float ig32 = rsqrtf((float)g2);
-        const double ig = (double)ig32 * (1.5 - 0.5 * g2 * (double)ig32 * (double)ig32);   // 1 / |g|
+        // (below ~1e-36 the fp32 estimate of g2 is subnormal and rsqrtf loses all accuracy -- measured
+        // |e|^2 - 1 = -0.14 on a rank-deficient slice, which broke V's orthonormality -- so those rare
+        // pairs take the exact fp64 route)
+        double ig;
+        if (g2 > 1e-36) {
+          const float ig32 = rsqrtf((float)g2);
+          ig = (double)ig32 * (1.5 - 0.5 * g2 * (double)ig32 * (double)ig32);   // 1 / |g|
+        } else {
+          ig = 1.0 / sqrt(g2);
+        }
         const float zeta = (float)((be - al) * 0.5 * ig);
         const float t32 = copysignf(1.f, zeta) / (fabsf(zeta) + sqrtf(1.f + zeta * zeta));
         const double t = t32, t2p1 = 1.0 + t * t;
@@ -390,6 +398,25 @@ __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float*
 #ifdef TPROD_SVT_DEBUG
   if (tid == 0 && f < 2) printf("svt f=%d m=%d n=%d G=%d sweeps=%d cycles=%lld\n", f, m, n, G, nsweeps, clock64() - t0);
 #endif
+#ifdef TPROD_SVT_DEBUG
+  __syncthreads();
+  if (tid == 0 && want_v && f < 2) {
+    double dev = 0.0, imx = 0.0;
+    for (int p = 0; p < n; ++p)
+      for (int q = 0; q < n; ++q) {
+        double gr = 0.0, gi = 0.0;
+        for (int i = 0; i < n; ++i) {
+          const double2 x = v[p * n + i], y = v[q * n + i];
+          gr += x.x * y.x + x.y * y.y;
+          gi += x.x * y.y - x.y * y.x;
+          imx = fmax(imx, fabs(x.y));
+        }
+        dev = fmax(dev, fabs(gr - (p == q ? 1.0 : 0.0)) + fabs(gi));
+      }
+    printf("svd f=%d tr=%d m=%d n=%d |V^H V - I|=%g max|Im V|=%g\n", f, (int)tr, m, n, dev, imx);
+  }
+  __syncthreads();
+#endif
   // sigma_j = ||(A V)_j||, weights (1 - tau / sigma_j)_+
   for (int j = warp; j < n; j += nw) {
     double ss = 0.0;
@@ -420,12 +447,54 @@ __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float*
     const int r = n;                                     // n = min(M, N) after the swap
     const int64_t uo = (int64_t)f * M * r, vo = (int64_t)f * N * r, so = (int64_t)f * r * r;
     for (int idx = tid; idx < r * r; idx += blockDim.x) fo.sre[so + idx] = 0.f;
+    // Left vectors (A V)_j / sigma_j, normalised in place.  A column whose sigma is at the rounding
+    // level of the slice (rank-deficient input) has no reliable direction: it is replaced by a unit
+    // vector Gram-Schmidt-orthogonalised (twice) against the other columns, so the factor keeps
+    // orthonormal columns (Theorem 2.2: U^* U = I) while A = U S V^* still holds to that level.
+    double smax = 0.0;
+    for (int k = 0; k < n; ++k) smax = fmax(smax, wgt[k]);
+    const double thr = smax * 1e-6;
+    for (int idx = tid; idx < m * n; idx += blockDim.x) {
+      const int j = idx / m;
+      const double sg = wgt[j];
+      const double inv = sg > thr ? 1.0 / sg : 0.0;
+      a[idx] = make_double2(a[idx].x * inv, a[idx].y * inv);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < n; ++j) {
+        if (wgt[j] > thr) continue;
+        for (int e = 0; e < m; ++e) {                    // try e_0, e_1, ... until one survives
+          double2* x = a + j * m;
+          for (int i = 0; i < m; ++i) x[i] = make_double2(i == e ? 1.0 : 0.0, 0.0);
+          for (int pass = 0; pass < 2; ++pass)
+            for (int k = 0; k < n; ++k) {
+              if (k == j) continue;
+              const double2* y = a + k * m;              // (zero columns still pending contribute nothing)
+              double pr = 0.0, pi = 0.0;                 // <y, x> = y^H x
+              for (int i = 0; i < m; ++i) {
+                pr += y[i].x * x[i].x + y[i].y * x[i].y;
+                pi += y[i].x * x[i].y - y[i].y * x[i].x;
+              }
+              for (int i = 0; i < m; ++i)
+                x[i] = make_double2(x[i].x - (pr * y[i].x - pi * y[i].y), x[i].y - (pr * y[i].y + pi * y[i].x));
+            }
+          double nn = 0.0;
+          for (int i = 0; i < m; ++i) nn += x[i].x * x[i].x + x[i].y * x[i].y;
+          if (nn > 0.25) {
+            const double inv = 1.0 / sqrt(nn);
+            for (int i = 0; i < m; ++i) x[i] = make_double2(x[i].x * inv, x[i].y * inv);
+            break;
+          }
+        }
+      }
+    }
     __syncthreads();
     for (int j = tid; j < n; j += blockDim.x) {
       int pos = 0;
       for (int k = 0; k < n; ++k) pos += (wgt[k] > wgt[j]) || (wgt[k] == wgt[j] && k < j);
       const double sg = wgt[j];
-      const double inv = sg > 0.0 ? 1.0 / sg : 0.0;
+      const double inv = 1.0;                            // columns already normalised above
       fo.sre[so + (int64_t)pos * r + pos] = (float)sg;
       // left vectors: length m (rows of the processed matrix), right: length n
       float* lre = tr ? fo.vre + vo : fo.ure + uo;        // left vectors of the processed matrix

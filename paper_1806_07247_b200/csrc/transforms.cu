@@ -306,7 +306,10 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
   if (tw.staged && launch_fwd_4step(X, P, Q, n3, role, maxbits, tw, out, ld, unscale, num_sms, s)) return;
   cudaGetLastError();
-  if (tw.st && launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
+  // 5-smooth n3 > 64: mixed-radix FFT (the handle's Stockham table); otherwise Bluestein's chirp-z
+  // through a 5-smooth length (its own tables); both return false for n3 <= 64
+  if (launch_fwd_fft(X, P, Q, n3, role, maxbits, tw.st, out, ld, unscale, s)) return;
+  cudaGetLastError();
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   int h = (int)h_slices(n3);
@@ -388,7 +391,8 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, u, X, num_sms, s)) return;
   cudaGetLastError();
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, u, X, s)) return;
-  if (tw.st && launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, u, X, s)) return;
+  if (launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, u, X, s)) return;
+  cudaGetLastError();
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   const size_t smem = tw_smem_bytes((const void*)inv_kernel<float, float2>, sizeof(float2) * (size_t)n3);

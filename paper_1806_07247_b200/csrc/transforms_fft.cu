@@ -25,6 +25,10 @@
 #include "common.cuh"
 #include "fft_reg.cuh"
 
+#include <complex>
+#include <map>
+#include <math.h>
+#include <mutex>
 #include <vector>
 
 namespace tprod {
@@ -176,14 +180,77 @@ __device__ void fft_smem(float2* z, int N, int F, int Np, const FftPlan& pl, con
   }
 }
 
+// Bluestein's chirp-z transform (for n3 that are not 5-smooth): the length-N DFT of each of the F
+// buffers, Z_f = sum_k z_k w^{fk} (w = e^{-2 pi i/N}), through one length-M (5-smooth, M >= 2N - 1)
+// cyclic convolution:  w^{fk} = c_f c_k / c_{f-k} with the chirp c_k = e^{-pi i k^2 / N}, so
+//   Z_f = c_f sum_k (z_k c_k) b_{f-k},   b_m = e^{+pi i m^2 / N} = conj(c_m)
+// and the sum is IFFT_M(FFT_M(z c) . FFT_M(b)) with b wrapped cyclically (bh = FFT_M(b) / M is
+// precomputed in fp64).  In / out: z_k, k < N, at pad(k) of each buffer (stride Np >= padded M).
+template <int NT>
+__device__ void bluestein(float2* z, int N, int M, int F, int Np, const FftPlan& pl, const float2* __restrict__ st,
+                          const float2* __restrict__ chirp, const float2* __restrict__ bh) {
+  for (int idx = threadIdx.x; idx < F * M; idx += NT) {
+    const int c = idx / M, k = idx - c * M;
+    float2* e = z + c * Np + pad(k);
+    *e = k < N ? cmul(*e, __ldg(chirp + k)) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  fft_smem<-1, NT>(z, M, F, Np, pl, st);
+  for (int idx = threadIdx.x; idx < F * M; idx += NT) {
+    const int c = idx / M, k = idx - c * M;
+    float2* e = z + c * Np + pad(k);
+    *e = cmul(*e, __ldg(bh + k));
+  }
+  __syncthreads();
+  fft_smem<+1, NT>(z, M, F, Np, pl, st);
+  for (int idx = threadIdx.x; idx < F * N; idx += NT) {
+    const int c = idx / N, f = idx - c * N;
+    float2* e = z + c * Np + pad(f);
+    *e = cmul(*e, __ldg(chirp + f));
+  }
+  __syncthreads();
+}
+
+// Plan of one transform length: the FFT itself (M = 0) or Bluestein of length N through a
+// length-M FFT (pl / st then describe M).
+struct FftJob {
+  int M;
+  const float2* chirp;
+  const float2* bh;
+};
+
+template <int DIR, int NT>
+__device__ void fft_core(float2* z, int N, int F, int Np, const FftPlan& pl, const float2* __restrict__ st,
+                         const FftJob& job) {
+  if (!job.M) {
+    fft_smem<DIR, NT>(z, N, F, Np, pl, st);
+    return;
+  }
+  if (DIR < 0) {
+    bluestein<NT>(z, N, job.M, F, Np, pl, st, job.chirp, job.bh);
+  } else {                                            // inverse DFT = conj(DFT(conj z))
+    for (int idx = threadIdx.x; idx < F * N; idx += NT) {
+      float2* e = z + (idx / N) * Np + pad(idx % N);
+      e->y = -e->y;
+    }
+    __syncthreads();
+    bluestein<NT>(z, N, job.M, F, Np, pl, st, job.chirp, job.bh);
+    for (int idx = threadIdx.x; idx < F * N; idx += NT) {
+      float2* e = z + (idx / N) * Np + pad(idx % N);
+      e->y = -e->y;
+    }
+    __syncthreads();
+  }
+}
+
 template <int ROLE>
 __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
     const float* __restrict__ X, int64_t P, int64_t Q, int N, int F, const __grid_constant__ FftPlan pl,
     const unsigned* __restrict__ maxbits, const float2* __restrict__ st, __half* __restrict__ out,
-    int64_t ld, float* __restrict__ unscale, int vec) {
+    int64_t ld, float* __restrict__ unscale, int vec, FftJob job) {
   extern __shared__ float2 z[];
   const int TUB = 2 * F;
-  const int Np = bstride(N, F);
+  const int Np = bstride(job.M ? job.M : N, F);
   const int64_t pblocks = (P + TUB - 1) / TUB;
   const int64_t q = blockIdx.x / pblocks;
   const int64_t p0 = (blockIdx.x - q * pblocks) * TUB;
@@ -224,7 +291,7 @@ __global__ void __launch_bounds__(FFT_THREADS, 1) fft_fwd_split_kernel(
     }
   }
   __syncthreads();
-  fft_smem<-1, FFT_THREADS>(z, N, F, Np, pl, st);
+  fft_core<-1, FFT_THREADS>(z, N, F, Np, pl, st, job);
   // ---- Hermitian half, real-pair separation, 2^e scaling, fp16 hi/lo split
   const int H = N / 2 + 1;
   const int64_t plane = Q * ld;
@@ -286,11 +353,11 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
                                                                  int64_t fstride, int64_t P, int64_t Q,
                                                                  int N, int F, const __grid_constant__ FftPlan pl,
                                                                  const float2* __restrict__ st, OutUnscale u,
-                                                                 float* __restrict__ X, int vec) {
+                                                                 float* __restrict__ X, int vec, FftJob job) {
   extern __shared__ float2 z[];
   __shared__ float2 ssc[2 * (FFT_POINTS / 64)];   // per-tube output scale (1/N and R18), TUB <= 256
   const int TUB = 2 * F;
-  const int Np = bstride(N, F);
+  const int Np = bstride(job.M ? job.M : N, F);
   const int64_t pblocks = (P + TUB - 1) / TUB;
   const int64_t q = blockIdx.x / pblocks;
   const int64_t p0 = (blockIdx.x - q * pblocks) * TUB;
@@ -317,7 +384,7 @@ __global__ void __launch_bounds__(IFFT_THREADS, 1) fft_inv_kernel(const float* _
   for (int t = threadIdx.x; t < TUB; t += IFFT_THREADS)
     ssc[t] = p0 + t < P ? out_scale(u.row, p0 + t, u.col, q, 1.f / (float)N) : make_float2(0.f, 0.f);
   __syncthreads();
-  fft_smem<+1, IFFT_THREADS>(z, N, F, Np, pl, st);
+  fft_core<+1, IFFT_THREADS>(z, N, F, Np, pl, st, job);
   const int64_t PQ = P * Q;
   float* xo = X + P * q + p0;
   if (vec && (TUB % 4) == 0 && p0 + TUB <= P && (P % 4) == 0 && (((uintptr_t)X) & 15) == 0) {
@@ -381,42 +448,157 @@ bool fft_supported(int64_t n3) {
   return n3 > 64 && n3 <= FFT_POINTS && make_plan((int)n3, &pl);
 }
 
-bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
-                    const float2* st, __half* out, int64_t ld, float* unscale, cudaStream_t s) {
-  if (!fft_supported(n3)) return false;
+namespace {
+
+// Smallest 5-smooth M >= 2 n - 1 (the Bluestein convolution length), 0 if above FFT_POINTS.
+int bluestein_len(int n) {
+  for (int m = 2 * n - 1; m <= FFT_POINTS; ++m) {
+    FftPlan pl;
+    if (make_plan(m, &pl)) return m;
+  }
+  return 0;
+}
+
+// Host mixed-radix (2, 3, 5) DFT in fp64, recursive decimation in time; sign -1 (forward).
+void host_fft(std::vector<std::complex<double>>& a) {
+  const int n = (int)a.size();
+  if (n == 1) return;
+  const int r = n % 2 == 0 ? 2 : n % 3 == 0 ? 3 : 5;
+  const int m = n / r;
+  std::vector<std::vector<std::complex<double>>> sub(r, std::vector<std::complex<double>>(m));
+  for (int j = 0; j < m; ++j)
+    for (int q = 0; q < r; ++q) sub[q][j] = a[j * r + q];
+  for (int q = 0; q < r; ++q) host_fft(sub[q]);
+  for (int k = 0; k < n; ++k) {
+    std::complex<double> acc = 0.0;
+    for (int q = 0; q < r; ++q) {
+      const double ang = -2.0 * M_PI * (double)(((long long)q * k) % n) / (double)n;
+      acc += sub[q][k % m] * std::complex<double>(cos(ang), sin(ang));
+    }
+    a[k] = acc;
+  }
+}
+
+struct BlueTab {
+  int M = 0;
+  const float2* chirp = nullptr;   // c_k = e^{-pi i k^2 / N}, k < N
+  const float2* bh = nullptr;      // FFT_M(b) / M, b the wrapped conj chirp
+  const float2* st = nullptr;      // Stockham table of M
+};
+
+// Bluestein tables of length n (device copies, cached per device); false if n has no length-M plan.
+bool get_bluestein(int n, BlueTab* out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, BlueTab> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, n});
+  if (it != cache.end()) { *out = it->second; return out->M > 0; }
+  BlueTab t;
+  t.M = bluestein_len(n);
+  if (t.M) {
+    const int M = t.M;
+    std::vector<float2> chirp(n), bh(M);
+    std::vector<std::complex<double>> b(M, 0.0);
+    for (int k = 0; k < n; ++k) {
+      const long long m = ((long long)k * k) % (2LL * n);     // exact: e^{-pi i k^2/n} has period 2n in k^2
+      const double ang = M_PI * (double)m / (double)n;
+      chirp[k] = make_float2((float)cos(ang), (float)-sin(ang));
+      b[k] = std::complex<double>(cos(ang), sin(ang));
+      if (k) b[M - k] = b[k];
+    }
+    host_fft(b);
+    for (int k = 0; k < M; ++k) bh[k] = make_float2((float)(b[k].real() / M), (float)(b[k].imag() / M));
+    std::vector<double> cs(2 * (size_t)M);
+    host_twiddles(M, cs.data());
+    std::vector<float2> st(stockham_table_len(M) + 1);
+    host_stockham_table(M, cs.data(), st.data());
+    void *dc = nullptr, *db = nullptr, *ds = nullptr;
+    if (cudaMalloc(&dc, sizeof(float2) * n) != cudaSuccess || cudaMalloc(&db, sizeof(float2) * M) != cudaSuccess ||
+        cudaMalloc(&ds, sizeof(float2) * st.size()) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaMemcpy(dc, chirp.data(), sizeof(float2) * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(db, bh.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+    cudaMemcpy(ds, st.data(), sizeof(float2) * st.size(), cudaMemcpyHostToDevice);
+    t.chirp = (const float2*)dc;
+    t.bh = (const float2*)db;
+    t.st = (const float2*)ds;
+  }
+  cache[{dev, n}] = t;
+  *out = t;
+  return t.M > 0;
+}
+
+// The transform job of length n: the mixed-radix FFT for 5-smooth n (st = the handle's table), else
+// Bluestein through a 5-smooth length M (its own tables).  L = the buffer length of a job.
+bool fft_job(int64_t n3, const float2* st_n, FftPlan* pl, const float2** st, FftJob* job, int* L) {
+  if (n3 <= 64 || n3 > FFT_POINTS) return false;
+  if (make_plan((int)n3, pl)) {
+    if (!st_n) return false;
+    *st = st_n;
+    *job = FftJob{0, nullptr, nullptr};
+    *L = (int)n3;
+    return true;
+  }
+  BlueTab t;
+  if (!get_bluestein((int)n3, &t) || !make_plan(t.M, pl)) return false;
+  *st = t.st;
+  *job = FftJob{t.M, t.chirp, t.bh};
+  *L = t.M;
+  return true;
+}
+
+}  // namespace
+
+bool bluestein_supported(int64_t n3) {
   FftPlan pl;
-  make_plan((int)n3, &pl);
-  const int N = (int)n3, F = fft_F(N);
+  return n3 > 64 && n3 <= FFT_POINTS && !make_plan((int)n3, &pl) && bluestein_len((int)n3) > 0;
+}
+
+bool launch_fwd_fft(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                    const float2* st_n, __half* out, int64_t ld, float* unscale, cudaStream_t s) {
+  FftPlan pl;
+  const float2* st = nullptr;
+  FftJob job;
+  int L = 0;
+  if (!fft_job(n3, st_n, &pl, &st, &job, &L)) return false;
+  const int N = (int)n3, F = fft_F(L);
   const int TUB = 2 * F;
-  const size_t smem = fft_smem_bytes(N);
+  const size_t smem = fft_smem_bytes(L);
   const int64_t blocks = (P + TUB - 1) / TUB * Q;
   // vectorised loads need every block full and 16-byte aligned rows
   const int vec = (TUB % 4 == 0) && (P % TUB == 0) && (((uintptr_t)X) & 15) == 0;
   const void* k = role == 0 ? (const void*)fft_fwd_split_kernel<0> : (const void*)fft_fwd_split_kernel<1>;
-  if (!fft_smem_ok(k, N)) return false;
+  if (!fft_smem_ok(k, L)) return false;
   if (role == 0)
     fft_fwd_split_kernel<0><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, F, pl, maxbits, st, out, ld,
-                                                                       unscale, vec);
+                                                                       unscale, vec, job);
   else
     fft_fwd_split_kernel<1><<<(unsigned)blocks, FFT_THREADS, smem, s>>>(X, P, Q, N, F, pl, maxbits, st, out, ld,
-                                                                       unscale, vec);
+                                                                       unscale, vec, job);
   return cudaGetLastError() == cudaSuccess;
 }
 
 bool launch_inv_fft(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P, int64_t Q,
-                    int64_t n3, const float2* st, OutUnscale u, float* X, cudaStream_t s) {
-  if (!fft_supported(n3)) return false;
+                    int64_t n3, const float2* st_n, OutUnscale u, float* X, cudaStream_t s) {
   FftPlan pl;
-  make_plan((int)n3, &pl);
-  const int N = (int)n3, F = fft_F(N);
+  const float2* st = nullptr;
+  FftJob job;
+  int L = 0;
+  if (!fft_job(n3, st_n, &pl, &st, &job, &L)) return false;
+  const int N = (int)n3, F = fft_F(L);
   const int TUB = 2 * F;
-  const size_t smem = fft_smem_bytes(N);
+  const size_t smem = fft_smem_bytes(L);
   const int64_t blocks = (P + TUB - 1) / TUB * Q;
   // paired float2 loads of C-bar need both tubes of every pair in range and 8-byte alignment
   const int vec = (P % TUB == 0) && (ld % 2 == 0) && (fstride % 2 == 0) && (((uintptr_t)Cre) & 7) == 0 &&
                   (((uintptr_t)Cim) & 7) == 0;
-  if (!fft_smem_ok((const void*)fft_inv_kernel, N)) return false;
-  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, F, pl, st, u, X, vec);
+  if (!fft_smem_ok((const void*)fft_inv_kernel, L)) return false;
+  fft_inv_kernel<<<(unsigned)blocks, IFFT_THREADS, smem, s>>>(Cre, Cim, ld, fstride, P, Q, N, F, pl, st, u, X, vec,
+                                                              job);
   return cudaGetLastError() == cudaSuccess;
 }
 

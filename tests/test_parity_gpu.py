@@ -123,11 +123,12 @@ def test_fp64_longer_tubes(T, dims):
     assert O.rel_err(C, ref) <= TOL64
 
 
-@pytest.mark.parametrize("dims", [(40, 24, 67, 20), (33, 17, 97, 9), (64, 16, 97, 12), (8, 6, 4099, 5)],
+@pytest.mark.parametrize("dims", [(40, 24, 67, 20), (33, 17, 97, 9), (64, 16, 97, 12), (8, 6, 4099, 5),
+                                  (2, 3, 8209, 2)],      # prime > 8192: no Bluestein length fits, generic O(n3^2)
                          ids=lambda d: "x".join(map(str, d)))
 def test_fp32_non_smooth_long_tubes(T, dims):
-    """fp32 end to end for n3 > 64 that is not 5-smooth (prime 67, 97, 4099): the generic
-    O(n3^2) forward and inverse kernels (R12), incl. the inverse's per-tube unscale (R18)."""
+    """fp32 end to end for n3 > 64 that is not 5-smooth (prime 67, 97, 4099): Bluestein's chirp-z
+    through a 5-smooth FFT, forward and inverse (R12), incl. the inverse's per-tube unscale (R18)."""
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 700 + n3)
     B = normal((n2, n4, n3), 800 + n3)
@@ -176,7 +177,8 @@ def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
 
 # ------------------------------------------------------------------------------- stages
 @pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 65, 96, 100, 120, 128, 256, 375, 1000, 1536,
-                                2048, 4096, 6000, 8192, 15360])
+                                2048, 4096, 6000, 8192, 15360,
+                                67, 97, 127, 1021, 4099, 8191])      # not 5-smooth: Bluestein
 def test_stage_forward_dft(T, n3):
     """S1/S2 vs numpy.fft.rfft (library special case), both operand roles."""
     p, q = (37, 5) if n3 > 64 else (133, 9)
@@ -189,7 +191,7 @@ def test_stage_forward_dft(T, n3):
 
 
 @pytest.mark.parametrize("n3", [1, 2, 7, 31, 32, 64, 96, 100, 128, 375, 512, 1000, 4096, 6000, 8192,
-                                15360])
+                                15360, 67, 97, 1021, 4099])
 def test_stage_inverse_roundtrip(T, n3):
     """S4(S1(X)) = X and the 1x1xn3 circular-convolution worked example."""
     import torch
@@ -425,6 +427,33 @@ def test_tsvd_factors_gpu(T, dims):
     assert O.rel_err(S, S_ref) <= 1e-5
     A64 = A.astype(np.float64)
     assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A64) <= 1e-5
+    assert O.rel_err(O.tprod_bcirc(O.tran(U), U), O.teye(r, n3)) <= 1e-5
+    assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, n3)) <= 1e-5
+
+
+@pytest.mark.parametrize("dims,rank", [((8, 8, 5), 2), ((12, 20, 7), 3), ((16, 6, 4), 0)],
+                         ids=lambda d: "x".join(map(str, d)) if isinstance(d, tuple) else str(d))
+def test_tsvd_factors_rank_deficient(T, dims, rank):
+    """Theorem 2.2 asks for orthogonal factors also when A is rank-deficient: with A = U0 * V0 of
+    tubal rank 2 or 3 (and the zero tensor), every spectral slice has zero singular values, whose
+    left vectors the Jacobi SVD cannot supply; the kernel completes them to an orthonormal set, so
+    U^* * U = V^* * V = I still holds, A = U * S * V^* and S matches the oracle."""
+    n1, n2, n3 = dims
+    r = min(n1, n2)
+    if rank:
+        U0 = normal((n1, rank, n3), 141 + n3, np.float64)
+        V0 = normal((rank, n2, n3), 142 + n3, np.float64)
+        A = O.tprod_bcirc(U0, V0).astype(np.float32)
+    else:
+        A = np.zeros(dims, np.float32)
+    U, S, V = (host(x) for x in T.tsvd(dev(A)))
+    assert np.isfinite(U).all() and np.isfinite(V).all()
+    _, S_ref, _ = O.tsvd(A.astype(np.float64))
+    if rank:
+        assert O.rel_err(S, S_ref) <= 1e-5
+        assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A.astype(np.float64)) <= 1e-5
+    else:
+        assert np.all(S == 0.0)
     assert O.rel_err(O.tprod_bcirc(O.tran(U), U), O.teye(r, n3)) <= 1e-5
     assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, n3)) <= 1e-5
 
