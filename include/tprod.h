@@ -113,10 +113,12 @@ int tprod_teye_f64(double* I, int64_t n, int64_t n3, void* stream, tprod_handle 
 int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream, tprod_handle h);
 
 /* NEXT-2: t-SVT, the proximal operator of tau * TNN (Algorithm 3, Eq. (19)-(21)).
- * Y, X: n1 x n2 x n3 DEVICE pointers in Matlab layout, 1 <= n1, n2 <= 64, tau >= 0.  Forward DFT
- * (production K1 kernels, decoded to fp32), one-sided Jacobi SVD + singular-value shrinkage per
- * spectral slice f < h, inverse DFT with the conjugate fill (production K3 kernels).  Asynchronous.
- * TPROD_EUNSUPPORTED beyond 64 x 64 slices, TPROD_EINVAL for tau < 0 or NaN. */
+ * Y, X: n1 x n2 x n3 DEVICE pointers in Matlab layout, n1, n2 >= 1, tau >= 0.  Forward DFT
+ * (production K1 kernels, decoded to fp32), one-sided Jacobi SVD in fp64 + singular-value shrinkage
+ * per spectral slice f < h (slices up to 64 x 64: one CTA per slice in shared memory; larger: a
+ * blocked Jacobi over column blocks of 32 with the slices in the workspace, 16 (m n + n^2) h bytes,
+ * n = min(n1, n2)), inverse DFT with the conjugate fill (production K3 kernels).  Asynchronous.
+ * TPROD_EINVAL for tau < 0 or NaN, TPROD_ENOMEM if the workspace does not fit. */
 int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3, float tau, void* stream,
                    tprod_handle h);
 

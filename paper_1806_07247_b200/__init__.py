@@ -262,7 +262,8 @@ def tinv(A, out=None, handle=None, stream=None):
 
 
 def tsvt(Y, tau: float, out=None, handle=None, stream=None):
-    """Prox of tau * TNN (Algorithm 3, t-SVT) for a float32 n1 x n2 x n3 CUDA tensor, n1, n2 <= 64."""
+    """Prox of tau * TNN (Algorithm 3, t-SVT) for a float32 n1 x n2 x n3 CUDA tensor (any slice
+    size: one CTA per spectral slice up to 64 x 64, a blocked Jacobi beyond)."""
     import torch
     if Y.dim() != 3 or Y.dtype != torch.float32 or not Y.is_cuda or not is_matlab_layout(Y):
         raise ValueError("tsvt needs a float32 3-D CUDA tensor in the Matlab layout")

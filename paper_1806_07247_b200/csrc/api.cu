@@ -862,19 +862,27 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   if (!h || !Y || !X || !(tau >= 0.f)) return TPROD_EINVAL;
   int st = validate_dims(n1, n2, n3, 1);
   if (st) return st;
-  if (!svt_supported(n1, n2)) return TPROD_EUNSUPPORTED;
   const size_t b = 4 * (size_t)(n1 * n2 * n3);
   if (overlaps(Y, b, X, b)) return TPROD_EALIAS;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t hh = h_slices(n3), mn = n1 * n2;
+  // slices up to 64 x 64: one CTA per slice, Jacobi in shared memory; larger: blocked Jacobi with the
+  // slices in the workspace (tsvt_block.cu)
+  const bool small = svt_supported(n1, n2);
+  const size_t wbytes = align_up(4 * (size_t)(2 * hh * mn), 1024);
+  const size_t extra_bytes = wbytes + (small ? 0 : bj_workspace_bytes(n1, n2, hh));
   float *re, *im;
   void* extra;
   Twiddles32 T;
-  if ((st = spectral_planes(h, Y, n1, n2, n3, 4 * (size_t)(2 * hh * mn), &re, &im, &extra, &T, s))) return st;  // Alg. 3 step 1
+  if ((st = spectral_planes(h, Y, n1, n2, n3, extra_bytes, &re, &im, &extra, &T, s))) return st;  // Alg. 3 step 1
   float* wre = (float*)extra;
   float* wim = wre + hh * mn;
-  if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, s)) return TPROD_ECUDA;   // step 2
+  if (small) {
+    if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, s)) return TPROD_ECUDA;   // step 2
+  } else {
+    if (launch_block_svt(re, im, n1, n2, hh, mn, tau, wre, wim, nullptr, (char*)extra + wbytes, s)) return TPROD_ECUDA;
+  }
   launch_inv_f32(wre, wim, n1, mn, n1, n2, n3, T, OutUnscale{}, X, h->num_sms, s);         // step 2b + 3
   h->last_launches = 5;
   return launch_status();

@@ -113,6 +113,11 @@ int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, i
                      int64_t fstride, float tau, cudaStream_t s);
 int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
                              float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s);
+// Blocked one-sided Jacobi of every spectral slice (tsvt_block.cu), any slice size: t-SVT (tau >= 0)
+// into wre / wim, or (tau < 0) the singular values into sig_out ([h][min(m, n)], unsorted).
+size_t bj_workspace_bytes(int64_t m, int64_t n, int64_t h);
+int launch_block_svt(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride, float tau,
+                     float* wre, float* wim, double* sig_out, void* ws, cudaStream_t s);
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
                        double* sv, float rtol, float* out, cudaStream_t s);
 
