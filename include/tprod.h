@@ -101,11 +101,14 @@ int tprod_release_a(tprod_handle h);
  *   At(:,:,0) = A(:,:,0)^T and At(:,:,k) = A(:,:,n3-k)^T (real data).  At must not overlap A.
  * tprod_teye_*: I = the n x n x n3 identity tensor (Definition 2.3).
  * tprod_tinv_f32: X = A^-1 (Definition 2.4, Eq. (11)), A and X n x n x n3,
- *   1 <= n <= 96: forward DFT (production K1 kernels), a complex Gauss-Jordan inverse with partial
- *   pivoting per spectral slice f < h (fp32), inverse DFT with the conjugate fill (production K3
- *   kernels).  SYNCHRONOUS (waits for `stream`): returns TPROD_ESINGULAR if a pivot falls to
- *   <= n * 2^-20 times the largest spectral entry (X is then unspecified), TPROD_EUNSUPPORTED for
- *   n > 96. */
+ *   1 <= n <= 8192: forward DFT (production K1 kernels), a complex Gauss-Jordan inverse with partial
+ *   pivoting per spectral slice f < h (n <= 96: one CTA per slice in shared memory, fp32; larger: the
+ *   augmented slices in the workspace, 32 n^2 h bytes, fp64, two launches per pivot column), inverse
+ *   DFT with the conjugate fill (production K3 kernels).  A slice is singular when a pivot falls to
+ *   <= n * 2^-20 times the largest spectral entry (X is then unspecified).  With
+ *   TPROD_OPT_SYNC_CHECKS = 1 (default) the call is SYNCHRONOUS (waits for `stream`) and returns
+ *   TPROD_ESINGULAR; with 0 it is asynchronous and sets TPROD_STATUS_SINGULAR in the handle's status
+ *   word (tprod_status).  TPROD_EUNSUPPORTED for n > 8192. */
 int tprod_tran_f32(const float* A, float* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
 int tprod_tran_f64(const double* A, double* At, int64_t n1, int64_t n2, int64_t n3, void* stream, tprod_handle h);
 int tprod_teye_f32(float* I, int64_t n, int64_t n3, void* stream, tprod_handle h);
@@ -115,15 +118,17 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
 /* NEXT-2: t-SVT, the proximal operator of tau * TNN (Algorithm 3, Eq. (19)-(21)).
  * Y, X: n1 x n2 x n3 DEVICE pointers in Matlab layout, n1, n2 >= 1, tau >= 0.  Forward DFT
  * (production K1 kernels, decoded to fp32), one-sided Jacobi SVD in fp64 + singular-value shrinkage
- * per spectral slice f < h (slices up to 64 x 64: one CTA per slice in shared memory; larger: a
- * blocked Jacobi over column blocks of 32 with the slices in the workspace, 16 (m n + n^2) h bytes,
- * n = min(n1, n2)), inverse DFT with the conjugate fill (production K3 kernels).  Asynchronous.
+ * per spectral slice f < h (slices up to 64 x 64: one CTA per slice in shared memory, at most 40
+ * sweeps; larger: a blocked Jacobi over column blocks of 32 with the slices in the workspace,
+ * about 16 (m n + n^2) h bytes, m = max(n1, n2), n = min(n1, n2) <= 65535, at most 30 sweeps),
+ * inverse DFT with the conjugate fill (production K3 kernels).  Asynchronous.  A slice still
+ * rotating at the sweep cap sets TPROD_STATUS_NOCONVERGE in the handle's status word (tprod_status).
  * TPROD_EINVAL for tau < 0 or NaN, TPROD_ENOMEM if the workspace does not fit. */
 int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3, float tau, void* stream,
                    tprod_handle h);
 
 /* NEXT-3: t-SVD scalars (Theorem 2.2 / Algorithm 2 step 2, Eq. (13)-(18)) of a
- * DEVICE n1 x n2 x n3 tensor A (Matlab layout, 1 <= n1, n2 <= 64).  Writes to the DEVICE array
+ * DEVICE n1 x n2 x n3 tensor A (Matlab layout, any slice size as tprod_tsvt_f32).  Writes to the DEVICE array
  * `out` (r + 3 floats, r = min(n1, n2)): out[0..r) = the singular values S(i,i,1) of A (Eq. (14),
  * non-increasing), out[r] = TNN (Def. 2.9), out[r+1] = TSN = ||bcirc(A)||_2 (Def. 2.8),
  * out[r+2] = tubal rank #{i : S(i,i,1) > rtol * S(1,1,1)} (Eq. (16)).  Same transforms and per-slice
@@ -131,11 +136,13 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
 int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, float rtol, float* out, void* stream,
                           tprod_handle h);
 /* Skinny t-SVD factors (Algorithm 2, Theorem 2.2 Eq. (12); R17): A = U * S * V^* with
- * U n1 x r x n3, S r x r x n3 (f-diagonal), V n2 x r x n3, r = min(n1, n2) <= 64, all DEVICE
- * pointers in Matlab layout.  Per spectral slice f < h the Jacobi SVD's factors (columns in
- * non-increasing singular-value order), conjugate fill and inverse DFT of each factor.  Singular
- * vectors are unique up to a unit phase per column and slice (S is unique); a zero singular value
- * leaves a zero left-vector column.  Asynchronous. */
+ * U n1 x r x n3, S r x r x n3 (f-diagonal), V n2 x r x n3, r = min(n1, n2), all DEVICE pointers in
+ * Matlab layout, any slice size as tprod_tsvt_f32.  Per spectral slice f < h the Jacobi SVD's
+ * factors (columns in non-increasing singular-value order), conjugate fill and inverse DFT of each
+ * factor.  Singular vectors are unique up to a unit phase per column and slice (S is unique); a
+ * left vector whose singular value is <= 1e-6 of the slice's largest is replaced by a unit vector
+ * Gram-Schmidt-orthogonalised against the others, so U^* U = I holds for rank-deficient A too.
+ * Asynchronous; non-convergence as tprod_tsvt_f32. */
 int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3, void* stream,
                    tprod_handle h);
 
@@ -192,7 +199,10 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
-       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7 };
+       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7, TPROD_OPT_SYNC_CHECKS = 8 };
+/* TPROD_OPT_SYNC_CHECKS: 1 (default) = tprod_tinv_f32 waits for its stream and returns
+ * TPROD_ESINGULAR for a singular tensor; 0 = it returns at once and reports singularity through
+ * the status word (tprod_status). */
 /* TPROD_OPT_POISON: 1 = before every call the handle fills the workspace it will use (and a prepared
  * operand's buffers) with 0xFF bytes -- NaN in fp16 / fp32 / fp64 -- on the call's stream, so that any
  * kernel reading workspace it has not written first turns the result into NaN (a test-time stand-in
@@ -223,6 +233,14 @@ int tprod_set_option(tprod_handle h, int option, int64_t value);
  * [K0 scales, K1 forward DFTs, K2 per-frequency GEMMs, K3 inverse DFT], synchronising on the
  * last event.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that call. */
 int tprod_last_stage_ms(tprod_handle h, float* out);
+
+/* Status word of the handle: an OR of the TPROD_STATUS_* bits raised on the device by the handle's
+ * kernels since the previous tprod_status call.  Enqueues a read and a clear of the word on
+ * `stream`, waits for `stream`, and writes the bits to *bits (host).  Call it after the work to
+ * check was enqueued on `stream` (or after synchronising the other streams that ran it). */
+enum { TPROD_STATUS_SINGULAR = 1,     /* tprod_tinv_f32 with TPROD_OPT_SYNC_CHECKS = 0: singular */
+       TPROD_STATUS_NOCONVERGE = 2 }; /* t-SVT / t-SVD: a spectral slice reached the sweep cap */
+int tprod_status(tprod_handle h, void* stream, int* bits);
 
 #ifdef __cplusplus
 }

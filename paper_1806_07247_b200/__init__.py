@@ -86,6 +86,16 @@ class Handle:
         check(lib().tprod_last_launch_count(self._h, C.byref(out)), "tprod_last_launch_count")
         return out.value
 
+    def status(self, stream=None) -> int:
+        """TPROD_STATUS_* bits the handle's kernels raised since the last query (SINGULAR from an
+        asynchronous tinv, NOCONVERGE from an SVD slice that hit its sweep cap); synchronises
+        `stream` (default: the current stream) and clears the word (tprod_status)."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        out = C.c_int()
+        check(lib().tprod_status(self._h, C.c_void_p(s.cuda_stream), C.byref(out)), "tprod_status")
+        return out.value
+
     def last_stage_ms(self):
         """[K0 scales, K1 forward, K2 GEMM, K3 inverse] durations (ms) of the last fp32 call
         (requires set_option(TPROD_OPT_TIMING, 1) before the call)."""
@@ -244,8 +254,10 @@ def teye(n: int, n3: int, dtype=None, device="cuda", handle=None, stream=None):
 
 
 def tinv(A, out=None, handle=None, stream=None):
-    """A^-1 (Definition 2.4, Eq. (11)) for a float32 n x n x n3 CUDA tensor, n <= 96.  Synchronous;
-    raises TprodError (status TPROD_ESINGULAR) if a spectral slice is singular to working precision."""
+    """A^-1 (Definition 2.4, Eq. (11)) for a float32 n x n x n3 CUDA tensor (n <= 8192).  By default
+    synchronous, raising TprodError (status TPROD_ESINGULAR) if a spectral slice is singular to
+    working precision; with handle.set_option(TPROD_OPT_SYNC_CHECKS, 0) asynchronous, singularity
+    then reported by handle.status()."""
     import torch
     if A.dim() != 3 or A.shape[0] != A.shape[1] or A.dtype != torch.float32 or not A.is_cuda:
         raise ValueError("tinv needs a float32 n x n x n3 CUDA tensor")
@@ -279,7 +291,7 @@ def tsvt(Y, tau: float, out=None, handle=None, stream=None):
 
 
 def tsvd_values(A, rtol: float = 1e-6, handle=None, stream=None):
-    """t-SVD scalars of a float32 n1 x n2 x n3 CUDA tensor (n1, n2 <= 64): returns a CUDA float32
+    """t-SVD scalars of a float32 n1 x n2 x n3 CUDA tensor (any slice size): returns a CUDA float32
     vector [S(1,1,1) .. S(r,r,1), TNN, TSN, tubal rank] (Eq. (14), Def. 2.9, Def. 2.8, Eq. (16))."""
     import torch
     if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda or not is_matlab_layout(A):
@@ -293,7 +305,7 @@ def tsvd_values(A, rtol: float = 1e-6, handle=None, stream=None):
 
 
 def tsvd(A, handle=None, stream=None):
-    """Skinny t-SVD (Algorithm 2) of a float32 n1 x n2 x n3 CUDA tensor (min(n1, n2) <= 64, both <= 64):
+    """Skinny t-SVD (Algorithm 2) of a float32 n1 x n2 x n3 CUDA tensor (any slice size):
     returns (U n1 x r x n3, S r x r x n3, V n2 x r x n3) with A = U * S * V^*."""
     import torch
     if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda or not is_matlab_layout(A):

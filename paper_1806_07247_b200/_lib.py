@@ -14,7 +14,8 @@ TPROD_OK, TPROD_EINVAL, TPROD_EALIAS, TPROD_ENOMEM, TPROD_ECUDA, TPROD_ENCCL, \
     TPROD_EUNSUPPORTED, TPROD_ENOWORLD, TPROD_ESINGULAR = range(9)
 TPROD_DTYPE_F32, TPROD_DTYPE_F64 = 0, 1
 (TPROD_OPT_ENGINE, TPROD_OPT_GEMM_BN, TPROD_OPT_TIMING, TPROD_OPT_GEMM_CLUSTER, TPROD_OPT_TRANSFORM,
- TPROD_OPT_GRAPHS, TPROD_OPT_POISON) = 1, 2, 3, 4, 5, 6, 7
+ TPROD_OPT_GRAPHS, TPROD_OPT_POISON, TPROD_OPT_SYNC_CHECKS) = 1, 2, 3, 4, 5, 6, 7, 8
+TPROD_STATUS_SINGULAR, TPROD_STATUS_NOCONVERGE = 1, 2
 
 # name -> (restype, argtypes); the full list of symbols include/tprod.h declares
 _i64, _vp, _int = C.c_int64, C.c_void_p, C.c_int
@@ -36,6 +37,7 @@ SIGNATURES = {
     "tprod_idft_f32": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "tprod_set_option": (_int, [_vp, _int, _i64]),
     "tprod_last_stage_ms": (_int, [_vp, C.POINTER(C.c_float)]),
+    "tprod_status": (_int, [_vp, _vp, C.POINTER(_int)]),
     "tprod_prepare_a_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "tprod_f32_prepared": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "tprod_release_a": (_int, [_vp]),

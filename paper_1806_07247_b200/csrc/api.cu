@@ -63,6 +63,8 @@ struct tprod_ctx {
   // parameters derive from (operand / workspace / table pointers, shapes, options)
   bool graphs = true;
   bool poison = false;                                 // TPROD_OPT_POISON: NaN-fill the workspace before each call
+  bool sync_checks = true;                             // TPROD_OPT_SYNC_CHECKS
+  int* status = nullptr;                               // device status word (TPROD_STATUS_* bits), tprod_status
   cudaStream_t cap = nullptr;                          // private capture stream
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -700,9 +702,14 @@ int tprod_create(int device, tprod_handle* out) {
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10 || prop.minor != 0) return TPROD_EUNSUPPORTED;   // sm_100a binary only
+  CK(cudaSetDevice(device));
+  int* status = nullptr;
+  CK(cudaMalloc(&status, sizeof(int)));
+  CK(cudaMemset(status, 0, sizeof(int)));
   tprod_ctx* h = new tprod_ctx;
   h->device = device;
   h->num_sms = prop.multiProcessorCount;
+  h->status = status;
   *out = h;
   return TPROD_OK;
 }
@@ -729,6 +736,7 @@ int tprod_destroy(tprod_handle h) {
   clear_graphs(h);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->ws) cudaFree(h->ws);
+  if (h->status) cudaFree(h->status);
   for (void* p : h->retired) cudaFree(p);
   delete h;
   return TPROD_OK;
@@ -808,7 +816,7 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   if (!h || !A || !X) return TPROD_EINVAL;
   int st = validate_dims(n, n, n3, 1);
   if (st) return st;
-  if (!tinv_supported(n)) return TPROD_EUNSUPPORTED;
+  if (n > 8192) return TPROD_EUNSUPPORTED;
   const size_t b = 4 * (size_t)(n * n * n3);
   if (overlaps(A, b, X, b)) return TPROD_EALIAS;
   CK(cudaSetDevice(h->device));
@@ -823,6 +831,8 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   const size_t off_sp = o;   o = align_up(o + 2 * (size_t)(hh * NPLANES * n * ld), 1024);
   const size_t off_re = o;   o = align_up(o + 4 * (size_t)(4 * hh * nn), 1024);  // re, im, xre, xim
   const size_t off_w = o;    o = align_up(o + (f1 ? b : 0), 1024);
+  const bool small = tinv_supported(n);                                     // n <= 96: shared-memory kernel
+  const size_t off_gj = o;   o = align_up(o + (small ? 0 : gj_workspace_bytes(n, hh)), 1024);
   if ((st = ensure_ws(h, o, s)) || (st = poison_ws(h, o, s))) return st;
   char* ws = (char*)h->ws;
   Twiddles32 T;
@@ -847,13 +857,20 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   launch_decode_split(sp, ld, n, n, n3, 0, u, re, im, s);                    // fp32 planes [f][q][p]
   launch_absmax_planes(re, im, hh * nn, amax, s);
   const float rtol = (float)n * 9.5367431640625e-07f;                        // n * 2^-20
-  if (launch_slice_inverse(re, im, xre, xim, n, hh, nn, rtol, amax, flag, s)) return TPROD_ECUDA;
+  // synchronous checks: this call's own flag, read back below; else the handle's status word
+  int* sflag = h->sync_checks ? flag : h->status;
+  if (small) {
+    if (launch_slice_inverse(re, im, xre, xim, n, hh, nn, rtol, amax, sflag, s)) return TPROD_ECUDA;
+  } else {
+    if (launch_slice_inverse_large(re, im, xre, xim, n, hh, nn, rtol, amax, sflag, ws + off_gj, s)) return TPROD_ECUDA;
+  }
   launch_inv_f32(xre, xim, n, nn, n, n, n3, T, OutUnscale{}, X, h->num_sms, s);            // fill + inverse DFT
   if ((st = launch_status())) return st;
+  h->last_launches = small ? 7 : 8 + 2 * n;
+  if (!h->sync_checks) return TPROD_OK;
   int host_flag = 0;
   CK(cudaMemcpyAsync(&host_flag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  h->last_launches = 7;
   return host_flag ? TPROD_ESINGULAR : TPROD_OK;
 }
 
@@ -872,6 +889,7 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   const bool small = svt_supported(n1, n2);
   const size_t wbytes = align_up(4 * (size_t)(2 * hh * mn), 1024);
   const size_t extra_bytes = wbytes + (small ? 0 : bj_workspace_bytes(n1, n2, hh));
+  if (!small && std::min(n1, n2) > 65535) return TPROD_EUNSUPPORTED;
   float *re, *im;
   void* extra;
   Twiddles32 T;
@@ -879,9 +897,13 @@ int tprod_tsvt_f32(const float* Y, float* X, int64_t n1, int64_t n2, int64_t n3,
   float* wre = (float*)extra;
   float* wim = wre + hh * mn;
   if (small) {
-    if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, s)) return TPROD_ECUDA;   // step 2
+    if (launch_slice_svt(re, im, wre, wim, n1, n2, hh, mn, tau, h->status, s)) return TPROD_ECUDA;   // step 2
   } else {
-    if (launch_block_svt(re, im, n1, n2, hh, mn, tau, wre, wim, nullptr, (char*)extra + wbytes, s)) return TPROD_ECUDA;
+    BjOut o{};
+    o.tau = tau;
+    o.wre = wre;
+    o.wim = wim;
+    if (launch_block_svd(re, im, n1, n2, hh, mn, BJ_SVT, o, (char*)extra + wbytes, h->status, s)) return TPROD_ECUDA;
   }
   launch_inv_f32(wre, wim, n1, mn, n1, n2, n3, T, OutUnscale{}, X, h->num_sms, s);         // step 2b + 3
   h->last_launches = 5;
@@ -893,7 +915,8 @@ int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int
   if (!h || !A || !U || !S || !V) return TPROD_EINVAL;
   int st = validate_dims(n1, n2, n3, 1);
   if (st) return st;
-  if (!svt_supported(n1, n2)) return TPROD_EUNSUPPORTED;
+  const bool small = svt_supported(n1, n2);
+  if (!small && std::min(n1, n2) > 65535) return TPROD_EUNSUPPORTED;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t hh = h_slices(n3), r = std::min(n1, n2);
@@ -901,7 +924,8 @@ int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int
   float *re, *im;
   void* extra;
   Twiddles32 T;
-  const size_t ex = 4 * (size_t)(hh * (2 * nu + 2 * ns + 2 * nv));
+  const size_t fbytes = align_up(4 * (size_t)(hh * (2 * nu + 2 * ns + 2 * nv)), 1024);
+  const size_t ex = fbytes + (small ? 0 : bj_workspace_bytes(n1, n2, hh));
   if ((st = spectral_planes(h, A, n1, n2, n3, ex, &re, &im, &extra, &T, s))) return st;   // Alg. 2 step 1
   float* ure = (float*)extra;
   float* uim = ure + hh * nu;
@@ -910,7 +934,19 @@ int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int
   float* vre = sim + hh * ns;
   float* vim = vre + hh * nv;
   CK(cudaMemsetAsync(sim, 0, 4 * (size_t)(hh * ns), s));                                  // S-bar is real
-  if (launch_slice_svd_factors(re, im, n1, n2, hh, n1 * n2, ure, uim, sre, vre, vim, s)) return TPROD_ECUDA;  // step 2
+  if (small) {
+    if (launch_slice_svd_factors(re, im, n1, n2, hh, n1 * n2, ure, uim, sre, vre, vim, h->status, s))
+      return TPROD_ECUDA;                                                                  // step 2
+  } else {
+    BjOut o{};
+    o.ure = ure;
+    o.uim = uim;
+    o.sre = sre;
+    o.vre = vre;
+    o.vim = vim;
+    if (launch_block_svd(re, im, n1, n2, hh, n1 * n2, BJ_FACTORS, o, (char*)extra + fbytes, h->status, s))
+      return TPROD_ECUDA;
+  }
   // step 2b + 3: conjugate fill + inverse DFT of each factor (S-bar's copy rule = conj of a real slice)
   launch_inv_f32(ure, uim, n1, nu, n1, r, n3, T, OutUnscale{}, U, h->num_sms, s);
   launch_inv_f32(sre, sim, r, ns, r, r, n3, T, OutUnscale{}, S, h->num_sms, s);
@@ -924,15 +960,27 @@ int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, fl
   if (!h || !A || !out || !(rtol >= 0.f)) return TPROD_EINVAL;
   int st = validate_dims(n1, n2, n3, 1);
   if (st) return st;
-  if (!svt_supported(n1, n2)) return TPROD_EUNSUPPORTED;
+  const bool small = svt_supported(n1, n2);
+  if (!small && std::min(n1, n2) > 65535) return TPROD_EUNSUPPORTED;
   CK(cudaSetDevice(h->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t hh = h_slices(n3), r = std::min(n1, n2);
   float *re, *im;
   void* extra;
   Twiddles32 T;
-  if ((st = spectral_planes(h, A, n1, n2, n3, 8 * (size_t)(hh * r), &re, &im, &extra, &T, s))) return st;  // Alg. 2 step 1
-  if (launch_tsvd_values(re, im, n1, n2, hh, n3, n1 * n2, (double*)extra, rtol, out, s)) return TPROD_ECUDA;
+  const size_t svb = align_up(8 * (size_t)(hh * r), 1024);
+  const size_t ex = svb + (small ? 0 : bj_workspace_bytes(n1, n2, hh));
+  if ((st = spectral_planes(h, A, n1, n2, n3, ex, &re, &im, &extra, &T, s))) return st;  // Alg. 2 step 1
+  if (small) {
+    if (launch_tsvd_values(re, im, n1, n2, hh, n3, n1 * n2, (double*)extra, rtol, out, h->status, s))
+      return TPROD_ECUDA;
+  } else {
+    BjOut o{};
+    o.sv = (double*)extra;
+    if (launch_block_svd(re, im, n1, n2, hh, n1 * n2, BJ_VALUES, o, (char*)extra + svb, h->status, s) ||
+        launch_tsvd_reduce((double*)extra, r, hh, n3, rtol, out, s))
+      return TPROD_ECUDA;
+  }
   h->last_launches = 5;
   return launch_status();
 }
@@ -1092,9 +1140,25 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       if (value != 0 && value != 1) return TPROD_EINVAL;
       h->poison = value != 0;
       return TPROD_OK;
+    case TPROD_OPT_SYNC_CHECKS:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->sync_checks = value != 0;
+      return TPROD_OK;
     default:
       return TPROD_EINVAL;
   }
+}
+
+int tprod_status(tprod_handle h, void* stream, int* bits) {
+  if (!h || !bits) return TPROD_EINVAL;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int v = 0;
+  CK(cudaMemcpyAsync(&v, h->status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemsetAsync(h->status, 0, sizeof(int), s));
+  CK(cudaStreamSynchronize(s));
+  *bits = v;
+  return TPROD_OK;
 }
 
 int tprod_last_stage_ms(tprod_handle h, float* out) {

@@ -108,18 +108,36 @@ bool tinv_supported(int64_t n);
 int launch_slice_inverse(const float* re, const float* im, float* xre, float* xim, int64_t n, int64_t h,
                          int64_t fstride, float rtol, const unsigned* maxp, int* singular, cudaStream_t s);
 void launch_absmax_planes(const float* re, const float* im, int64_t count, unsigned* out, cudaStream_t s);
+// n > 96: Gauss-Jordan in global memory (fp64), workspace gj_workspace_bytes(n, h)
+size_t gj_workspace_bytes(int64_t n, int64_t h);
+int launch_slice_inverse_large(const float* re, const float* im, float* xre, float* xim, int64_t n, int64_t h,
+                               int64_t fstride, float rtol, const unsigned* maxp, int* singular, void* ws,
+                               cudaStream_t s);
 bool svt_supported(int64_t m, int64_t n);
 int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
-                     int64_t fstride, float tau, cudaStream_t s);
+                     int64_t fstride, float tau, int* status, cudaStream_t s);
 int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
-                             float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s);
-// Blocked one-sided Jacobi of every spectral slice (tsvt_block.cu), any slice size: t-SVT (tau >= 0)
-// into wre / wim, or (tau < 0) the singular values into sig_out ([h][min(m, n)], unsorted).
+                             float* ure, float* uim, float* sre, float* vre, float* vim, int* status, cudaStream_t s);
+// Blocked one-sided Jacobi of every spectral slice (tsvt_block.cu), any slice size.  BJ_SVT: t-SVT
+// with threshold tau into wre / wim (planes [f][col][row] of the m x n slice, pitch fstride);
+// BJ_VALUES: the singular values of every slice, non-increasing, into sv ([h][min(m, n)]);
+// BJ_FACTORS: skinny factors into ure/uim ([h][r][m]), sre ([h][r][r], real), vre/vim ([h][r][n]).
+// `status` (device int) gets STATUS_NOCONV or-ed in when a slice hits the sweep cap.
+constexpr int STATUS_SINGULAR = 1, STATUS_NOCONV = 2;
+enum { BJ_SVT = 0, BJ_VALUES = 1, BJ_FACTORS = 2 };
+struct BjOut {
+  float tau;
+  float *wre, *wim;                  // BJ_SVT
+  double* sv;                        // BJ_VALUES
+  float *ure, *uim, *sre, *vre, *vim;  // BJ_FACTORS
+};
 size_t bj_workspace_bytes(int64_t m, int64_t n, int64_t h);
-int launch_block_svt(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride, float tau,
-                     float* wre, float* wim, double* sig_out, void* ws, cudaStream_t s);
+int launch_block_svd(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride, int mode,
+                     BjOut o, void* ws, int* status, cudaStream_t s);
+// t-SVD scalars from per-slice singular values sv ([h][r], non-increasing), any r (tsvt_block.cu)
+int launch_tsvd_reduce(const double* sv, int64_t r, int64_t h, int64_t n3, float rtol, float* out, cudaStream_t s);
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
-                       double* sv, float rtol, float* out, cudaStream_t s);
+                       double* sv, float rtol, float* out, int* status, cudaStream_t s);
 
 // ------------------------------------------------------------------ fp64 path
 // spectra as fp64 planes [f][re|im][q][ld]

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) slice_inverse_kernel(const float* __restr
     }
     if (threadIdx.x == 0) {
       piv_row = red_i[0];
-      if (!(sqrtf(red_v[0]) > thresh)) atomicExch(singular, 1);
+      if (!(sqrtf(red_v[0]) > thresh)) atomicOr(singular, STATUS_SINGULAR);
     }
     __syncthreads();
     const int pr = piv_row;
@@ -212,6 +212,132 @@ int launch_slice_inverse(const float* re, const float* im, float* xre, float* xi
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
+// ---------------------------------------------------------------------- large slices (n > 96)
+// Gauss-Jordan with partial pivoting on [A-bar_f | I] in global memory, fp64 complex, all h slices
+// at once: per pivot column k one pivot launch (one CTA per slice: pivot among the rows not yet
+// used, multipliers l_i = a_ik / a_pk) and one elimination launch (a_ij -= l_i a_pj, j > k, i != p;
+// the pivot row is never scaled, so nothing reads a row while it changes).  Rows are not swapped:
+// piv[k] = p records the order, and X(k, :) = right half of row piv[k] / a_{piv[k], k} at the end.
+// Row-major augmented slices: (i, j) at f * n * 2n + i * 2n + j.
+__global__ void gj_init_kernel(const float* __restrict__ re, const float* __restrict__ im, int n, int64_t fstride,
+                               double2* __restrict__ aug, int* __restrict__ used) {
+  const int f = blockIdx.y, w = 2 * n;
+  double2* a = aug + (int64_t)f * n * w;
+  const float* ar = re + (int64_t)f * fstride;
+  const float* ai = im + (int64_t)f * fstride;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)n * w;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / w), c = (int)(idx - (int64_t)r * w);
+    a[idx] = c < n ? make_double2(ar[(int64_t)c * n + r], ai[(int64_t)c * n + r])
+                   : make_double2(c - n == r ? 1.0 : 0.0, 0.0);
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    used[(int64_t)f * n + r] = 0;
+}
+
+__global__ void __launch_bounds__(256) gj_pivot_kernel(const double2* __restrict__ aug, int n, int k, float rtol,
+                                                       const unsigned* __restrict__ maxp, int* __restrict__ used,
+                                                       int* __restrict__ piv, double2* __restrict__ fac,
+                                                       int* __restrict__ singular) {
+  __shared__ double bv_s[8];
+  __shared__ int bi_s[8];
+  __shared__ int p_s;
+  const int f = blockIdx.x, w = 2 * n, tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const double2* a = aug + (int64_t)f * n * w;
+  int* u = used + (int64_t)f * n;
+  double bv = -1.0;
+  int bi = n;
+  for (int r = tid; r < n; r += blockDim.x) {
+    if (u[r]) continue;
+    const double2 v = a[(int64_t)r * w + k];
+    const double m2 = v.x * v.x + v.y * v.y;
+    if (m2 > bv) { bv = m2; bi = r; }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double tv = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int ti = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (tv > bv || (tv == bv && ti < bi)) { bv = tv; bi = ti; }
+  }
+  if (lane == 0) { bv_s[wp] = bv; bi_s[wp] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+      if (bv_s[q] > bv_s[0] || (bv_s[q] == bv_s[0] && bi_s[q] < bi_s[0])) { bv_s[0] = bv_s[q]; bi_s[0] = bi_s[q]; }
+    const int p = bi_s[0] < n ? bi_s[0] : 0;
+    const double thresh = (double)rtol * (double)__uint_as_float(*maxp);
+    if (!(sqrt(bv_s[0]) > thresh)) atomicOr(singular, STATUS_SINGULAR);
+    u[p] = 1;
+    piv[(int64_t)f * n + k] = p;
+    p_s = p;
+  }
+  __syncthreads();
+  const int p = p_s;
+  const double2 pk = a[(int64_t)p * w + k];
+  const double den = pk.x * pk.x + pk.y * pk.y;
+  const double2 ipk = den > 0.0 ? make_double2(pk.x / den, -pk.y / den) : make_double2(0.0, 0.0);
+  for (int r = tid; r < n; r += blockDim.x) {
+    const double2 v = a[(int64_t)r * w + k];
+    fac[(int64_t)f * n + r] = r == p ? make_double2(0.0, 0.0)
+                                     : make_double2(v.x * ipk.x - v.y * ipk.y, v.x * ipk.y + v.y * ipk.x);
+  }
+}
+
+// one CTA per (row i, slice f); columns j > k of the row
+__global__ void __launch_bounds__(256) gj_elim_kernel(double2* __restrict__ aug, int n, int k,
+                                                      const int* __restrict__ piv, const double2* __restrict__ fac) {
+  const int i = blockIdx.x, f = blockIdx.y, w = 2 * n;
+  const double2 l = fac[(int64_t)f * n + i];
+  if (l.x == 0.0 && l.y == 0.0) return;                  // pivot row, or nothing to eliminate
+  const int p = piv[(int64_t)f * n + k];
+  double2* a = aug + (int64_t)f * n * w;
+  const double2* ap = a + (int64_t)p * w;
+  double2* ai = a + (int64_t)i * w;
+  for (int j = k + 1 + threadIdx.x; j < w; j += blockDim.x) {
+    const double2 b = ap[j];
+    double2 v = ai[j];
+    v.x -= l.x * b.x - l.y * b.y;
+    v.y -= l.x * b.y + l.y * b.x;
+    ai[j] = v;
+  }
+}
+
+// X(q, c) = a(piv[q], n + c) / a(piv[q], q) into fp32 planes [f][c][q]
+__global__ void gj_out_kernel(const double2* __restrict__ aug, int n, const int* __restrict__ piv,
+                              float* __restrict__ xre, float* __restrict__ xim, int64_t fstride) {
+  const int q = blockIdx.x, f = blockIdx.y, w = 2 * n;
+  const int p = piv[(int64_t)f * n + q];
+  const double2* ap = aug + (int64_t)f * n * w + (int64_t)p * w;
+  const double2 d = ap[q];
+  const double den = d.x * d.x + d.y * d.y;
+  const double2 id = den > 0.0 ? make_double2(d.x / den, -d.y / den) : make_double2(0.0, 0.0);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double2 v = ap[n + c];
+    xre[(int64_t)f * fstride + (int64_t)c * n + q] = (float)(v.x * id.x - v.y * id.y);
+    xim[(int64_t)f * fstride + (int64_t)c * n + q] = (float)(v.x * id.y + v.y * id.x);
+  }
+}
+
+size_t gj_workspace_bytes(int64_t n, int64_t h) {
+  return 16 * (size_t)(h * n * 2 * n) + 16 * (size_t)(h * n) + 8 * (size_t)(h * n) + 1024;
+}
+
+int launch_slice_inverse_large(const float* re, const float* im, float* xre, float* xim, int64_t n, int64_t h,
+                               int64_t fstride, float rtol, const unsigned* maxp, int* singular, void* ws,
+                               cudaStream_t s) {
+  double2* aug = (double2*)ws;
+  double2* fac = aug + h * n * 2 * n;
+  int* piv = (int*)(fac + h * n);
+  int* used = piv + h * n;
+  const int gx = (int)std::min<int64_t>((n * 2 * n + 255) / 256, 2048);
+  gj_init_kernel<<<dim3(gx, (unsigned)h), 256, 0, s>>>(re, im, (int)n, fstride, aug, used);
+  for (int k = 0; k < (int)n; ++k) {
+    gj_pivot_kernel<<<(unsigned)h, 256, 0, s>>>(aug, (int)n, k, rtol, maxp, used, piv, fac, singular);
+    gj_elim_kernel<<<dim3((unsigned)n, (unsigned)h), 256, 0, s>>>(aug, (int)n, k, piv, fac);
+  }
+  gj_out_kernel<<<dim3((unsigned)n, (unsigned)h), 256, 0, s>>>(aug, (int)n, piv, xre, xim, fstride);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
+}
+
 // largest |entry| over the decoded spectral planes (for the singularity threshold)
 __global__ void absmax_planes_kernel(const float* __restrict__ re, const float* __restrict__ im, int64_t count,
                                      unsigned* __restrict__ out) {
@@ -260,7 +386,7 @@ template <int G>
 __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float* __restrict__ re, const float* __restrict__ im,
                                                         float* __restrict__ wre, float* __restrict__ wim, int m, int n,
                                                         int64_t fstride, float tau, double* __restrict__ sv,
-                                                        SvdOut fo) {
+                                                        SvdOut fo, int* __restrict__ status) {
   extern __shared__ double2 sm[];
   double2* a = sm;                                      // column j at a + j*m
   double2* v = a + n * m;                               // column j at v + j*n
@@ -299,6 +425,7 @@ __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float*
   const long long t0 = clock64();
   int nsweeps = 0;
 #endif
+  bool converged = false;
   for (int sweep = 0; sweep < 40; ++sweep) {
 #ifdef TPROD_SVT_DEBUG
     nsweeps = sweep + 1;
@@ -393,8 +520,12 @@ __global__ void __launch_bounds__(G * SVT_MAX / 2) slice_svt_kernel(const float*
       }
       __syncthreads();
     }
-    if (!rotated[sweep % 3]) break;                     // no pair above the tolerance: read after a barrier
+    if (!rotated[sweep % 3]) {                          // no pair above the tolerance: read after a barrier
+      converged = true;
+      break;
+    }
   }
+  if (!converged && tid == 0 && status) atomicOr(status, STATUS_NOCONV);   // sweep cap reached: reported
 #ifdef TPROD_SVT_DEBUG
   if (tid == 0 && f < 2) printf("svt f=%d m=%d n=%d G=%d sweeps=%d cycles=%lld\n", f, m, n, G, nsweeps, clock64() - t0);
 #endif
@@ -544,7 +675,8 @@ bool svt_supported(int64_t m, int64_t n) { return m >= 1 && n >= 1 && m <= SVT_M
 // iteration is issue-bound on one SM); columns are max(m, n) <= 64 long.  The pairs of a round
 // (ceil(min(m, n) / 2)) fill ceil(pairs * G / 32) warps.
 static int launch_svt_common(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n,
-                             int64_t h, int64_t fstride, float tau, double* sv, SvdOut fo, cudaStream_t s) {
+                             int64_t h, int64_t fstride, float tau, double* sv, SvdOut fo, int* status,
+                             cudaStream_t s) {
   if (!svt_supported(m, n)) return 6;
   // the slice (m n) and, unless only singular values are wanted, V (r x r, r = min(m, n))
   const int64_t len = std::max(m, n), r = std::min(m, n), pairs = (r + 1) / 2;
@@ -558,16 +690,16 @@ static int launch_svt_common(const float* re, const float* im, float* wre, float
   if (threads < 64) threads = 64;
   auto go = [&](auto kern) -> int {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 4;
-    kern<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, sv, fo);
+    kern<<<(unsigned)h, threads, smem, s>>>(re, im, wre, wim, (int)m, (int)n, fstride, tau, sv, fo, status);
     return cudaGetLastError() == cudaSuccess ? 0 : 4;
   };
   return G == 8 ? go(slice_svt_kernel<8>) : G == 16 ? go(slice_svt_kernel<16>) : go(slice_svt_kernel<32>);
 }
 
 int launch_slice_svt(const float* re, const float* im, float* wre, float* wim, int64_t m, int64_t n, int64_t h,
-                     int64_t fstride, float tau, cudaStream_t s) {
+                     int64_t fstride, float tau, int* status, cudaStream_t s) {
   return launch_svt_common(re, im, wre, wim, m, n, h, fstride, tau, nullptr,
-                           SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, s);
+                           SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, status, s);
 }
 
 // t-SVD scalars (NEXT-3).  sv: [h][r] per-slice singular values (r = min(m, n), non-increasing).
@@ -603,14 +735,15 @@ __global__ void tsvd_reduce_kernel(const double* __restrict__ sv, int r, int h, 
 }
 
 int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride,
-                             float* ure, float* uim, float* sre, float* vre, float* vim, cudaStream_t s) {
-  return launch_svt_common(re, im, nullptr, nullptr, m, n, h, fstride, 0.f, nullptr, SvdOut{ure, uim, sre, vre, vim}, s);
+                             float* ure, float* uim, float* sre, float* vre, float* vim, int* status, cudaStream_t s) {
+  return launch_svt_common(re, im, nullptr, nullptr, m, n, h, fstride, 0.f, nullptr, SvdOut{ure, uim, sre, vre, vim},
+                           status, s);
 }
 
 int launch_tsvd_values(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t n3, int64_t fstride,
-                       double* sv, float rtol, float* out, cudaStream_t s) {
+                       double* sv, float rtol, float* out, int* status, cudaStream_t s) {
   const int rc = launch_svt_common(re, im, nullptr, nullptr, m, n, h, fstride, 0.f, sv,
-                                   SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, s);
+                                   SvdOut{nullptr, nullptr, nullptr, nullptr, nullptr}, status, s);
   if (rc) return rc;
   tsvd_reduce_kernel<<<1, 64, 0, s>>>(sv, (int)std::min(m, n), (int)h, (int)n3, rtol, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 4;

@@ -333,18 +333,216 @@ __global__ void __launch_bounds__(256) bj_svt_out_kernel(const double2* __restri
   }
 }
 
+// Non-increasing order of the slice's sigma_j: perm[f][pos] = j (ties by index), sorted[f][pos] = sigma_j.
+__global__ void bj_rank_kernel(const double* __restrict__ sig, int n, int* __restrict__ perm,
+                               double* __restrict__ sorted) {
+  const int f = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double* sg = sig + (int64_t)f * n;
+  const double sj = sg[j];
+  int pos = 0;
+  for (int k = 0; k < n; ++k) {
+    const double sk = sg[k];
+    pos += (sk > sj) || (sk == sj && k < j);
+  }
+  if (perm) perm[(int64_t)f * n + pos] = j;
+  if (sorted) sorted[(int64_t)f * n + pos] = sj;
+}
+
+__device__ __forceinline__ double block_reduce(double v, bool is_max, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, t) : v + t;
+  }
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int k = 1; k < nw; ++k) r = is_max ? fmax(r, red[k]) : r + red[k];
+  return r;
+}
+
+// Left singular vectors of the processed slice: x_j / sigma_j, normalised in place (fp64).  A column
+// whose sigma is at the rounding level of the slice (sigma_j <= 1e-6 sigma_max: rank-deficient input)
+// has no reliable direction: it is replaced by the unit vector e_c of the row c least covered by the
+// columns so far (row coverage rc_i = sum_k |x_k[i]|^2; e_c keeps a residual >= 1 - k/m after the
+// projection), Gram-Schmidt-orthogonalised twice against all other columns and normalised -- the
+// same rule as the per-slice kernel, so U^* U = I (Theorem 2.2) for any rank.  One CTA per slice;
+// dots ([h][n]) and rc ([h][m]) are workspace.
+__global__ void __launch_bounds__(1024) bj_left_kernel(double2* __restrict__ X, const double* __restrict__ sig, int m,
+                                                       int n, int64_t xs, double2* __restrict__ dots,
+                                                       double* __restrict__ rcov) {
+  __shared__ double red[32];
+  __shared__ double bestv[32];
+  __shared__ int besti[32];
+  const int f = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  double2* x = X + (int64_t)f * xs;
+  const double* sg = sig + (int64_t)f * n;
+  double2* d = dots + (int64_t)f * n;
+  double* rc = rcov + (int64_t)f * m;
+  double mx = 0.0;
+  for (int k = tid; k < n; k += blockDim.x) mx = fmax(mx, sg[k]);
+  const double thr = block_reduce(mx, true, red) * 1e-6;
+  for (int64_t idx = tid; idx < (int64_t)m * n; idx += blockDim.x) {
+    const double sj = sg[idx / m];
+    const double inv = sj > thr ? 1.0 / sj : 0.0;
+    x[idx] = make_double2(x[idx].x * inv, x[idx].y * inv);
+  }
+  int z = 0;
+  for (int k = tid; k < n; k += blockDim.x) z += sg[k] > thr ? 0 : 1;
+  if (block_reduce((double)z, false, red) == 0.0) return;   // full rank: nothing to complete
+  for (int i = tid; i < m; i += blockDim.x) {
+    double c = 0.0;
+    for (int k = 0; k < n; ++k) c += x[(int64_t)k * m + i].x * x[(int64_t)k * m + i].x +
+                                     x[(int64_t)k * m + i].y * x[(int64_t)k * m + i].y;
+    rc[i] = c;
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (sg[j] > thr) continue;                               // block-uniform
+    double2* xj = x + (int64_t)j * m;
+    // least-covered row
+    double bv = 3.0;
+    int bi = 0;
+    for (int i = tid; i < m; i += blockDim.x)
+      if (rc[i] < bv) { bv = rc[i]; bi = i; }
+    for (int o = 16; o; o >>= 1) {
+      const double tv = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int ti = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (tv < bv || (tv == bv && ti < bi)) { bv = tv; bi = ti; }
+    }
+    if (lane == 0) { bestv[w] = bv; besti[w] = bi; }
+    __syncthreads();
+    int c = besti[0];
+    double cv = bestv[0];
+    for (int k = 1; k < nw; ++k)
+      if (bestv[k] < cv || (bestv[k] == cv && besti[k] < c)) { cv = bestv[k]; c = besti[k]; }
+    for (int i = tid; i < m; i += blockDim.x) xj[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int k = w; k < n; k += nw) {                      // d_k = x_k^H x_j (zero columns pending: 0)
+        double pr = 0.0, pi = 0.0;
+        if (k != j) {
+          const double2* y = x + (int64_t)k * m;
+          for (int i = lane; i < m; i += 32) {
+            const double2 a = y[i], b = xj[i];
+            pr += a.x * b.x + a.y * b.y;
+            pi += a.x * b.y - a.y * b.x;
+          }
+        }
+        for (int o = 16; o; o >>= 1) {
+          pr += __shfl_xor_sync(0xffffffffu, pr, o);
+          pi += __shfl_xor_sync(0xffffffffu, pi, o);
+        }
+        if (lane == 0) d[k] = make_double2(pr, pi);
+      }
+      __syncthreads();
+      for (int i = tid; i < m; i += blockDim.x) {            // x_j -= sum_k x_k d_k
+        double ar = 0.0, ai = 0.0;
+        for (int k = 0; k < n; ++k) {
+          const double2 a = x[(int64_t)k * m + i], dk = d[k];
+          ar += a.x * dk.x - a.y * dk.y;
+          ai += a.x * dk.y + a.y * dk.x;
+        }
+        xj[i] = make_double2(xj[i].x - ar, xj[i].y - ai);
+      }
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (int i = tid; i < m; i += blockDim.x) nn += xj[i].x * xj[i].x + xj[i].y * xj[i].y;
+    nn = block_reduce(nn, false, red);
+    const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+    for (int i = tid; i < m; i += blockDim.x) {
+      const double2 v = make_double2(xj[i].x * inv, xj[i].y * inv);
+      xj[i] = v;
+      rc[i] += v.x * v.x + v.y * v.y;
+    }
+    __syncthreads();
+  }
+}
+
+// Skinny factors in non-increasing sigma order (column pos = blockIdx.y): left vectors of the
+// processed slice (length m) and right vectors (length n); a transposed (wide) slice swaps the
+// roles: Y^H = L S R^H gives Y = R S L^H, i.e. U = R and V = L.  Column pos of S is written whole.
+__global__ void bj_factors_kernel(const double2* __restrict__ X, const double2* __restrict__ V,
+                                  const double* __restrict__ sig, const int* __restrict__ perm, int m, int n,
+                                  int64_t xs, int64_t vs, int tr, float* __restrict__ ure, float* __restrict__ uim,
+                                  float* __restrict__ sre, float* __restrict__ vre, float* __restrict__ vim) {
+  const int f = blockIdx.z, pos = blockIdx.y, r = n;
+  const int j = perm[(int64_t)f * n + pos];
+  const int M = tr ? n : m, N = tr ? m : n;                  // rows of the slice's U and V
+  float* lre = tr ? vre + (int64_t)f * N * r : ure + (int64_t)f * M * r;
+  float* lim = tr ? vim + (int64_t)f * N * r : uim + (int64_t)f * M * r;
+  float* rre = tr ? ure + (int64_t)f * M * r : vre + (int64_t)f * N * r;
+  float* rim = tr ? uim + (int64_t)f * M * r : vim + (int64_t)f * N * r;
+  const double2* xj = X + (int64_t)f * xs + (int64_t)j * m;
+  const double2* vj = V + (int64_t)f * vs + (int64_t)j * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    lre[(int64_t)pos * m + i] = (float)xj[i].x;
+    lim[(int64_t)pos * m + i] = (float)xj[i].y;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    rre[(int64_t)pos * n + i] = (float)vj[i].x;
+    rim[(int64_t)pos * n + i] = (float)vj[i].y;
+    sre[(int64_t)f * r * r + (int64_t)pos * r + i] = i == pos ? (float)sig[(int64_t)f * n + j] : 0.f;
+  }
+}
+
+// A slice whose last allowed sweep still rotated is not certified converged: reported, not silent.
+__global__ void bj_status_kernel(const int* __restrict__ flags, int h, int* __restrict__ status) {
+  for (int f = threadIdx.x; f < h; f += blockDim.x)
+    if (flags[f * MAX_SWEEPS + MAX_SWEEPS - 1]) atomicOr(status, STATUS_NOCONV);
+}
+
+// t-SVD scalars (Eq. (14), Def. 2.8, 2.9, Eq. (16)) from sorted per-slice singular values, any r:
+// out[i] = (1/n3) sum_{j < n3} S-bar(i,i,j) (conjugate slices counted twice), out[r] = TNN,
+// out[r+1] = TSN = max_f sv[f][0], out[r+2] = #{i : out[i] > rtol out[0]}.  One CTA.
+__global__ void __launch_bounds__(1024) bj_reduce_kernel(const double* __restrict__ sv, int r, int h, int n3,
+                                                         float rtol, float* __restrict__ out) {
+  __shared__ double red[32];
+  auto S = [&](int i) {
+    double acc = 0.0;
+    for (int f = 0; f < h; ++f) acc += ((f == 0 || 2 * f == n3) ? 1.0 : 2.0) * sv[(int64_t)f * r + i];
+    return acc / n3;
+  };
+  const double s0 = S(0);
+  double tnn = 0.0, rank = 0.0, tsn = 0.0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    const double si = S(i);
+    out[i] = (float)si;
+    tnn += si;
+    rank += (s0 > 0.0 && si > (double)rtol * s0) ? 1.0 : 0.0;
+  }
+  for (int f = threadIdx.x; f < h; f += blockDim.x) tsn = fmax(tsn, sv[(int64_t)f * r]);
+  tnn = block_reduce(tnn, false, red);
+  rank = block_reduce(rank, false, red);
+  tsn = block_reduce(tsn, true, red);
+  if (threadIdx.x == 0) {
+    out[r] = (float)tnn;
+    out[r + 1] = (float)tsn;
+    out[r + 2] = (float)rank;
+  }
+}
+
 }  // namespace
 
 size_t bj_workspace_bytes(int64_t m_in, int64_t n_in, int64_t h) {
   const int64_t m = std::max(m_in, n_in), n = std::min(m_in, n_in);
-  return 16 * (size_t)h * (size_t)(m * n + n * n) + 8 * (size_t)h * n + 4 * (size_t)h * MAX_SWEEPS + 4096;
+  // X, V, sigma, flags, perm, dots, row coverage (+ alignment slack)
+  return 16 * (size_t)h * (size_t)(m * n + n * n) + 8 * (size_t)h * n + 4 * (size_t)h * MAX_SWEEPS +
+         4 * (size_t)h * n + 16 * (size_t)h * n + 8 * (size_t)h * m + 8192;
+}
+
+int launch_tsvd_reduce(const double* sv, int64_t r, int64_t h, int64_t n3, float rtol, float* out, cudaStream_t s) {
+  bj_reduce_kernel<<<1, 1024, 0, s>>>(sv, (int)r, (int)h, (int)n3, rtol, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
 // Blocked Jacobi of all h spectral slices (re / im planes [f][col][row], m_in x n_in, pitch
-// fstride) in the workspace `ws` (bj_workspace_bytes).  tau >= 0: t-SVT into wre / wim; tau < 0:
-// the singular values only, into `sig_out` (h x min(m, n) doubles, unsorted per slice).
-int launch_block_svt(const float* re, const float* im, int64_t m_in, int64_t n_in, int64_t h, int64_t fstride,
-                     float tau, float* wre, float* wim, double* sig_out, void* ws, cudaStream_t s) {
+// fstride) in the workspace `ws` (bj_workspace_bytes); `mode` / `o` as in internal.h.
+int launch_block_svd(const float* re, const float* im, int64_t m_in, int64_t n_in, int64_t h, int64_t fstride,
+                     int mode, BjOut o, void* ws, int* status, cudaStream_t s) {
   const bool tr = m_in < n_in;
   const int m = (int)std::max(m_in, n_in), n = (int)std::min(m_in, n_in);
   const int64_t xs = (int64_t)m * n, vs = (int64_t)n * n;
@@ -352,6 +550,9 @@ int launch_block_svt(const float* re, const float* im, int64_t m_in, int64_t n_i
   double2* V = X + h * xs;
   double* sig = (double*)(V + h * vs);
   int* flags = (int*)(sig + h * n);
+  int* perm = flags + h * MAX_SWEEPS;
+  double2* dots = (double2*)(((uintptr_t)(perm + h * n) + 15) & ~(uintptr_t)15);
+  double* rcov = (double*)(dots + h * n);
   cudaMemsetAsync(flags, 0, 4 * (size_t)h * MAX_SWEEPS, s);
   {
     const int64_t work = (int64_t)m * n;
@@ -360,19 +561,16 @@ int launch_block_svt(const float* re, const float* im, int64_t m_in, int64_t n_i
                                                         xs, vs);
   }
   const int nb = (n + BJ - 1) / BJ;
-  const int nbp = nb + (nb & 1);                                   // even number of players
+  const int nbp = std::max(2, nb + (nb & 1));                     // even number of players (>= 2)
   const size_t smem = sizeof(double2) * (2 * BS + ROWS) * LP;
   if (cudaFuncSetAttribute(bj_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return 4;
-  if (nb == 1) {
-    // a single block: one "pair" of block 0 with the empty block 1 orthogonalises all n columns
-    for (int sw = 0; sw < 2; ++sw)
-      bj_round_kernel<<<dim3(1, (unsigned)h), BJ_THREADS, smem, s>>>(X, V, m, n, xs, vs, 2, 0, sw, flags);
-  } else {
-    for (int sw = 0; sw < MAX_SWEEPS; ++sw)
-      for (int r = 0; r < nbp - 1; ++r)
-        bj_round_kernel<<<dim3(nbp / 2, (unsigned)h), BJ_THREADS, smem, s>>>(X, V, m, n, xs, vs, nbp, r, sw, flags);
-  }
+  // a single block (n <= 32) is the pair (block 0, empty block 1); every sweep's launches return at
+  // once for a slice whose previous sweep rotated nothing
+  for (int sw = 0; sw < MAX_SWEEPS; ++sw)
+    for (int r = 0; r < nbp - 1; ++r)
+      bj_round_kernel<<<dim3(nbp / 2, (unsigned)h), BJ_THREADS, smem, s>>>(X, V, m, n, xs, vs, nbp, r, sw, flags);
+  if (status) bj_status_kernel<<<1, 256, 0, s>>>(flags, (int)h, status);
 #ifdef TPROD_SVT_DEBUG
   {
     std::vector<int> fl((size_t)h * MAX_SWEEPS);
@@ -385,10 +583,19 @@ int launch_block_svt(const float* re, const float* im, int64_t m_in, int64_t n_i
     }
   }
 #endif
-  bj_sigma_kernel<<<dim3((n * 32 + 255) / 256, (unsigned)h), 256, 0, s>>>(X, m, n, xs, sig_out ? sig_out : sig);
-  if (tau >= 0.f) {
+  bj_sigma_kernel<<<dim3((n * 32 + 255) / 256, (unsigned)h), 256, 0, s>>>(X, m, n, xs, sig);
+  if (mode == BJ_SVT) {
     dim3 g((unsigned)((m + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)h);
-    bj_svt_out_kernel<<<g, 256, 0, s>>>(X, V, sig, m, n, xs, vs, tau, tr ? 1 : 0, (int)m_in, wre, wim, fstride);
+    bj_svt_out_kernel<<<g, 256, 0, s>>>(X, V, sig, m, n, xs, vs, o.tau, tr ? 1 : 0, (int)m_in, o.wre, o.wim, fstride);
+  } else if (mode == BJ_VALUES) {
+    bj_rank_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)h), 256, 0, s>>>(sig, n, nullptr, o.sv);
+  } else {
+    bj_rank_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)h), 256, 0, s>>>(sig, n, perm, nullptr);
+    bj_left_kernel<<<(unsigned)h, 1024, 0, s>>>(X, sig, m, n, xs, dots, rcov);
+    const int gx = std::min(8, (m + 255) / 256);
+    bj_factors_kernel<<<dim3((unsigned)gx, (unsigned)n, (unsigned)h), 256, 0, s>>>(X, V, sig, perm, m, n, xs, vs,
+                                                                                  tr ? 1 : 0, o.ure, o.uim, o.sre,
+                                                                                  o.vre, o.vim);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }

@@ -94,10 +94,12 @@ def test_poisoned_workspace_and_guarded_buffers(T, case):
         h.release_a()
 
 
-@pytest.mark.parametrize("dims", [(24, 20, 9), (33, 17, 64), (8, 12, 4096)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("dims", [(24, 20, 9), (33, 17, 64), (8, 12, 4096), (100, 72, 5), (130, 130, 3)],
+                         ids=lambda d: "x".join(map(str, d)))
 def test_poisoned_next_rows(T, dims):
-    """t-SVT, t-SVD scalars, tinv and the forward stage entry with a poisoned workspace and guarded
-    outputs."""
+    """t-SVT, t-SVD scalars and factors, tinv and the forward stage entry with a poisoned workspace
+    and guarded outputs (the last two shapes take the blocked Jacobi and the global-memory
+    Gauss-Jordan)."""
     import torch
     n1, n2, n3 = dims
     h = T.Handle()
@@ -111,6 +113,9 @@ def test_poisoned_next_rows(T, dims):
     assert O.rel_err(dX.cpu().numpy(), O.tsvt(Y.astype(np.float64), 2.0)) <= 1e-5
     out = T.tsvd_values(dY, rtol=1e-6, handle=h).cpu().numpy()
     assert np.isfinite(out).all()
+    U, S, V = (x.cpu().numpy() for x in T.tsvd(dY, handle=h))
+    _, S_ref, _ = O.tsvd(Y.astype(np.float64))
+    assert O.rel_err(S, S_ref) <= 1e-5 and np.isfinite(U).all() and np.isfinite(V).all()
     n = min(n1, n2)
     Z = normal((n, n, n3), 71 + n3, np.float64) * (0.2 / np.sqrt(n3))   # spectral slices 2 I + O(0.2)
     Z[:, :, 0] += 2.0 * np.eye(n)

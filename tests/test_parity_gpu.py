@@ -337,10 +337,12 @@ def _well_conditioned(n, n3, seed):
     return A.astype(np.float32)
 
 
-@pytest.mark.parametrize("n,n3", [(1, 1), (5, 4), (32, 7), (96, 2), (16, 64), (8, 100)])
+@pytest.mark.parametrize("n,n3", [(1, 1), (5, 4), (32, 7), (96, 2), (16, 64), (8, 100), (97, 2), (128, 5),
+                                  (200, 3)])
 def test_tinv_gpu_vs_oracle(T, n, n3):
-    """tinv (Def. 2.4) through the production transforms + per-slice Gauss-Jordan vs the oracle's
-    literal bcirc solve, and both sides of Eq. (11) in the oracle."""
+    """tinv (Def. 2.4) through the production transforms + per-slice Gauss-Jordan (n <= 96 in shared
+    memory, larger in global memory in fp64) vs the oracle's literal bcirc solve, and both sides of
+    Eq. (11) in the oracle."""
     A = _well_conditioned(n, n3, 93 + n)
     X = host(T.tinv(dev(A)))
     ref = O.tinv(A)
@@ -367,9 +369,28 @@ def test_tinv_gpu_long_tubes_and_errors(T):
     with pytest.raises(T.TprodError) as e:
         T.tinv(dev(np.real(O.idft_mode3(Ab)).astype(np.float32)))
     assert e.value.status == T._lib.TPROD_ESINGULAR
-    with pytest.raises(T.TprodError) as e:
-        T.tinv(dev(_well_conditioned(97, 2, 1)))
-    assert e.value.status == T._lib.TPROD_EUNSUPPORTED
+    with pytest.raises(T.TprodError) as e:                # large-slice path, singular
+        T.tinv(dev(np.zeros((100, 100, 3), np.float32)))
+    assert e.value.status == T._lib.TPROD_ESINGULAR
+    Y = dev(np.zeros((4, 4, 3), np.float32))
+    assert T._lib.lib().tprod_tinv_f32(Y.data_ptr(), Y.data_ptr() + 4096, 8193, 1, None,
+                                       T.Handle().ptr) == T._lib.TPROD_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("n", [6, 120], ids=["smem", "global"])
+def test_tinv_async_status(T, n):
+    """TPROD_OPT_SYNC_CHECKS = 0: tinv returns at once and a singular tensor is reported through the
+    handle's status word (TPROD_STATUS_SINGULAR), which tprod_status clears; a regular tensor leaves
+    it 0 and still matches the oracle."""
+    h = T.Handle()
+    h.set_option(T._lib.TPROD_OPT_SYNC_CHECKS, 0)
+    T.tinv(dev(np.zeros((n, n, 3), np.float32)), handle=h)          # no exception
+    assert h.status() == T._lib.TPROD_STATUS_SINGULAR
+    assert h.status() == 0                                           # cleared by the read
+    A = _well_conditioned(n, 3, 7)
+    X = host(T.tinv(dev(A), handle=h))
+    assert h.status() == 0
+    assert O.rel_err(X, O.tinv(A)) <= 1e-5
 
 
 @pytest.mark.parametrize("dims,tau", [((5, 4, 6), 1.5), ((64, 64, 7), 20.0), ((33, 17, 31), 8.0),
@@ -390,7 +411,8 @@ def test_tsvt_gpu_vs_oracle(T, dims, tau):
 
 
 @pytest.mark.parametrize("dims,tau", [((96, 80, 5), 8.0), ((65, 130, 3), 6.0), ((256, 256, 3), 20.0),
-                                      ((200, 72, 9), 0.0), ((300, 40, 16), 1e6)],
+                                      ((200, 72, 9), 0.0), ((300, 40, 16), 1e6), ((200, 20, 5), 3.0),
+                                      ((7, 150, 4), 2.0)],
                          ids=lambda d: "x".join(map(str, d)) if isinstance(d, tuple) else str(d))
 def test_tsvt_large_slices_gpu_vs_oracle(T, dims, tau):
     """t-SVT (Algorithm 3) for slices beyond 64 x 64: the blocked one-sided Jacobi (column blocks of
@@ -399,7 +421,9 @@ def test_tsvt_large_slices_gpu_vs_oracle(T, dims, tau):
     zero (Eq. (19)-(21))."""
     n1, n2, n3 = dims
     Y = normal((n1, n2, n3), 171 + n3)
-    X = host(T.tsvt(dev(Y), tau))
+    h = T.Handle()
+    X = host(T.tsvt(dev(Y), tau, handle=h))
+    assert h.status() == 0                                # every slice converged
     ref = O.tsvt(Y.astype(np.float64), tau)
     if tau >= 1e6:
         assert np.abs(X).max() <= 1e-6 * np.abs(Y).max()
@@ -423,11 +447,13 @@ def test_tsvt_1024x1024x31_gpu(T):
     assert err <= 1e-5
 
 
-@pytest.mark.parametrize("dims", [(6, 5, 7), (64, 64, 8), (40, 12, 33), (16, 16, 100)],
+@pytest.mark.parametrize("dims", [(6, 5, 7), (64, 64, 8), (40, 12, 33), (16, 16, 100), (100, 70, 5),
+                                  (65, 130, 8), (300, 20, 3)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_tsvd_values_gpu_vs_oracle(T, dims):
-    """t-SVD scalars on the GPU (per-slice Jacobi SVD + Eq. (14) reduction) vs the oracle: singular
-    values, TNN, TSN (the oracle's through bcirc), tubal rank."""
+    """t-SVD scalars on the GPU (per-slice Jacobi SVD -- one CTA per slice up to 64 x 64, blocked
+    beyond -- + Eq. (14) reduction) vs the oracle: singular values, TNN, TSN (the oracle's through
+    bcirc), tubal rank."""
     n1, n2, n3 = dims
     A = normal((n1, n2, n3), 111 + n3)
     out = host(T.tsvd_values(dev(A), rtol=1e-6))
@@ -438,16 +464,19 @@ def test_tsvd_values_gpu_vs_oracle(T, dims):
     assert int(out[r + 2]) == rank
 
 
-def test_tsvd_tubal_rank_gpu(T):
-    """Tubal rank of U * V (Def. 2.7) with U 40 x 5 x 31, V 5 x 30 x 31 is 5 on the GPU."""
-    U = normal((40, 5, 31), 121, np.float64)
-    V = normal((5, 30, 31), 122, np.float64)
+@pytest.mark.parametrize("n1,n2", [(40, 30), (150, 90)])
+def test_tsvd_tubal_rank_gpu(T, n1, n2):
+    """Tubal rank of U * V (Def. 2.7) with U n1 x 5 x 31, V 5 x n2 x 31 is 5 on the GPU (small and
+    blocked Jacobi)."""
+    U = normal((n1, 5, 31), 121, np.float64)
+    V = normal((5, n2, 31), 122, np.float64)
     A = O.tprod_bcirc(U, V).astype(np.float32)
     out = host(T.tsvd_values(dev(A), rtol=1e-4))
-    assert int(out[30 + 2]) == 5
+    assert int(out[min(n1, n2) + 2]) == 5
 
 
-@pytest.mark.parametrize("dims", [(6, 4, 5), (3, 7, 4), (64, 48, 9), (20, 64, 31), (8, 8, 64)],
+@pytest.mark.parametrize("dims", [(6, 4, 5), (3, 7, 4), (64, 48, 9), (20, 64, 31), (8, 8, 64), (100, 70, 5),
+                                  (40, 130, 4), (200, 10, 3)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_tsvd_factors_gpu(T, dims):
     """Skinny t-SVD on the GPU: S equals the oracle's (unique); U, V (unique only up to phases) are
@@ -465,7 +494,8 @@ def test_tsvd_factors_gpu(T, dims):
     assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, n3)) <= 1e-5
 
 
-@pytest.mark.parametrize("dims,rank", [((8, 8, 5), 2), ((12, 20, 7), 3), ((16, 6, 4), 0)],
+@pytest.mark.parametrize("dims,rank", [((8, 8, 5), 2), ((12, 20, 7), 3), ((16, 6, 4), 0), ((100, 80, 5), 3),
+                                       ((70, 90, 3), 0), ((40, 130, 4), 2)],
                          ids=lambda d: "x".join(map(str, d)) if isinstance(d, tuple) else str(d))
 def test_tsvd_factors_rank_deficient(T, dims, rank):
     """Theorem 2.2 asks for orthogonal factors also when A is rank-deficient: with A = U0 * V0 of
@@ -503,10 +533,9 @@ def test_next_rows_argument_errors(T):
     assert L.tprod_tsvt_f32(Y.data_ptr(), X.data_ptr(), 4, 3, 5, C_float(-1.0), None, h.ptr) == T._lib.TPROD_EINVAL
     assert L.tprod_tsvt_f32(Y.data_ptr(), X.data_ptr(), 4, 3, 5, C_float(float("nan")), None, h.ptr) == T._lib.TPROD_EINVAL
     assert L.tprod_tsvt_f32(Y.data_ptr(), Y.data_ptr(), 4, 3, 5, C_float(1.0), None, h.ptr) == T._lib.TPROD_EALIAS
-    big = dev(normal((65, 3, 2), 3))
-    with pytest.raises(T.TprodError) as e:                # (t-SVT takes any size: blocked Jacobi)
-        T.tsvd_values(big)
-    assert e.value.status == T._lib.TPROD_EUNSUPPORTED
+    # every slice size up to min(n1, n2) = 65535 runs (blocked Jacobi); beyond: unsupported, nothing read
+    assert L.tprod_tsvd_values_f32(Y.data_ptr(), 65536, 65536, 1, C_float(1e-6), X.data_ptr(), None,
+                                   h.ptr) == T._lib.TPROD_EUNSUPPORTED
     assert L.tprod_tran_f32(Y.data_ptr(), Y.data_ptr(), 4, 3, 5, None, h.ptr) == T._lib.TPROD_EALIAS
     assert L.tprod_teye_f32(None, 3, 2, None, h.ptr) == T._lib.TPROD_EINVAL
     assert L.tprod_tinv_f32(Y.data_ptr(), X.data_ptr(), 0, 5, None, h.ptr) == T._lib.TPROD_EINVAL
