@@ -265,24 +265,35 @@ def tsvd_values(A: np.ndarray, rtol: float = 1e-10):
     return s, float(s.sum()), tsn, rank
 
 
-def tsvd(A: np.ndarray):
-    """Algorithm 2, T-SVD, step by step, in its skinny form (r = min(n1, n2)
-    columns, reading R17): A-bar = fft(A, [], 3); for i = 1..ceil((n3+1)/2):
-    [U-bar, S-bar, V-bar] = SVD(A-bar^(i)); the rest by conjugation (S-bar copied); U = ifft(U-bar),
-    S = ifft(S-bar), V = ifft(V-bar).  Returns (U n1 x r x n3, S r x r x n3, V n2 x r x n3) with
-    A = U * S * V^* (Theorem 2.2, Eq. (12)).  The factors are unique up to a unit phase per
-    singular vector and spectral slice; S is unique."""
+def tsvd(A: np.ndarray, full: bool = False):
+    """Algorithm 2, T-SVD, step by step: A-bar = fft(A, [], 3); for
+    i = 1..ceil((n3+1)/2): [U-bar, S-bar, V-bar] = SVD(A-bar^(i)); the rest by conjugation (S-bar
+    copied); U = ifft(U-bar), S = ifft(S-bar), V = ifft(V-bar).  full=False: the skinny form (r =
+    min(n1, n2) columns, DESIGN.md reading R17), U n1 x r x n3, S r x r x n3, V n2 x r x n3;
+    full=True: Theorem 2.2's shapes, U n1 x n1 x n3, S n1 x n2 x n3 (f-diagonal), V n2 x n2 x n3.
+    Either way A = U * S * V^* (Eq. (12)).  The factors are unique up to a unit phase per singular
+    vector and spectral slice (and, full, up to a unitary mix of the null-space columns); S is
+    unique."""
     A = np.asarray(A, dtype=np.float64)
     n1, n2, n3 = A.shape
     r = min(n1, n2)
+    cu, cv = (n1, n2) if full else (r, r)
     Ab = dft_mode3(A)
-    Ub = np.empty((n1, r, n3), dtype=np.complex128)
-    Sb = np.zeros((r, r, n3), dtype=np.complex128)
-    Vb = np.empty((n2, r, n3), dtype=np.complex128)
+    Ub = np.empty((n1, cu, n3), dtype=np.complex128)
+    Sb = np.zeros((cu, cv, n3), dtype=np.complex128)
+    Vb = np.empty((n2, cv, n3), dtype=np.complex128)
     hh = h_slices(n3)
     for i in range(1, hh + 1):
-        U, S, Vh = np.linalg.svd(Ab[:, :, i - 1], full_matrices=False)
-        Ub[:, :, i - 1], Sb[:, :, i - 1], Vb[:, :, i - 1] = U, np.diag(S), Vh.conj().T
+        M = Ab[:, :, i - 1]
+        if i == 1 or 2 * (i - 1) == n3:
+            # Eq. (8) (PAPER.md:L142-145): the self-conjugate slices (DC, and Nyquist for even n3)
+            # are real; the literal DFT leaves ~1e-16 imaginary noise, which would let LAPACK pick
+            # complex null-space vectors that the conjugate fill cannot represent (DESIGN.md R19)
+            M = M.real
+        U, S, Vh = np.linalg.svd(M, full_matrices=full)
+        Sd = np.zeros((cu, cv))
+        Sd[np.arange(r), np.arange(r)] = S
+        Ub[:, :, i - 1], Sb[:, :, i - 1], Vb[:, :, i - 1] = U, Sd, Vh.conj().T
     for i in range(hh + 1, n3 + 1):
         j = (n3 - i + 2) - 1
         Ub[:, :, i - 1], Sb[:, :, i - 1], Vb[:, :, i - 1] = np.conj(Ub[:, :, j]), Sb[:, :, j], np.conj(Vb[:, :, j])

@@ -462,3 +462,28 @@ def test_tsvd_factors_pins():
             off[:, :, k] -= np.diag(np.diag(S[:, :, k]))
         assert np.abs(off).max() < 1e-13
         np.testing.assert_allclose(np.diag(S[:, :, 0]), O.tsvd_values(A)[0], rtol=1e-12)
+
+
+def test_tsvd_full_factors_pins():
+    """Theorem 2.2 in its stated shapes: U n1 x n1, S n1 x n2 f-diagonal,
+    V n2 x n2 with A = U * S * V^* and BOTH U^* * U = U * U^* = I_n1 and V^* * V = V * V^* = I_n2
+    (orthogonal, Def. 2.5: square, so the product in either order is the identity); S's leading
+    r x r block equals the skinny S; tall, wide and rank-deficient shapes."""
+    U0 = normal((7, 2, 4), 36, np.float64)
+    V0 = normal((2, 5, 4), 37, np.float64)
+    cases = ((normal((6, 4, 5), 34, np.float64)), normal((3, 7, 4), 35, np.float64), O.tprod_bcirc(U0, V0))
+    for A in cases:
+        n1, n2, n3 = A.shape
+        r = min(n1, n2)
+        U, S, V = O.tsvd(A, full=True)
+        assert U.shape == (n1, n1, n3) and S.shape == (n1, n2, n3) and V.shape == (n2, n2, n3)
+        assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A) < 1e-13
+        for Q, n in ((U, n1), (V, n2)):
+            assert O.rel_err(O.tprod_bcirc(O.tran(Q), Q), O.teye(n, n3)) < 1e-13
+            assert O.rel_err(O.tprod_bcirc(Q, O.tran(Q)), O.teye(n, n3)) < 1e-13
+        off = S.copy()
+        for k in range(n3):
+            off[np.arange(r), np.arange(r), k] = 0.0
+        assert np.abs(off).max() < 1e-13
+        _, Ss, _ = O.tsvd(A)
+        assert O.rel_err(S[:r, :r, :], Ss) < 1e-13
