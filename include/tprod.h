@@ -145,6 +145,17 @@ int tprod_tsvd_values_f32(const float* A, int64_t n1, int64_t n2, int64_t n3, fl
  * Asynchronous; non-convergence as tprod_tsvt_f32. */
 int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3, void* stream,
                    tprod_handle h);
+/* Full t-SVD (Theorem 2.2 in its stated shapes, Eq. (12)): A = U * S * V^* with
+ * U n1 x n1 x n3 and V n2 x n2 x n3 orthogonal (U^* U = U U^* = I) and S n1 x n2 x n3 f-diagonal, all
+ * DEVICE pointers in Matlab layout, max(n1, n2) <= 65535.  Per spectral slice f < h the blocked
+ * Jacobi SVD (any size) with the left basis of the processed slice completed to max(n1, n2)
+ * orthonormal columns (the unit vector of the least-covered row, Gram-Schmidt twice, fp64); the
+ * self-conjugate slices are taken as exactly real (Eq. (8), R19).  Columns follow
+ * non-increasing singular values; the null-space columns are one valid orthonormal completion.
+ * Workspace about 16 (m^2 + n^2) h bytes (m = max, n = min(n1, n2)).  Asynchronous;
+ * non-convergence as tprod_tsvt_f32. */
+int tprod_tsvd_full_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3,
+                        void* stream, tprod_handle h);
 
 /* Same in fp64 (all arithmetic fp64). */
 int tprod_f64(const double* A, const double* B, double* C,

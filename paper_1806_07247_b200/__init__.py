@@ -18,7 +18,7 @@ import ctypes as C
 from . import _lib
 from ._lib import TprodError, check, lib, strerror, workspace_bytes  # noqa: F401
 
-__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tsvd_values", "tsvd", "tprod_f32_host", "tprod_f64_host",
+__all__ = ["Handle", "tprod", "tprod_f32", "tprod_f64", "tprod_prepared", "tran", "teye", "tinv", "tsvt", "tsvd_values", "tsvd", "tsvd_full", "tprod_f32_host", "tprod_f64_host",
            "matlab_empty", "to_matlab", "is_matlab_layout", "dft_f32", "idft_f32",
            "nccl_unique_id", "workspace_bytes", "TprodError", "h_slices"]
 
@@ -318,6 +318,22 @@ def tsvd(A, handle=None, stream=None):
     h, s = _h_s(A, handle, stream)
     check(lib().tprod_tsvd_f32(A.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), n1, n2, n3, s, h.ptr),
           "tprod_tsvd_f32")
+    return U, S, V
+
+
+def tsvd_full(A, handle=None, stream=None):
+    """Full t-SVD (Theorem 2.2) of a float32 n1 x n2 x n3 CUDA tensor: returns (U n1 x n1 x n3,
+    S n1 x n2 x n3, V n2 x n2 x n3) with A = U * S * V^*, U and V orthogonal."""
+    import torch
+    if A.dim() != 3 or A.dtype != torch.float32 or not A.is_cuda or not is_matlab_layout(A):
+        raise ValueError("tsvd_full needs a float32 3-D CUDA tensor in the Matlab layout")
+    n1, n2, n3 = (int(x) for x in A.shape)
+    U = matlab_empty(n1, n1, n3, torch.float32, A.device)
+    S = matlab_empty(n1, n2, n3, torch.float32, A.device)
+    V = matlab_empty(n2, n2, n3, torch.float32, A.device)
+    h, s = _h_s(A, handle, stream)
+    check(lib().tprod_tsvd_full_f32(A.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), n1, n2, n3, s, h.ptr),
+          "tprod_tsvd_full_f32")
     return U, S, V
 
 

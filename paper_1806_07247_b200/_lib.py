@@ -49,6 +49,7 @@ SIGNATURES = {
     "tprod_tsvt_f32": (_int, [_vp, _vp, _i64, _i64, _i64, C.c_float, _vp, _vp]),
     "tprod_tsvd_values_f32": (_int, [_vp, _i64, _i64, _i64, C.c_float, _vp, _vp, _vp]),
     "tprod_tsvd_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
+    "tprod_tsvd_full_f32": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp]),
 }
 
 _lib = None

@@ -684,6 +684,10 @@ int spectral_planes(tprod_ctx* h, const float* Y, int64_t n1, int64_t n2, int64_
   launch_absmax(Y, n1, n2, n3, 0, mx, s);
   launch_fwd_split(Y, n1, n2, n3, 0, mx, T, sp, ld, u, h->num_sms, s);
   launch_decode_split(sp, ld, n1, n2, n3, 0, u, *re, *im, s);
+  // Eq. (8): the DC slice and (n3 even) the Nyquist slice are real; their imaginary planes are set
+  // to exact zeros, so the per-slice SVD of those slices stays real (R19)
+  CK(cudaMemsetAsync(*im, 0, 4 * (size_t)mn, s));
+  if (n3 % 2 == 0) CK(cudaMemsetAsync(*im + (n3 / 2) * mn, 0, 4 * (size_t)mn, s));
   *Tout = T;
   return launch_status();
 }
@@ -951,6 +955,46 @@ int tprod_tsvd_f32(const float* A, float* U, float* S, float* V, int64_t n1, int
   launch_inv_f32(ure, uim, n1, nu, n1, r, n3, T, OutUnscale{}, U, h->num_sms, s);
   launch_inv_f32(sre, sim, r, ns, r, r, n3, T, OutUnscale{}, S, h->num_sms, s);
   launch_inv_f32(vre, vim, n2, nv, n2, r, n3, T, OutUnscale{}, V, h->num_sms, s);
+  h->last_launches = 8;
+  return launch_status();
+}
+
+int tprod_tsvd_full_f32(const float* A, float* U, float* S, float* V, int64_t n1, int64_t n2, int64_t n3,
+                        void* stream, tprod_handle h) {
+  if (!h || !A || !U || !S || !V) return TPROD_EINVAL;
+  int st = validate_dims(n1, n2, n3, 1);
+  if (st) return st;
+  if (std::max(n1, n2) > 65535) return TPROD_EUNSUPPORTED;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t hh = h_slices(n3);
+  const int64_t nu = n1 * n1, ns = n1 * n2, nv = n2 * n2;
+  float *re, *im;
+  void* extra;
+  Twiddles32 T;
+  const size_t fbytes = align_up(4 * (size_t)(hh * (2 * nu + 2 * ns + 2 * nv)), 1024);
+  const size_t ex = fbytes + bj_workspace_bytes(n1, n2, hh, true);
+  if ((st = spectral_planes(h, A, n1, n2, n3, ex, &re, &im, &extra, &T, s))) return st;   // Alg. 2 step 1
+  float* ure = (float*)extra;
+  float* uim = ure + hh * nu;
+  float* sre = uim + hh * nu;
+  float* sim = sre + hh * ns;
+  float* vre = sim + hh * ns;
+  float* vim = vre + hh * nv;
+  CK(cudaMemsetAsync(sim, 0, 4 * (size_t)(hh * ns), s));                                  // S-bar is real
+  BjOut o{};
+  o.ure = ure;
+  o.uim = uim;
+  o.sre = sre;
+  o.vre = vre;
+  o.vim = vim;
+  // step 2: full SVD of every spectral slice (blocked Jacobi for all sizes; the left basis of the
+  // processed slice completed to max(n1, n2) orthonormal columns)
+  if (launch_block_svd(re, im, n1, n2, hh, n1 * n2, BJ_FACTORS_FULL, o, (char*)extra + fbytes, h->status, s))
+    return TPROD_ECUDA;
+  launch_inv_f32(ure, uim, n1, nu, n1, n1, n3, T, OutUnscale{}, U, h->num_sms, s);          // step 2b + 3
+  launch_inv_f32(sre, sim, n1, ns, n1, n2, n3, T, OutUnscale{}, S, h->num_sms, s);
+  launch_inv_f32(vre, vim, n2, nv, n2, n2, n3, T, OutUnscale{}, V, h->num_sms, s);
   h->last_launches = 8;
   return launch_status();
 }

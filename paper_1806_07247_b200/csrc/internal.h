@@ -121,17 +121,18 @@ int launch_slice_svd_factors(const float* re, const float* im, int64_t m, int64_
 // Blocked one-sided Jacobi of every spectral slice (tsvt_block.cu), any slice size.  BJ_SVT: t-SVT
 // with threshold tau into wre / wim (planes [f][col][row] of the m x n slice, pitch fstride);
 // BJ_VALUES: the singular values of every slice, non-increasing, into sv ([h][min(m, n)]);
-// BJ_FACTORS: skinny factors into ure/uim ([h][r][m]), sre ([h][r][r], real), vre/vim ([h][r][n]).
+// BJ_FACTORS: skinny factors into ure/uim ([h][r][m]), sre ([h][r][r], real), vre/vim ([h][r][n]);
+// BJ_FACTORS_FULL: full factors, ure/uim [h][m][m], sre [h][n][m] (f-diagonal), vre/vim [h][n][n].
 // `status` (device int) gets STATUS_NOCONV or-ed in when a slice hits the sweep cap.
 constexpr int STATUS_SINGULAR = 1, STATUS_NOCONV = 2;
-enum { BJ_SVT = 0, BJ_VALUES = 1, BJ_FACTORS = 2 };
+enum { BJ_SVT = 0, BJ_VALUES = 1, BJ_FACTORS = 2, BJ_FACTORS_FULL = 3 };
 struct BjOut {
   float tau;
   float *wre, *wim;                  // BJ_SVT
   double* sv;                        // BJ_VALUES
   float *ure, *uim, *sre, *vre, *vim;  // BJ_FACTORS
 };
-size_t bj_workspace_bytes(int64_t m, int64_t n, int64_t h);
+size_t bj_workspace_bytes(int64_t m, int64_t n, int64_t h, bool full = false);
 int launch_block_svd(const float* re, const float* im, int64_t m, int64_t n, int64_t h, int64_t fstride, int mode,
                      BjOut o, void* ws, int* status, cudaStream_t s);
 // t-SVD scalars from per-slice singular values sv ([h][r], non-increasing), any r (tsvt_block.cu)

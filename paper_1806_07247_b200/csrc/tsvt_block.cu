@@ -462,30 +462,40 @@ __global__ void __launch_bounds__(1024) bj_left_kernel(double2* __restrict__ X, 
   }
 }
 
-// Skinny factors in non-increasing sigma order (column pos = blockIdx.y): left vectors of the
-// processed slice (length m) and right vectors (length n); a transposed (wide) slice swaps the
-// roles: Y^H = L S R^H gives Y = R S L^H, i.e. U = R and V = L.  Column pos of S is written whole.
+// Factors in non-increasing sigma order (column pos = blockIdx.y): ml left vectors of the processed
+// slice (length m; ml = n skinny, m full) and n right vectors (length n); a transposed (wide) slice
+// swaps the roles: Y^H = L S R^H gives Y = R S^T L^H, i.e. U = R and V = L.  perm: [f][ml].
+// S (the slice's m_s x n_s plane, f-diagonal) is written whole by the CTAs with blockIdx.x == 0:
+// column pos < n_s holds sigma at row pos.
 __global__ void bj_factors_kernel(const double2* __restrict__ X, const double2* __restrict__ V,
-                                  const double* __restrict__ sig, const int* __restrict__ perm, int m, int n,
-                                  int64_t xs, int64_t vs, int tr, float* __restrict__ ure, float* __restrict__ uim,
-                                  float* __restrict__ sre, float* __restrict__ vre, float* __restrict__ vim) {
-  const int f = blockIdx.z, pos = blockIdx.y, r = n;
-  const int j = perm[(int64_t)f * n + pos];
-  const int M = tr ? n : m, N = tr ? m : n;                  // rows of the slice's U and V
-  float* lre = tr ? vre + (int64_t)f * N * r : ure + (int64_t)f * M * r;
-  float* lim = tr ? vim + (int64_t)f * N * r : uim + (int64_t)f * M * r;
-  float* rre = tr ? ure + (int64_t)f * M * r : vre + (int64_t)f * N * r;
-  float* rim = tr ? uim + (int64_t)f * M * r : vim + (int64_t)f * N * r;
+                                  const double* __restrict__ sig, const int* __restrict__ perm, int m, int n, int ml,
+                                  int64_t xs, int64_t vs, int tr, int m_s, int n_s, float* __restrict__ ure,
+                                  float* __restrict__ uim, float* __restrict__ sre, float* __restrict__ vre,
+                                  float* __restrict__ vim) {
+  const int f = blockIdx.z, pos = blockIdx.y;
+  const int j = perm[(int64_t)f * ml + pos];
+  // left planes [f][ml][m], right planes [f][n][n]
+  float* lre = tr ? vre : ure;
+  float* lim = tr ? vim : uim;
+  float* rre = tr ? ure : vre;
+  float* rim = tr ? uim : vim;
+  const int64_t lo = (int64_t)f * ml * m + (int64_t)pos * m, ro = (int64_t)f * n * n + (int64_t)pos * n;
   const double2* xj = X + (int64_t)f * xs + (int64_t)j * m;
-  const double2* vj = V + (int64_t)f * vs + (int64_t)j * n;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    lre[(int64_t)pos * m + i] = (float)xj[i].x;
-    lim[(int64_t)pos * m + i] = (float)xj[i].y;
+    lre[lo + i] = (float)xj[i].x;
+    lim[lo + i] = (float)xj[i].y;
   }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    rre[(int64_t)pos * n + i] = (float)vj[i].x;
-    rim[(int64_t)pos * n + i] = (float)vj[i].y;
-    sre[(int64_t)f * r * r + (int64_t)pos * r + i] = i == pos ? (float)sig[(int64_t)f * n + j] : 0.f;
+  if (pos < n) {                                               // the first n positions are columns j < n
+    const double2* vj = V + (int64_t)f * vs + (int64_t)j * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      rre[ro + i] = (float)vj[i].x;
+      rim[ro + i] = (float)vj[i].y;
+    }
+  }
+  if (blockIdx.x == 0 && pos < n_s) {
+    const float sv = pos < n ? (float)sig[(int64_t)f * ml + j] : 0.f;
+    for (int i = threadIdx.x; i < m_s; i += blockDim.x)
+      sre[(int64_t)f * m_s * n_s + (int64_t)pos * m_s + i] = i == pos ? sv : 0.f;
   }
 }
 
@@ -527,11 +537,11 @@ __global__ void __launch_bounds__(1024) bj_reduce_kernel(const double* __restric
 
 }  // namespace
 
-size_t bj_workspace_bytes(int64_t m_in, int64_t n_in, int64_t h) {
-  const int64_t m = std::max(m_in, n_in), n = std::min(m_in, n_in);
-  // X, V, sigma, flags, perm, dots, row coverage (+ alignment slack)
-  return 16 * (size_t)h * (size_t)(m * n + n * n) + 8 * (size_t)h * n + 4 * (size_t)h * MAX_SWEEPS +
-         4 * (size_t)h * n + 16 * (size_t)h * n + 8 * (size_t)h * m + 8192;
+size_t bj_workspace_bytes(int64_t m_in, int64_t n_in, int64_t h, bool full) {
+  const int64_t m = std::max(m_in, n_in), n = std::min(m_in, n_in), ml = full ? m : n;
+  // X (m x ml), V, sigma, flags, perm, dots, row coverage (+ alignment slack)
+  return 16 * (size_t)h * (size_t)(m * ml + n * n) + 8 * (size_t)h * ml + 4 * (size_t)h * MAX_SWEEPS +
+         4 * (size_t)h * ml + 16 * (size_t)h * ml + 8 * (size_t)h * m + 8192;
 }
 
 int launch_tsvd_reduce(const double* sv, int64_t r, int64_t h, int64_t n3, float rtol, float* out, cudaStream_t s) {
@@ -545,15 +555,19 @@ int launch_block_svd(const float* re, const float* im, int64_t m_in, int64_t n_i
                      int mode, BjOut o, void* ws, int* status, cudaStream_t s) {
   const bool tr = m_in < n_in;
   const int m = (int)std::max(m_in, n_in), n = (int)std::min(m_in, n_in);
-  const int64_t xs = (int64_t)m * n, vs = (int64_t)n * n;
+  const bool full = mode == BJ_FACTORS_FULL;
+  const int ml = full ? m : n;                                      // columns of X (left vectors)
+  const int64_t xs = (int64_t)m * ml, vs = (int64_t)n * n;
   double2* X = (double2*)ws;
   double2* V = X + h * xs;
   double* sig = (double*)(V + h * vs);
-  int* flags = (int*)(sig + h * n);
+  int* flags = (int*)(sig + h * ml);
   int* perm = flags + h * MAX_SWEEPS;
-  double2* dots = (double2*)(((uintptr_t)(perm + h * n) + 15) & ~(uintptr_t)15);
-  double* rcov = (double*)(dots + h * n);
+  double2* dots = (double2*)(((uintptr_t)(perm + h * ml) + 15) & ~(uintptr_t)15);
+  double* rcov = (double*)(dots + h * ml);
   cudaMemsetAsync(flags, 0, 4 * (size_t)h * MAX_SWEEPS, s);
+  if (ml > n)                                                       // full factors: columns n.. start at 0
+    cudaMemset2DAsync(X + (int64_t)n * m, 16 * (size_t)xs, 0, 16 * (size_t)(ml - n) * m, (size_t)h, s);
   {
     const int64_t work = (int64_t)m * n;
     const int gx = (int)std::min<int64_t>((work + 255) / 256, 1024);
@@ -583,19 +597,21 @@ int launch_block_svd(const float* re, const float* im, int64_t m_in, int64_t n_i
     }
   }
 #endif
-  bj_sigma_kernel<<<dim3((n * 32 + 255) / 256, (unsigned)h), 256, 0, s>>>(X, m, n, xs, sig);
+  bj_sigma_kernel<<<dim3((ml * 32 + 255) / 256, (unsigned)h), 256, 0, s>>>(X, m, ml, xs, sig);
   if (mode == BJ_SVT) {
     dim3 g((unsigned)((m + 31) / 32), (unsigned)((n + 31) / 32), (unsigned)h);
     bj_svt_out_kernel<<<g, 256, 0, s>>>(X, V, sig, m, n, xs, vs, o.tau, tr ? 1 : 0, (int)m_in, o.wre, o.wim, fstride);
   } else if (mode == BJ_VALUES) {
     bj_rank_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)h), 256, 0, s>>>(sig, n, nullptr, o.sv);
   } else {
-    bj_rank_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)h), 256, 0, s>>>(sig, n, perm, nullptr);
-    bj_left_kernel<<<(unsigned)h, 1024, 0, s>>>(X, sig, m, n, xs, dots, rcov);
+    // (full: the extra columns have sigma 0 and sort last, so positions < n are the columns j < n)
+    bj_rank_kernel<<<dim3((unsigned)((ml + 255) / 256), (unsigned)h), 256, 0, s>>>(sig, ml, perm, nullptr);
+    bj_left_kernel<<<(unsigned)h, 1024, 0, s>>>(X, sig, m, ml, xs, dots, rcov);
     const int gx = std::min(8, (m + 255) / 256);
-    bj_factors_kernel<<<dim3((unsigned)gx, (unsigned)n, (unsigned)h), 256, 0, s>>>(X, V, sig, perm, m, n, xs, vs,
-                                                                                  tr ? 1 : 0, o.ure, o.uim, o.sre,
-                                                                                  o.vre, o.vim);
+    // S: r x r (skinny) or the slice's m_in x n_in plane (full)
+    const int m_s = full ? (int)m_in : n, n_s = full ? (int)n_in : n;
+    bj_factors_kernel<<<dim3((unsigned)gx, (unsigned)std::max(ml, n_s), (unsigned)h), 256, 0, s>>>(
+        X, V, sig, perm, m, n, ml, xs, vs, tr ? 1 : 0, m_s, n_s, o.ure, o.uim, o.sre, o.vre, o.vim);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }

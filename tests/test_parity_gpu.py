@@ -522,6 +522,38 @@ def test_tsvd_factors_rank_deficient(T, dims, rank):
     assert O.rel_err(O.tprod_bcirc(O.tran(V), V), O.teye(r, n3)) <= 1e-5
 
 
+@pytest.mark.parametrize("dims,rank", [((6, 4, 5), 0), ((3, 7, 4), 0), ((64, 48, 9), 0), ((100, 70, 6), 0),
+                                       ((40, 130, 4), 0), ((12, 20, 7), 3), ((100, 80, 5), 3), ((16, 6, 4), -1),
+                                       ((1, 5, 3), 0)],
+                         ids=lambda d: "x".join(map(str, d)) if isinstance(d, tuple) else str(d))
+def test_tsvd_full_factors_gpu(T, dims, rank):
+    """Full t-SVD (Theorem 2.2 shapes) on the GPU: S equals the oracle's full S; U (n1 x n1) and V
+    (n2 x n2) are orthogonal both ways and A = U * S * V^*, checked in the oracle (the null-space
+    columns are one valid completion, so they are not compared one by one).  rank > 0: a tubal-rank
+    product; -1: the zero tensor."""
+    n1, n2, n3 = dims
+    if rank > 0:
+        A = O.tprod_bcirc(normal((n1, rank, n3), 151 + n3, np.float64),
+                          normal((rank, n2, n3), 152 + n3, np.float64)).astype(np.float32)
+    elif rank < 0:
+        A = np.zeros(dims, np.float32)
+    else:
+        A = normal(dims, 161 + n3)
+    h = T.Handle()
+    U, S, V = (host(x) for x in T.tsvd_full(dev(A), handle=h))
+    assert h.status() == 0
+    assert U.shape == (n1, n1, n3) and S.shape == (n1, n2, n3) and V.shape == (n2, n2, n3)
+    _, S_ref, _ = O.tsvd(A.astype(np.float64), full=True)
+    if rank >= 0:
+        assert O.rel_err(S, S_ref) <= 1e-5
+        assert O.rel_err(O.tprod_bcirc(O.tprod_bcirc(U, S), O.tran(V)), A.astype(np.float64)) <= 1e-5
+    else:
+        assert np.all(S == 0.0)
+    for Q, n in ((U, n1), (V, n2)):
+        assert O.rel_err(O.tprod_bcirc(O.tran(Q), Q), O.teye(n, n3)) <= 1e-5
+        assert O.rel_err(O.tprod_bcirc(Q, O.tran(Q)), O.teye(n, n3)) <= 1e-5
+
+
 def test_next_rows_argument_errors(T):
     """Argument errors of the NEXT-row entry points come back before any work: tau < 0 / NaN,
     slices beyond the 64 x 64 Jacobi kernel of the t-SVD scalars, aliasing output."""
