@@ -230,8 +230,10 @@ enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_
  * kernels where they apply, else the register-resident / mixed-radix / generic ones), 1 =
  * register-resident and generic transform kernels only, 2 = for 2 <= n3 <= 64 the tensor-core
  * DFT-matrix kernels (Eq. (2) as a tcgen05 3xTF32 contraction, transforms_tc.cu; measured slower
- * than auto on B200), else auto.  Same result up to the rounding of the DFT sums (all
- * within the stage tolerances). */
+ * than auto on B200), else auto, 3 = auto except that n3 = 4096 takes the one-pass
+ * 8-CTA cluster kernels (transforms_cluster.cu: the four-step intermediate kept in distributed shared
+ * memory) instead of the two-pass four-step kernels.  Same result up to the rounding of the DFT sums
+ * (all within the stage tolerances). */
 /* TPROD_OPT_GEMM_CLUSTER: 0 = auto, 1 = independent CTAs, 2 = 2-CTA clusters along N sharing the
  * A tile by TMA multicast, 3 = CTA pairs issuing tcgen05.mma.cta_group::2 (256 x 128 tiles over two
  * SMs; requires the 128 N tile), 4 = 4-CTA clusters of two such pairs stacked along M sharing the B

@@ -5,7 +5,7 @@
 //          K1 fwd_split(A), K1 fwd_split(B)      Alg. 1 step 1 on the Hermitian half
 //          K2 gemm (tcgen05; SIMT reference)     Alg. 1 step 2, first branch (h slices)
 //          K3 inv                                Alg. 1 step 2 second branch + step 3, fused
-//   fp64:  K1 fwd_f64 x2, K2 gemm_simt_f64, K3 inv_f64
+//   fp64:  K1 fwd_f64 x2 (mixed-radix / Bluestein fp64 FFT, transforms_f64.cu), K2 gemm_simt_f64, K3 inv_f64
 #include "../../include/tprod.h"
 #include "internal.h"
 
@@ -347,6 +347,7 @@ int prepare_into(tprod_ctx* h, PreparedA& P, const float* A, int64_t n1, int64_t
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   T.staged = h->transform != 1;
+  T.cluster = h->transform == 3;
   T.tc = h->transform == 2;
   int f1 = 0, f2 = 0;
   fourstep_factors(n3, &f1, &f2);
@@ -451,6 +452,7 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
                int64_t n4, cudaStream_t s, const PreparedA* pa, const Layout32& L, Twiddles32 T) {
   int st = 0;
   T.staged = h->transform != 1;
+  T.cluster = h->transform == 3;
   T.tc = h->transform == 2;
   char* ws = (char*)h->ws;
   T.scratch = L.W_bytes ? (float*)(ws + L.off_W) : nullptr;
@@ -507,6 +509,7 @@ int run_f64(tprod_ctx* h, const double* A, const double* B, double* C, int64_t n
   if (st) return st;
   const double2* tw = nullptr;
   if ((st = get_tw64(h, (int)n3, &tw))) return st;
+  fft64_prepare(n3);                  // FFT tables built outside any capture (false: generic kernels)
   char* ws = (char*)h->ws;
   double* Ab = (double*)(ws + L.off_Ab);
   double* Bb = (double*)(ws + L.off_Bb);
@@ -671,6 +674,7 @@ int spectral_planes(tprod_ctx* h, const float* Y, int64_t n1, int64_t n2, int64_
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   T.staged = h->transform != 1;
+  T.cluster = h->transform == 3;
   T.tc = 0;   // NEXT rows decode the spectrum to fp32: the FFT forward kernels (more accurate than 3xTF32)
   T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
   T.scratch_bytes = wb;
@@ -842,6 +846,7 @@ int tprod_tinv_f32(const float* A, float* X, int64_t n, int64_t n3, void* stream
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   T.staged = h->transform != 1;
+  T.cluster = h->transform == 3;
   T.tc = 0;   // NEXT rows decode the spectrum to fp32: the FFT forward kernels (more accurate than 3xTF32)
   T.scratch = f1 ? (float*)(ws + off_w) : nullptr;
   T.scratch_bytes = f1 ? b : 0;
@@ -1121,6 +1126,7 @@ int tprod_dft_f32(const float* X, float* Xre, float* Xim, int64_t p, int64_t q, 
   Twiddles32 T;
   if ((st = get_twiddles32(h, (int)n3, &T))) return st;
   T.staged = h->transform != 1;
+  T.cluster = h->transform == 3;
   T.tc = h->transform == 2;
   T.scratch = w_bytes ? (float*)((char*)h->ws + off_w) : nullptr;
   T.scratch_bytes = w_bytes;
@@ -1169,7 +1175,7 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       h->force_cn = (int)value;
       return TPROD_OK;
     case TPROD_OPT_TRANSFORM:
-      if (value < 0 || value > 2) return TPROD_EINVAL;
+      if (value < 0 || value > 3) return TPROD_EINVAL;
       h->transform = (int)value;
       return TPROD_OK;
     case TPROD_OPT_GEMM_BN:

@@ -24,6 +24,7 @@ struct Twiddles32 {
   const float2* st = nullptr;    // Stockham per-pass twiddle table (FFT path only), see transforms_fft.cu
   int staged = 1;                // 0: skip the TMA-staged / tube kernels (TPROD_OPT_TRANSFORM = 1)
   int tc = 1;                    // tensor-core DFT-matrix kernels for n3 <= 64 (0: TPROD_OPT_TRANSFORM = 1, 2)
+  int cluster = 0;               // one-pass cluster kernels for n3 = 4096 (TPROD_OPT_TRANSFORM = 3)
   // four-step long-tube forward (n3 = N1*N2 in {4096, 8192, 16384}): Stockham tables of the two
   // factors and a workspace the size of the larger operand
   const float2* st_n1 = nullptr;
@@ -94,6 +95,15 @@ bool launch_fwd_4step(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 // inverse: C-bar in the production layout (Cim = Cre + Q*ld, slice pitch 2*Q*ld)
 bool launch_inv_4step(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const Twiddles32& tw,
                       OutUnscale u, float* X, int num_sms, cudaStream_t s);
+// One-pass long-tube transforms for n3 = 4096 on 8-CTA clusters (transforms_cluster.cu): the
+// four-step intermediate stays in distributed shared memory.  Same arguments and results as the
+// four-step launchers; false = not handled (then the four-step kernels run).
+bool cluster_fft_supported(int64_t n3);
+bool launch_fwd_cluster(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
+                        const float2* tw, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
+bool launch_inv_cluster(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* tw,
+                        OutUnscale u, float* X, int num_sms, cudaStream_t s);
+
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st,
@@ -149,6 +159,12 @@ void launch_gemm_simt_f64(const double* Ab, int64_t lda, const double* Bb, int64
                           cudaStream_t s);
 void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
                     double* X, cudaStream_t s);
+// In-smem mixed-radix fp64 FFT transforms (transforms_f64.cu) for 2 <= n3 <= 8192 (5-smooth, or
+// Bluestein through a 5-smooth length <= 8192); launch_fwd_f64 / launch_inv_f64 take them first.
+// fft64_prepare builds (and caches per device) the tables of n3 outside any stream capture.
+bool fft64_prepare(int64_t n3);
+bool launch_fwd_fft64(const double* X, int64_t P, int64_t Q, int64_t n3, double* out, int64_t ld, cudaStream_t s);
+bool launch_inv_fft64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, double* X, cudaStream_t s);
 
 // Tensor-core (tcgen05) DFT-matrix transforms for 2 <= n3 <= 64 (transforms_tc.cu); false = not
 // handled (P % 4 != 0, unaligned pointers).  The inverse requires C-bar in the production layout.

@@ -304,6 +304,8 @@ void launch_fwd_split(const float* X, int64_t P, int64_t Q, int64_t n3, int role
     cudaGetLastError();
   }
   if (launch_fwd_dense(X, P, Q, n3, role, maxbits, out, ld, unscale, s)) return;
+  if (tw.staged && tw.cluster && launch_fwd_cluster(X, P, Q, n3, role, maxbits, tw.tw, out, ld, unscale, num_sms, s)) return;
+  cudaGetLastError();
   if (tw.staged && launch_fwd_4step(X, P, Q, n3, role, maxbits, tw, out, ld, unscale, num_sms, s)) return;
   cudaGetLastError();
   // 5-smooth n3 > 64: mixed-radix FFT (the handle's Stockham table); otherwise Bluestein's chirp-z
@@ -388,6 +390,8 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   cudaGetLastError();
   if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, u, X, num_sms, s)) return;
   cudaGetLastError();
+  if (prod_layout && tw.cluster && launch_inv_cluster(Cre, ld, P, Q, n3, tw.tw, u, X, num_sms, s)) return;
+  cudaGetLastError();
   if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, u, X, num_sms, s)) return;
   cudaGetLastError();
   if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, u, X, s)) return;
@@ -437,6 +441,8 @@ __global__ void fwd_f64_kernel(const double* __restrict__ X, int64_t P, int64_t 
 
 void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw, double* out,
                     int64_t ld, cudaStream_t s) {
+  if (launch_fwd_fft64(X, P, Q, n3, out, ld, s)) return;
+  cudaGetLastError();
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   const size_t smem = tw_smem_bytes((const void*)fwd_f64_kernel, sizeof(double2) * (size_t)n3);
@@ -446,6 +452,8 @@ void launch_fwd_f64(const double* X, int64_t P, int64_t Q, int64_t n3, Twiddles6
 
 void launch_inv_f64(const double* Cb, int64_t ld, int64_t P, int64_t Q, int64_t n3, Twiddles64 tw,
                     double* X, cudaStream_t s) {
+  if (launch_inv_fft64(Cb, ld, P, Q, n3, X, s)) return;
+  cudaGetLastError();
   const int threads = 128;
   int64_t blocks = (P + threads - 1) / threads * Q;
   const size_t smem = tw_smem_bytes((const void*)inv_kernel<double, double2>, sizeof(double2) * (size_t)n3);

@@ -97,7 +97,7 @@ def test_sweep_fp32(T, dims):
     assert err <= TOL32, err
 
 
-@pytest.mark.parametrize("dims", SWEEP[:12], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("dims", SWEEP, ids=lambda d: "x".join(map(str, d)))
 def test_sweep_fp64(T, dims):
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 300 + n1 + n3, np.float64)
@@ -106,12 +106,18 @@ def test_sweep_fp64(T, dims):
 
 
 @pytest.mark.parametrize("dims", [(24, 20, 32, 16), (17, 33, 64, 9), (40, 24, 100, 20), (6, 5, 4096, 4),
-                                  (130, 70, 9, 100), (256, 96, 31, 200)],
+                                  (130, 70, 9, 100), (256, 96, 31, 200),
+                                  (9, 5, 2, 7), (7, 3, 3, 5),            # smallest FFT lengths
+                                  (33, 17, 97, 9), (5, 7, 1021, 3),      # Bluestein (prime n3), odd P
+                                  (4, 3, 4099, 3),                       # Bluestein, M = 8192
+                                  (3, 4, 8192, 2),                       # longest in-smem fp64 FFT
+                                  (2, 3, 8209, 2)],                      # beyond: generic O(n3^2)
                          ids=lambda d: "x".join(map(str, d)))
 def test_fp64_longer_tubes(T, dims):
-    """fp64 path beyond the sweep's n3 <= 31: power-of-two, 5-smooth and long tubes (n3 = 4096's
-    twiddle table no longer fits the default 48 KB of shared memory), and slices large enough for the
-    register-tiled fp64 GEMM (ragged 64 x 64 tiles) vs the oracle at 1e-12."""
+    """fp64 path beyond the sweep: the mixed-radix fp64 FFT (radix 8/4/2/3/5, transforms_f64.cu) at
+    power-of-two, 5-smooth and long tubes, Bluestein for prime n3 up to M = 8192, the generic kernel
+    beyond, and slices large enough for the register-tiled fp64 GEMM (ragged 64 x 64 tiles), vs the
+    oracle at 1e-12."""
     n1, n2, n3, n4 = dims
     A = normal((n1, n2, n3), 500 + n3, np.float64)
     B = normal((n2, n4, n3), 600 + n3, np.float64)
@@ -298,6 +304,58 @@ def test_fourstep_forward_stage(T, n3, p, q):
         got = host(T.dft_f32(dev(X), role=role))
         err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert err < 2e-6, (role, err)
+
+
+@pytest.mark.parametrize("p,q", [(36, 3), (64, 5), (132, 2), (4, 7), (96, 1)])
+def test_cluster_fft_stages(T, p, q):
+    """One-pass 8-CTA cluster transforms for n3 = 4096 (TPROD_OPT_TRANSFORM = 3,
+    transforms_cluster.cu; P % 4 == 0, ragged 32-tube items): forward vs numpy.fft.rfft for both
+    operand roles and vs the default two-pass four-step kernels; the inverse (conjugate fill fused)
+    round trip on both."""
+    import torch
+    n3 = 4096
+    X = normal((p, q, n3), 3 + p + q)
+    ref = np.fft.rfft(X.astype(np.float64), axis=2)
+    h3 = T.Handle()
+    h3.set_option(T._lib.TPROD_OPT_TRANSFORM, 3)
+    for role in (0, 1):
+        clu = host(T.dft_f32(dev(X), role=role, handle=h3))
+        four = host(T.dft_f32(dev(X), role=role))
+        assert np.linalg.norm(clu - ref) / np.linalg.norm(ref) < 2e-6, role
+        assert np.linalg.norm(clu - four) / np.linalg.norm(ref) < 2e-6, role
+    Xb = torch.from_numpy(ref.astype(np.complex64)).cuda()
+    for hh in (h3, None):
+        back = host(T.idft_f32(Xb, n3, handle=hh))
+        assert np.linalg.norm(back - X) / np.linalg.norm(X) < 2e-6
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 4096, 64), (36, 20, 4096, 12), (100, 8, 4096, 3)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_cluster_full_path(T, dims):
+    """Full t-product through the cluster transforms (TPROD_OPT_TRANSFORM = 3: K1 of A and B, K3) on
+    sampled frontal slices vs the oracle's Eq. (9) block rows, every row of C to its own scale with
+    rows of A spread over 2^-20 .. 2^20 and one zero row (R18), and vs the default two-pass four-step
+    kernels within 1e-6."""
+    n1, n2, n3, n4 = dims
+    rng = np.random.default_rng(n1 + n4)
+    A = normal((n1, n2, n3), 81 + n1).astype(np.float64) * np.exp2(rng.integers(-20, 21, size=n1)).reshape(n1, 1, 1)
+    A[n1 // 2] = 0.0
+    A = A.astype(np.float32)
+    B = normal((n2, n4, n3), 82 + n4)
+    h3 = T.Handle()
+    h3.set_option(T._lib.TPROD_OPT_TRANSFORM, 3)
+    C = gpu_tprod(T, A, B, handle=h3)
+    C3 = gpu_tprod(T, A, B)
+    tl = np.array([0, 1, 2047, 2048, n3 - 1])
+    ref = O.tprod_blockrow(A, B, tl, np.arange(n4))
+    assert O.rel_err(C[:, :, tl], ref) <= TOL32
+    assert not C[n1 // 2].any()
+    ra = np.abs(A).max(axis=(1, 2))
+    for i in range(n1):
+        if ra[i] > 0:
+            num = np.linalg.norm(C[i][:, tl] - ref[i])
+            assert num <= 1e-5 * ra[i] * np.abs(B).max() * np.sqrt(n2 * n3 * n4), (i, num)
+    assert O.rel_err(C, C3) <= 1e-6
 
 
 @pytest.mark.parametrize("dims", [(24, 16, 8192, 8), (132, 8, 4096, 12)], ids=lambda d: "x".join(map(str, d)))
@@ -642,7 +700,7 @@ def test_operand_scales_follow_rows_and_columns(T, dims):
             assert num <= 1e-5 * den, (i, j, num / den)
 
 
-@pytest.mark.parametrize("dims", [(40, 24, 31, 36), (64, 64, 64, 64), (20, 12, 2048, 8)],
+@pytest.mark.parametrize("dims", [(40, 24, 31, 36), (64, 64, 64, 64), (20, 12, 2048, 8), (36, 8, 4096, 8)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_zero_rows_columns_and_tensors(T, dims):
     """Degenerate operands: a zero row of A and a zero lateral slice of B take the max = 0 scale
