@@ -13,8 +13,8 @@
 // (two real tubes per complex FFT: 16 FFTs) and keeps Y on chip: CTA r TMA-loads the 512 rows
 // k1 in [8r, 8r+8) x all k2 (128-byte rows), runs step A on them, multiplies by the twiddle and
 // stores each result straight into the shared memory of the CTA that owns its f2 (distributed
-// shared memory, st.shared::cluster); after one cluster barrier every CTA holds all k1 of its 8
-// f2 values and runs step B.  Each operand moves through HBM once (read x, write the split
+// shared memory, st.async counted on the owner's mbarrier); once its 64 KB have arrived a CTA holds
+// all k1 of its 8 f2 values and runs step B.  Each operand moves through HBM once (read x, write the split
 // spectrum), half the traffic of the two-pass form.
 //
 // f2 ownership is mirror-closed (f2 and 64 - f2 in the same CTA), so the real-pair separation
@@ -24,7 +24,7 @@
 // rows, inverse step B over f1, twiddle, exchange by k1, inverse step A over f2, TMA store).
 //
 // Per CTA: a 64 KB TMA buffer (the next item's load is issued as soon as step A has read it),
-// a 64 KB exchange buffer, a 64 KB output staging buffer; 512 threads; 64-point FFTs as two
+// two 64 KB exchange buffers (alternating items), a 4 KB table of the step twiddles; 512 threads; 64-point FFTs as two
 // in-place radix-8 Stockham passes over 128 columns (every shared access of a warp is 32
 // consecutive float2).
 #include "internal.h"
@@ -44,14 +44,18 @@ using namespace fftreg;
 
 constexpr int CN = 4096, CR = 64;           // N = CR * CR
 constexpr int CS = 8;                       // CTAs per cluster
-constexpr int CTUB = 32, CPAIR = 16;        // tubes per work item, complex FFTs per item
+#ifndef TPROD_CL_TUB
+#define TPROD_CL_TUB 32
+#endif
+constexpr int CTUB = TPROD_CL_TUB, CPAIR = CTUB / 2;   // tubes per work item, complex FFTs per item
 constexpr int CK = CR / CS;                 // k1 rows (forward input) / f2 slots per CTA
 constexpr int COLS = CK * CPAIR;            // FFT columns per CTA (128)
-constexpr int CNT = 512;                    // threads per CTA
+constexpr int CNT = CTUB == 32 ? 512 : 256; // threads per CTA
+constexpr int CPS = CTUB == 32 ? 1 : 2;     // CTAs per SM
 constexpr int JB = CNT / COLS;              // butterfly rows per column handled side by side (4)
 constexpr int BPT = 8 / JB;                 // radix-8 butterflies per thread per pass (2)
 constexpr int ZF2 = CR * COLS;              // float2 per buffer (64 KB)
-constexpr int SMEM_CL = 3 * ZF2 * 8 + 256;  // load + exchange + staging buffers, the f = N/2 rows
+constexpr int SMEM_CL = 3 * ZF2 * 8 + CK * CR * 8 + 256;   // load + 2 exchange buffers, twiddles, f = N/2 rows
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
@@ -185,38 +189,55 @@ __device__ __forceinline__ void col_pass2(const float2* z, const float2* __restr
   }
 }
 
+// Exchange: st.async of each value into the owning CTA's buffer, counted on that CTA's receive
+// mbarrier (complete_tx bytes), so a CTA waits only for its own 64 KB, with no cluster-wide barrier
+// per item.  The exchange buffers alternate between items: a peer can write buffer b again only at
+// item n + 2, which needs this CTA's item-n+1 data, sent after this CTA has finished item n.
+__device__ __forceinline__ void st_async(uint32_t a, float2 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(a),
+               "f"(v.x), "f"(v.y), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed;\nbarrier.cluster.wait;" ::: "memory");
+}
+
 // K1: ROLE 0 = A (row scales per tube, applied before the shared FFT), 1 = B (column scale per q).
+// Output: split planes [f][plane][q][ld] written directly from registers (64-byte rows per half warp).
 template <int ROLE>
-__global__ void __launch_bounds__(CNT, 1) cl_fwd_kernel(const __grid_constant__ CUtensorMap mX,
-                                                        const __grid_constant__ CUtensorMap mO,
-                                                        const __grid_constant__ CUtensorMap mO3, int64_t P,
-                                                        int64_t Q, const unsigned* __restrict__ maxbits,
-                                                        const float2* __restrict__ tw, float* __restrict__ unscale) {
+__global__ void __launch_bounds__(CNT, CPS) cl_fwd_kernel(const __grid_constant__ CUtensorMap mX, int64_t P, int64_t Q,
+                                                        const unsigned* __restrict__ maxbits,
+                                                        const float2* __restrict__ tw, __half* __restrict__ out,
+                                                        int64_t ld, float* __restrict__ unscale) {
   extern __shared__ __align__(1024) unsigned char smc[];
   float2* X = reinterpret_cast<float2*>(smc);                 // [k2][k1 local][c]   (TMA load)
-  float2* W = X + ZF2;                                        // [k1][slot][c] -> [f1][slot][c]
-  __half2* S = reinterpret_cast<__half2*>(W + ZF2);           // [slot][f1][plane][c] (+ f = N/2)
-  __half2* Sx = S + CK * 32 * 4 * CPAIR;                      // [plane][c] of f = N/2
-  __shared__ uint64_t full;
+  float2* W0 = X + ZF2;                                       // [k1][slot][c] -> [f1][slot][c], 2 buffers
+  float2* tws = W0 + 2 * ZF2;                                 // w_N^{k1 f2}: [k1 local][f2]
+  __shared__ uint64_t full, recv[2];
   const int tid = threadIdx.x;
   const int rank = (int)cl_rank();
-  const int col = tid % COLS, c = col % CPAIR, k1 = CK * rank + col / CPAIR;
+  const int col = tid % COLS, c = col % CPAIR, k1l = col / CPAIR, k1 = CK * rank + k1l, jb = tid / COLS;
   const int64_t pblocks = (P + CTUB - 1) / CTUB, items = pblocks * Q;
   const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
   if (tid == 0) {
     mb_init(&full, 1);
+    mb_init(&recv[0], 1);
+    mb_init(&recv[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < CK * CR; i += CNT) tws[i] = twN<-1>(tw, (CK * rank + i / CR) * (i % CR));
   __syncthreads();
+  cl_sync_relaxed();                                          // every CTA's barriers initialised
   if (tid == 0 && cid < items) {
     const int64_t q = cid / pblocks, p0 = (cid - q * pblocks) * CTUB;
     mb_expect(&full, ZF2 * 8);
     load4(X, &mX, &full, (int)p0, (int)q, CK * rank, 0);
   }
-  const uint32_t Wb = s32(W);
-  cl_arrive();                                                // this CTA's W is free
-  uint32_t ph = 0;
-  for (int64_t it = cid; it < items; it += ncl, ph ^= 1) {
+  const int64_t plane = Q * ld;
+  uint32_t n = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++n) {
+    const int b = n & 1;
+    float2* W = W0 + b * ZF2;
     const int64_t q = it / pblocks, p0 = (it - q * pblocks) * CTUB;
     const int64_t p = p0 + 2 * c;
     const bool in0 = p < P, in1 = p + 1 < P;
@@ -234,57 +255,57 @@ __global__ void __launch_bounds__(CNT, 1) cl_fwd_kernel(const __grid_constant__ 
       post = make_float2(pow2f(e), pow2f(e));
       if (p0 == 0 && rank == 0 && tid == 0) unscale[q] = unscale_of(__ldg(maxbits + q), e);
     }
-    mb_wait(&full, ph);
+    mb_wait(&full, n & 1);
     // ---- step A: FFT over k2 for the CTA's 8 k1 rows x 16 pairs
     col_pass1<-1, ROLE == 0>(X, pre);
     float2 v[BPT][8];
     col_pass2<-1>(X, tw, v);
     __syncthreads();                                          // X fully read: refill it
-    if (tid == 0 && it + ncl < items) {
-      const int64_t it2 = it + ncl;
-      const int64_t q2 = it2 / pblocks, p2 = (it2 - q2 * pblocks) * CTUB;
-      fence_async();
-      mb_expect(&full, ZF2 * 8);
-      load4(X, &mX, &full, (int)p2, (int)q2, CK * rank, 0);
+    if (tid == 0) {
+      if (it + ncl < items) {
+        const int64_t it2 = it + ncl;
+        const int64_t q2 = it2 / pblocks, p2 = (it2 - q2 * pblocks) * CTUB;
+        fence_async();
+        mb_expect(&full, ZF2 * 8);
+        load4(X, &mX, &full, (int)p2, (int)q2, CK * rank, 0);
+      }
+      mb_expect(&recv[b], ZF2 * 8);                           // this item's 64 KB from the cluster
     }
-    cl_wait();                                                // every CTA's W is free
     {
-      const int jb = tid / COLS;
+      const uint32_t wa = s32(W) + (uint32_t)((k1 * CK * CPAIR + c) * 8), ra = s32(&recv[b]);
 #pragma unroll
       for (int u = 0; u < BPT; ++u) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int f2 = jb + JB * u + 8 * r;
-          const float2 y = cmul(v[u][r], twN<-1>(tw, k1 * f2));   // w_N^{k1 f2}
-          st_cl(cl_mapa(Wb + (uint32_t)(((k1 * CK + f2_slot(f2)) * CPAIR + c) * 8), (uint32_t)f2_owner(f2)), y);
+          const uint32_t dst = (uint32_t)f2_owner(f2);
+          st_async(cl_mapa(wa + (uint32_t)(f2_slot(f2) * CPAIR * 8), dst), cmul(v[u][r], tws[k1l * CR + f2]),
+                   cl_mapa(ra, dst));
         }
       }
     }
-    cl_arrive();
-    cl_wait();                                                // W complete in every CTA
+    mb_wait(&recv[b], (n >> 1) & 1);                          // all k1 of this CTA's f2 slots
     // ---- step B: FFT over k1 for the CTA's 8 f2 slots x 16 pairs (columns (slot, c))
     col_pass1<-1, false>(W, pre);
     col_pass2<-1>(W, tw, v);
     __syncthreads();
-    {
-      const int jb = tid / COLS;
 #pragma unroll
-      for (int u = 0; u < BPT; ++u)
+    for (int u = 0; u < BPT; ++u)
 #pragma unroll
-        for (int r = 0; r < 8; ++r) W[(jb + JB * u + 8 * r) * COLS + col] = v[u][r];   // [f1][slot][c]
-    }
-    if (tid == 0) wait_read();                                // the previous item's stores have read S
+      for (int r = 0; r < 8; ++r) W[(jb + JB * u + 8 * r) * COLS + col] = v[u][r];   // [f1][slot][c]
     __syncthreads();
-    // ---- Hermitian half: real-pair separation, 2^e scaling (B), fp16 hi/lo split into S
+    // ---- Hermitian half: real-pair separation, 2^e scaling (B), fp16 hi/lo split, stored as
+    // half2 (tubes 2c', 2c'+1) into the four planes of row f (CPAIR % ... : c' fixed per thread)
+    const int cc = tid % CPAIR;
+    const bool st_ok = p0 + 2 * cc < P;                       // P even: both tubes in range
+    __half* ob = out + q * ld + p0 + 2 * cc;
     for (int idx = tid; idx < CK * 32 * CPAIR + CPAIR; idx += CNT) {
-      int s, f1, cc;
+      int s, f1;
       if (idx < CK * 32 * CPAIR) {
-        cc = idx % CPAIR;
         f1 = (idx / CPAIR) % 32;
         s = idx / (32 * CPAIR);
       } else {                                                // f = N/2: slot 0 of CTA 0, f1 = 32
         if (rank != 0) break;
-        cc = idx - CK * 32 * CPAIR;
         f1 = 32;
         s = 0;
       }
@@ -298,42 +319,38 @@ __global__ void __launch_bounds__(CNT, 1) cl_fwd_kernel(const __grid_constant__ 
       const float2 im = make_float2(0.5f * (zf.y - zm.y) * sc.x, -0.5f * (zf.x - zm.x) * sc.y);
       const __half2 rh = __float22half2_rn(re), ih = __float22half2_rn(im);
       const float2 rhf = __half22float2(rh), ihf = __half22float2(ih);
-      __half2* row = f1 < 32 ? S + ((s * 32 + f1) * 4) * CPAIR + cc : Sx + cc;
-      row[PL_RE_HI * CPAIR] = rh;
-      row[PL_RE_LO * CPAIR] = __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));
-      row[PL_IM_HI * CPAIR] = ih;
-      row[PL_IM_LO * CPAIR] = __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));
+      if (st_ok) {
+        __half2* o = reinterpret_cast<__half2*>(ob + (int64_t)(4 * (f2 + CR * f1)) * plane);
+        o[0] = rh;                                                                   // PL_RE_HI
+        *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(o) + plane) =
+            __float22half2_rn(make_float2(re.x - rhf.x, re.y - rhf.y));              // PL_RE_LO
+        *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(o) + 2 * plane) = ih;   // PL_IM_HI
+        *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(o) + 3 * plane) =
+            __float22half2_rn(make_float2(im.x - ihf.x, im.y - ihf.y));              // PL_IM_LO
+      }
     }
-    fence_async();
-    __syncthreads();
-    if (tid == 0) {
-#pragma unroll 1
-      for (int s = 0; s < CK; ++s) store5(&mO, S + s * 32 * 4 * CPAIR, (int)p0, (int)q, 0, slot_f2(rank, s), 0);
-      if (rank == 0) store3(&mO3, Sx, (int)p0, (int)q, 4 * (CN / 2));
-      commit();
-    }
-    cl_arrive();                                              // this CTA is done reading W
   }
-  cl_wait();
-  if (tid == 0) wait_all();
+  cl_sync_relaxed();                                          // no peer still writes this CTA's smem
 }
 
 // K3 (same work items): load the CTA's Hermitian C-bar rows f = f2 + 64 f1 (f2 in its slots),
-// conjugate fill, inverse step B over f1, twiddle w_N^{-f2 k1}, exchange by k1, inverse step A
-// over f2, 1/N and the per-tube unscale, one TMA store of the rows k1 in [8r, 8r+8) x all k2.
-__global__ void __launch_bounds__(CNT, 1) cl_inv_kernel(const __grid_constant__ CUtensorMap mC5,
+// build Z with the conjugate fill in place, inverse step B over f1, twiddle w_N^{-f2 k1}, exchange by
+// k1, inverse step A over f2, 1/N and the per-tube unscale, one TMA store of the rows
+// k1 in [8r, 8r+8) x all k2.
+__global__ void __launch_bounds__(CNT, CPS) cl_inv_kernel(const __grid_constant__ CUtensorMap mC5,
                                                         const __grid_constant__ CUtensorMap mC3,
                                                         const __grid_constant__ CUtensorMap mXo, int64_t P,
                                                         int64_t Q, const float2* __restrict__ tw, OutUnscale u) {
   extern __shared__ __align__(1024) unsigned char smc[];
-  float* L = reinterpret_cast<float*>(smc);                   // [slot][f1 < 32][re|im][32 tubes]
-  float2* W = reinterpret_cast<float2*>(L + 2 * ZF2);         // [f1][slot][c] -> [k1][slot][c]
-  float2* Xb = W + ZF2;                                       // [f2][k1 local][c] -> [k2][k1 local][c]
-  float* Lx = reinterpret_cast<float*>(Xb + ZF2);             // [re|im][32 tubes] of f = N/2
-  __shared__ uint64_t full;
+  float* L = reinterpret_cast<float*>(smc);                   // [slot][f1 < 32][re|im][32 tubes] -> Z [f1][slot][c]
+  float2* Z = reinterpret_cast<float2*>(L);
+  float2* Xb0 = Z + ZF2;                                      // [f2][k1 local][c] -> [k2][k1 local][c], 2 buffers
+  float2* tws = Xb0 + 2 * ZF2;                                // w_N^{-f2 k1}: [slot][k1]
+  float* Lx = reinterpret_cast<float*>(tws + CK * CR);        // [re|im][32 tubes] of f = N/2
+  __shared__ uint64_t full, recv[2];
   const int tid = threadIdx.x;
   const int rank = (int)cl_rank();
-  const int col = tid % COLS, c = col % CPAIR;
+  const int col = tid % COLS, c = col % CPAIR, jb = tid / COLS;
   const int64_t pblocks = (P + CTUB - 1) / CTUB, items = pblocks * Q;
   const int64_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
   const uint32_t lbytes = CK * 32 * 2 * CTUB * 4 + (rank == 0 ? 2 * CTUB * 4 : 0);
@@ -346,62 +363,85 @@ __global__ void __launch_bounds__(CNT, 1) cl_inv_kernel(const __grid_constant__ 
   };
   if (tid == 0) {
     mb_init(&full, 1);
+    mb_init(&recv[0], 1);
+    mb_init(&recv[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < CK * CR; i += CNT) tws[i] = twN<+1>(tw, slot_f2(rank, i / CR) * (i % CR));
   __syncthreads();
+  cl_sync_relaxed();
   if (tid == 0 && cid < items) issue(cid);
-  const uint32_t Xbb = s32(Xb);
-  cl_arrive();                                                // this CTA's Xb is free
-  uint32_t ph = 0;
-  for (int64_t it = cid; it < items; it += ncl, ph ^= 1) {
+  uint32_t n = 0;
+  for (int64_t it = cid; it < items; it += ncl, ++n) {
+    const int b = n & 1;
+    float2* Xb = Xb0 + b * ZF2;
     const int64_t q = it / pblocks, p0 = (it - q * pblocks) * CTUB;
-    mb_wait(&full, ph);
-    // ---- Z_f = X_f + i Y_f for f = f2 + 64 f1, all f1, with the conjugate fill (Im of DC / N/2 dropped)
-    for (int idx = tid; idx < CR * CK * CPAIR; idx += CNT) {
-      const int cc = idx % CPAIR, s = (idx / CPAIR) % CK, f1 = idx / (CK * CPAIR);
-      const int f2 = slot_f2(rank, s);
-      float2 z;
-      if (f1 < 32 || (f2 == 0 && f1 == 32)) {
-        const float* src = f1 < 32 ? L + (s * 32 + f1) * 2 * CTUB : Lx;
-        const bool self = f2 == 0 && (f1 == 0 || f1 == 32);
-        const float2 re = reinterpret_cast<const float2*>(src)[cc];                       // (x_r, y_r)
-        const float2 im = self ? make_float2(0.f, 0.f) : reinterpret_cast<const float2*>(src + CTUB)[cc];
-        z = make_float2(re.x - im.y, im.x + re.y);                                        // X_f + i Y_f
-      } else {                                                                            // f > N/2
-        const int g1 = f2 == 0 ? 64 - f1 : 63 - f1;                                       // g = N - f
-        const int sg = f2 == 0 ? s : mirror_slot(rank, s);
-        const float* src = L + (sg * 32 + g1) * 2 * CTUB;
-        const float2 re = reinterpret_cast<const float2*>(src)[cc];
-        const float2 im = reinterpret_cast<const float2*>(src + CTUB)[cc];
-        z = make_float2(re.x + im.y, re.y - im.x);                                        // conj X_g + i conj Y_g
-      }
-      W[idx] = z;                                             // idx = (f1 * CK + s) * CPAIR + cc
+    mb_wait(&full, n & 1);
+    // ---- Z_f = X_f + i Y_f, f = f2 + 64 f1, with the conjugate fill (Im of DC / N/2 dropped), built in
+    // place: Hermitian row (s, f1 < 32) of pair c gives Z[f1][s][c] and, conjugated, the fill
+    // Z[63 - f1][s^1][c] (Z[64 - f1][0][c] for f2 = 0); f = N/2 (CTA 0) gives Z[32][0][c].
+    constexpr int PER = CK * 32 * CPAIR / CNT;                // Hermitian entries per thread (8)
+    float4 e[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = tid + k * CNT;
+      const int cc = idx % CPAIR, f1 = (idx / CPAIR) % 32, s = idx / (32 * CPAIR);
+      const float* src = L + (s * 32 + f1) * 2 * CTUB;
+      const float2 re = reinterpret_cast<const float2*>(src)[cc];
+      const float2 im = reinterpret_cast<const float2*>(src + CTUB)[cc];
+      e[k] = make_float4(re.x, re.y, im.x, im.y);             // (x_r, y_r, x_i, y_i)
+    }
+    float4 ex = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rank == 0 && tid < CPAIR) {
+      const float2 re = reinterpret_cast<const float2*>(Lx)[tid];
+      ex = make_float4(re.x, re.y, 0.f, 0.f);
     }
     __syncthreads();
-    if (tid == 0 && it + ncl < items) {                       // L fully read: refill it
-      fence_async();
-      issue(it + ncl);
-    }
-    // ---- inverse step B: over f1 (columns (slot, c)) -> U[k1][slot][c]
-    col_pass1<+1, false>(W, make_float2(1.f, 1.f));
-    float2 v[BPT][8];
-    col_pass2<+1>(W, tw, v);
-    cl_wait();                                                // every CTA's Xb is free
-    {
-      const int jb = tid / COLS, s = col / CPAIR;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int idx = tid + k * CNT;
+      const int cc = idx % CPAIR, f1 = (idx / CPAIR) % 32, s = idx / (32 * CPAIR);
       const int f2 = slot_f2(rank, s);
+      float4 x = e[k];
+      if (f2 == 0 && f1 == 0) x.z = x.w = 0.f;                // DC: Im dropped
+      Z[(f1 * CK + s) * CPAIR + cc] = make_float2(x.x - x.w, x.z + x.y);                    // X_f + i Y_f
+      if (f2 != 0 || f1 != 0) {
+        const int g1 = f2 == 0 ? 64 - f1 : 63 - f1;
+        const int sg = f2 == 0 ? s : mirror_slot(rank, s);
+        Z[(g1 * CK + sg) * CPAIR + cc] = make_float2(x.x + x.w, x.y - x.z);                 // conj fill
+      }
+    }
+    if (rank == 0 && tid < CPAIR) Z[(32 * CK + 0) * CPAIR + tid] = make_float2(ex.x, ex.y);  // f = N/2 (self)
+    __syncthreads();
+    // ---- inverse step B: over f1 (columns (slot, c)) -> U[k1][slot][c]
+    col_pass1<+1, false>(Z, make_float2(1.f, 1.f));
+    float2 v[BPT][8];
+    col_pass2<+1>(Z, tw, v);
+    __syncthreads();                                          // Z fully read: refill L
+    if (tid == 0) {
+      if (it + ncl < items) {
+        fence_async();
+        issue(it + ncl);
+      }
+      wait_read();            // the previous item's store has read Xb[b ^ 1] (peers refill it at item n + 1)
+      mb_expect(&recv[b], ZF2 * 8);
+    }
+    __syncthreads();
+    {
+      const int s = col / CPAIR, f2 = slot_f2(rank, s);
+      const uint32_t xa = s32(Xb) + (uint32_t)((f2 * CK * CPAIR + c) * 8), ra = s32(&recv[b]);
 #pragma unroll
       for (int uu = 0; uu < BPT; ++uu) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int k1 = jb + JB * uu + 8 * r;
-          const float2 y = cmul(v[uu][r], twN<+1>(tw, k1 * f2));   // w_N^{-f2 k1}
-          st_cl(cl_mapa(Xbb + (uint32_t)(((f2 * CK + (k1 % CK)) * CPAIR + c) * 8), (uint32_t)(k1 / CK)), y);
+          const uint32_t dst = (uint32_t)(k1 / CK);
+          st_async(cl_mapa(xa + (uint32_t)((k1 % CK) * CPAIR * 8), dst), cmul(v[uu][r], tws[s * CR + k1]),
+                   cl_mapa(ra, dst));
         }
       }
     }
-    cl_arrive();
-    cl_wait();                                                // Xb complete in every CTA
+    mb_wait(&recv[b], (n >> 1) & 1);                          // all f2 of this CTA's k1 rows
     // ---- inverse step A: over f2 (columns (k1 local, c)) -> x[k1 + 64 k2]
     col_pass1<+1, false>(Xb, make_float2(1.f, 1.f));
     col_pass2<+1>(Xb, tw, v);
@@ -410,26 +450,23 @@ __global__ void __launch_bounds__(CNT, 1) cl_inv_kernel(const __grid_constant__ 
       // 1/N and the per-tube unscale (R18): tubes 2c, 2c + 1 of this column
       const int64_t p = p0 + 2 * c;
       const float2 a = p < P ? out_scale(u.row, p, u.col, q, 1.f / (float)CN) : make_float2(0.f, 0.f);
-      const float2 b = p + 1 < P ? out_scale(u.row, p + 1, u.col, q, 1.f / (float)CN) : make_float2(0.f, 0.f);
-      const int jb = tid / COLS;
+      const float2 bb = p + 1 < P ? out_scale(u.row, p + 1, u.col, q, 1.f / (float)CN) : make_float2(0.f, 0.f);
 #pragma unroll
       for (int uu = 0; uu < BPT; ++uu)
 #pragma unroll
         for (int r = 0; r < 8; ++r)
           Xb[(jb + JB * uu + 8 * r) * COLS + col] =
-              make_float2((v[uu][r].x * a.x) * a.y, (v[uu][r].y * b.x) * b.y);   // [k2][k1 local][c]
+              make_float2((v[uu][r].x * a.x) * a.y, (v[uu][r].y * bb.x) * bb.y);   // [k2][k1 local][c]
     }
     fence_async();
     __syncthreads();
     if (tid == 0) {
       store4(&mXo, Xb, (int)p0, (int)q, CK * rank, 0);
       commit();
-      wait_read();                                            // Xb read before peers may refill it
     }
-    cl_arrive();
   }
-  cl_wait();
   if (tid == 0) wait_all();
+  cl_sync_relaxed();
 }
 
 // ---- host
@@ -497,27 +534,16 @@ bool cluster_fft_supported(int64_t n3) { return n3 == CN; }
 
 bool launch_fwd_cluster(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                         const float2* tw, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s) {
-  if (!cluster_fft_supported(n3) || !tw || P % 4 != 0 || ld % 8 != 0) return false;
-  CUtensorMap mx, mo, mo3;
+  if (!cluster_fft_supported(n3) || !tw || P % 4 != 0 || ld % 2 != 0) return false;
+  CUtensorMap mx;
   {
     const cuuint64_t dims[4] = {(cuuint64_t)P, (cuuint64_t)Q, CR, CR};
     const cuuint64_t st[3] = {(cuuint64_t)P * 4, (cuuint64_t)(P * Q) * 4, (cuuint64_t)(P * Q) * CR * 4};
     const cuuint32_t box[4] = {CTUB, 1, CK, CR};
     if (!make_map(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, X, dims, st, box)) return false;
   }
-  {   // split planes [f][plane][q][ld], row 4 f + plane, f = f2 + 64 f1 (f1 < 32)
-    const cuuint64_t row = (cuuint64_t)(Q * ld) * 2;
-    const cuuint64_t dims[5] = {(cuuint64_t)P, (cuuint64_t)Q, 4, CR, 32};
-    const cuuint64_t st[4] = {(cuuint64_t)ld * 2, row, 4 * row, 4 * CR * row};
-    const cuuint32_t box[5] = {CTUB, 1, 4, 1, 32};
-    if (!make_map(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5, out, dims, st, box)) return false;
-    const cuuint64_t d3[3] = {(cuuint64_t)P, (cuuint64_t)Q, (cuuint64_t)(4 * h_slices(n3))};
-    const cuuint64_t s3[2] = {(cuuint64_t)ld * 2, row};
-    const cuuint32_t b3[3] = {CTUB, 1, 4};
-    if (!make_map(&mo3, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, out, d3, s3, b3)) return false;
-  }
   const int64_t items = (P + CTUB - 1) / CTUB * Q;
-  void* args[] = {(void*)&mx, (void*)&mo, (void*)&mo3, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&tw,
+  void* args[] = {(void*)&mx, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&tw, (void*)&out, (void*)&ld,
                   (void*)&unscale};
   return role == 0 ? launch_cluster(cl_fwd_kernel<0>, items, num_sms, s, args)
                    : launch_cluster(cl_fwd_kernel<1>, items, num_sms, s, args);
