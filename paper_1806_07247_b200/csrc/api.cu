@@ -66,6 +66,9 @@ struct tprod_ctx {
   bool sync_checks = true;                             // TPROD_OPT_SYNC_CHECKS
   int* status = nullptr;                               // device status word (TPROD_STATUS_* bits), tprod_status
   cudaStream_t cap = nullptr;                          // private capture stream
+  // small problems: K1 of A on a side stream concurrently with K1 of B (fork / join by events)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     int seen = 0;                                      // direct runs before capture (< 0: capture failed, never retry)
@@ -116,9 +119,12 @@ bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
 // ---------------------------------------------------------------- workspace layout
 struct Layout32 {
   int64_t h, lda, ldb, ldc;
-  size_t off_maxA, off_maxB, off_uA, off_uB, off_Ab, off_Bb, off_Cb, off_W, W_bytes, total;
+  size_t off_maxA, off_maxB, off_uA, off_uB, off_Ab, off_Bb, off_Cb, off_W, W_bytes, off_W2, W2_bytes, total;
 };
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Small operands: K1 of A runs on a side stream concurrently with K1 of B (launch_f32).
+bool fork_dims(int64_t n1, int64_t n2, int64_t n3, int64_t n4) { return (n1 * n2 + n2 * n4) * n3 <= (int64_t)40 << 20; }
 
 // with_A = false: no A-bar region (prepared-operand calls read the handle's prepared planes)
 Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = true) {
@@ -142,6 +148,9 @@ Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = 
   fourstep_factors(n3, &f1, &f2);
   L.W_bytes = f1 ? 4 * (size_t)(std::max({with_A ? n1 * n2 : (int64_t)0, n2 * n4, n1 * n4}) * n3) : 0;
   L.off_W = o;    o = align_up(o + L.W_bytes, 1024);
+  // A's own four-step intermediate when K1 of A runs concurrently with K1 of B
+  L.W2_bytes = f1 && with_A && fork_dims(n1, n2, n3, n4) ? 4 * (size_t)(n1 * n2 * n3) : 0;
+  L.off_W2 = o;   o = align_up(o + L.W2_bytes, 1024);
   L.total = o;
   return L;
 }
@@ -448,6 +457,24 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
                    [&](cudaStream_t ls) { return launch_f32(h, A, B, C, n1, n2, n3, n4, ls, pa, L, T); });
 }
 
+// Side stream + fork / join events of the handle (created with the handle; false = run sequentially).
+bool fork_ready(tprod_ctx* h) {
+  if (!h->aux && cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    h->aux = nullptr;
+    return false;
+  }
+  if (!h->ev_fork && cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (!h->ev_join && cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
 int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, int64_t n2, int64_t n3,
                int64_t n4, cudaStream_t s, const PreparedA* pa, const Layout32& L, Twiddles32 T) {
   int st = 0;
@@ -476,9 +503,25 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0;
   launches += vec ? 1 : (A0 ? 2 : 1);
   mark(1);
-  // B first: the tail of B just streamed by K0 is still resident in L2
+  // Small operands (neither forward transform fills the GPU for long): K1 of A runs on a side stream
+  // concurrently with K1 of B (measured on config 2 / 4).  Otherwise B first: the tail
+  // of B just streamed by K0 is still resident in L2.
+  const bool fork = !pa && fork_dims(n1, n2, n3, n4) && (!L.W_bytes || L.W2_bytes) && fork_ready(h);
+  if (fork) {
+    Twiddles32 TA = T;                                  // four-step: A's own intermediate
+    if (L.W2_bytes) {
+      TA.scratch = (float*)(ws + L.off_W2);
+      TA.scratch_bytes = L.W2_bytes;
+    }
+    CK(cudaEventRecord(h->ev_fork, s));
+    CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+    launch_fwd_split(A, n1, n2, n3, 0, maxA, TA, Ab, L.lda, uA, h->num_sms, h->aux); ++launches;   // Alg.1 step 1 (A)
+    CK(cudaEventRecord(h->ev_join, h->aux));
+  }
   launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
-  if (!pa) {
+  if (fork) {
+    CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+  } else if (!pa) {
     launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
   }
   mark(2);
@@ -718,6 +761,7 @@ int tprod_create(int device, tprod_handle* out) {
   h->device = device;
   h->num_sms = prop.multiProcessorCount;
   h->status = status;
+  fork_ready(h);                      // side stream + events now, never inside a stream capture
   *out = h;
   return TPROD_OK;
 }
@@ -743,6 +787,9 @@ int tprod_destroy(tprod_handle h) {
   if (h->cs_out) cudaStreamDestroy(h->cs_out);
   clear_graphs(h);
   if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ws) cudaFree(h->ws);
   if (h->status) cudaFree(h->status);
   for (void* p : h->retired) cudaFree(p);

@@ -145,13 +145,36 @@ __global__ void __launch_bounds__(256) absmax2_kernel(const float* __restrict__ 
       const int64_t j = w % n4, k0 = w / n4;
       float m = 0.f;
       const int64_t r4 = n2 >> 2;                      // float4 per run B(:, j, k)
-      if (r4 >= 32) {
+      if (r4 >= 128) {
         for (int64_t k = k0; k < n3; k += wpc) {
           const float4* x = reinterpret_cast<const float4*>(B + n2 * (j + n4 * k));   // run (j,k)
 #pragma unroll 4
           for (int64_t l4 = lane; l4 < r4; l4 += 32) {
             float4 v = __ldg(x + l4);
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
+        }
+      } else if (r4 >= 32) {
+        // runs of 128..508 floats (config 2): KU runs of the column at a time, two float4 per run
+        // and lane, 8 loads in flight per lane (one run at a time measured 17.4 us for config 2's
+        // K0, this 13.5 us; long runs keep the loop above, which measured faster on config 3)
+        constexpr int KU = 4;
+        for (int64_t kb = k0; kb < n3; kb += KU * wpc) {
+          for (int64_t l4 = lane; l4 < r4; l4 += 64) {
+            float4 v[KU][2];
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+              const int64_t k = kb + u * wpc;
+              const float4* x = reinterpret_cast<const float4*>(B + n2 * (j + n4 * k));   // run (j,k)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+                v[u][hh] = (k < n3 && l4 + 32 * hh < r4) ? __ldg(x + l4 + 32 * hh) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < KU; ++u)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh)
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u][hh].x), fabsf(v[u][hh].y)), fmaxf(fabsf(v[u][hh].z), fabsf(v[u][hh].w))));
           }
         }
       } else {
@@ -192,6 +215,10 @@ void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int6
   const double szA = A ? (double)n1 * n2 * n3 : 0.0, szB = B ? (double)n2 * n4 * n3 : 0.0;
   const int64_t total = (int64_t)num_sms * 8;
   int64_t nbA_target = (int64_t)(total * szA / (szA + szB));
+  // small operands: >= 64 KB per CTA (config 2's 8 MB A took 592 CTAs of 14 KB each, and their
+  // 592 x n1 same-address atomicMax updates cost more than the loads: 13.5 us for 16.8 MB)
+  const int64_t capA = (int64_t)(szA * 4.0 / 65536.0) + 1, capB = (int64_t)(szB * 4.0 / 65536.0) + 1;
+  if (nbA_target > capA) nbA_target = capA;
   if (nbA_target < 1) nbA_target = 1;
   int txv = 1;
   while (txv < 64 && 4 * txv < n1) txv <<= 1;       // float4 lanes across p (narrow A: more column lanes)
@@ -205,6 +232,7 @@ void launch_absmax2(const float* A, const float* B, int64_t n1, int64_t n2, int6
   int64_t nbB = total - gxA * gyA;
   const int64_t runsB = n4 * n3;
   if (nbB > (runsB + 7) / 8) nbB = (runsB + 7) / 8;      // at most one run per warp
+  if (nbB > capB) nbB = capB;
   if (nbB < 1) nbB = 1;
   if (!B) nbB = 0;
   absmax2_kernel<<<(unsigned)(gxA * gyA + nbB), 256, 0, s>>>(A, n1, colsA, (int)gyA, (int)gxA, txv, B, n2,
