@@ -124,7 +124,12 @@ struct Layout32 {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Small operands: K1 of A runs on a side stream concurrently with K1 of B (launch_f32).
-bool fork_dims(int64_t n1, int64_t n2, int64_t n3, int64_t n4) { return (n1 * n2 + n2 * n4) * n3 <= (int64_t)40 << 20; }
+#ifndef TPROD_FORK_MELEMS
+#define TPROD_FORK_MELEMS 256
+#endif
+bool fork_dims(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
+  return (n1 * n2 + n2 * n4) * n3 <= (int64_t)TPROD_FORK_MELEMS << 20;
+}
 
 // with_A = false: no A-bar region (prepared-operand calls read the handle's prepared planes)
 Layout32 layout32(int64_t n1, int64_t n2, int64_t n3, int64_t n4, bool with_A = true) {
