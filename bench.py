@@ -411,14 +411,21 @@ def roofline(meas, peaks, src, workload, sustained):
 
     def gbs(b, t):
         return b / (t * 1e-3) / 1e9 if t > 0 else None
-    stages = {
-        "K0 scales": {"ms": k0, "bytes": sb["K0"], "GB/s": gbs(sb["K0"], k0), "frac": gbs(sb["K0"], k0) / BW},
-        "K1 forward DFT (A, B)": {"ms": k1, "bytes": sb["K1"], "GB/s": gbs(sb["K1"], k1),
-                                  "frac": gbs(sb["K1"], k1) / BW},
+    if k1 == 0.0:
+        # the A chain (K0 + K1 of A) ran concurrently with the B chain: one combined stage (tprod.h)
+        b01 = sb["K0"] + sb["K1"]
+        stages = {"K0 + K1 scales and forward DFTs (A, B chains concurrent)": {
+            "ms": k0, "bytes": b01, "GB/s": gbs(b01, k0), "frac": gbs(b01, k0) / BW}}
+    else:
+        stages = {
+            "K0 scales": {"ms": k0, "bytes": sb["K0"], "GB/s": gbs(sb["K0"], k0), "frac": gbs(sb["K0"], k0) / BW},
+            "K1 forward DFT (A, B)": {"ms": k1, "bytes": sb["K1"], "GB/s": gbs(sb["K1"], k1),
+                                      "frac": gbs(sb["K1"], k1) / BW}}
+    stages.update({
         "K2 GEMM": {"ms": k2, "TFLOP/s": achieved, "frac": achieved / P},
         "K3 fill + inverse DFT": {"ms": k3, "bytes": sb["K3"], "GB/s": gbs(sb["K3"], k3),
                                   "frac": gbs(sb["K3"], k3) / BW},
-    }
+    })
     return {"bound": "tensor", "achieved": achieved, "peak": P, "unit": "TFLOP/s",
             "frac": achieved / P, "traffic": tr,
             "kernel": "K2 per-frequency complex GEMM (gemm_tc2_kernel / gemm_tc_kernel)",

@@ -244,7 +244,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value);
 /* With TPROD_OPT_TIMING = 1, tprod_f32 records CUDA events on its stream between the stages of
  * the path; this returns the durations (ms) of the most recent call's stages, in order
  * [K0 scales, K1 forward DFTs, K2 per-frequency GEMMs, K3 inverse DFT], synchronising on the
- * last event.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that call. */
+ * last event.  When the call ran the A chain (K0 + K1 of A) concurrently with the B chain (operands
+ * of at most 256M elements, no prepared A), the first entry covers K0 and K1 of both operands and
+ * the second is exactly 0.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that
+ * call. */
 int tprod_last_stage_ms(tprod_handle h, float* out);
 
 /* Status word of the handle: an OR of the TPROD_STATUS_* bits raised on the device by the handle's

@@ -53,6 +53,7 @@ struct tprod_ctx {
   int rank = 0, world = 1;
   bool timing = false;
   bool timed_last = false;
+  bool forked_last = false;           // the last timed call ran the A / B chains concurrently
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   PreparedA prep;
   // pipelined host entry point (tprod_f32_host): copy streams, double-buffer events, its own A
@@ -126,6 +127,9 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // Small operands: K1 of A runs on a side stream concurrently with K1 of B (launch_f32).
 #ifndef TPROD_FORK_MELEMS
 #define TPROD_FORK_MELEMS 256
+#endif
+#ifndef TPROD_FORK_K0
+#define TPROD_FORK_K0 1
 #endif
 bool fork_dims(int64_t n1, int64_t n2, int64_t n3, int64_t n4) {
   return (n1 * n2 + n2 * n4) * n3 <= (int64_t)TPROD_FORK_MELEMS << 20;
@@ -504,30 +508,42 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   mark(0);
   CK(cudaMemsetAsync(ws + L.off_maxA, 0, L.off_uA - L.off_maxA, s));
   const float* A0 = pa ? nullptr : A;
-  launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
-  const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0;
-  launches += vec ? 1 : (A0 ? 2 : 1);
-  mark(1);
-  // Small operands (neither forward transform fills the GPU for long): K1 of A runs on a side stream
-  // concurrently with K1 of B (measured on config 2 / 4).  Otherwise B first: the tail
-  // of B just streamed by K0 is still resident in L2.
+  // Operands up to TPROD_FORK_MELEMS: the A chain (K0 + K1 of A) runs on a side stream concurrently
+  // with the B chain (measured on configs 2, 3 and 4), each K1 right after its own K0
+  // (its operand partly still in L2).  Otherwise one K0 launch for both, then B first: the tail of
+  // B just streamed by K0 is still resident in L2.
   const bool fork = !pa && fork_dims(n1, n2, n3, n4) && (!L.W_bytes || L.W2_bytes) && fork_ready(h);
+  h->forked_last = fork;              // tprod_last_stage_ms: stage 0 = K0 + K1 of both chains, stage 1 = 0
   if (fork) {
     Twiddles32 TA = T;                                  // four-step: A's own intermediate
     if (L.W2_bytes) {
       TA.scratch = (float*)(ws + L.off_W2);
       TA.scratch_bytes = L.W2_bytes;
     }
-    CK(cudaEventRecord(h->ev_fork, s));
-    CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+    if (TPROD_FORK_K0) {                                // fork before K0: one K0 launch per chain
+      CK(cudaEventRecord(h->ev_fork, s));
+      CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+      launch_absmax2(A, nullptr, n1, n2, n3, 1, maxA, nullptr, h->num_sms, h->aux); ++launches;
+      launch_absmax2(nullptr, B, n1, n2, n3, n4, nullptr, maxB, h->num_sms, s); ++launches;
+    } else {                                            // fork after the shared K0 launch
+      launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);
+      launches += (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0 && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 2;
+      CK(cudaEventRecord(h->ev_fork, s));
+      CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+    }
     launch_fwd_split(A, n1, n2, n3, 0, maxA, TA, Ab, L.lda, uA, h->num_sms, h->aux); ++launches;   // Alg.1 step 1 (A)
     CK(cudaEventRecord(h->ev_join, h->aux));
-  }
-  launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
-  if (fork) {
+    launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
     CK(cudaStreamWaitEvent(s, h->ev_join, 0));
-  } else if (!pa) {
-    launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
+  } else {
+    launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
+    const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0;
+    launches += vec ? 1 : (A0 ? 2 : 1);
+    mark(1);
+    launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
+    if (!pa) {
+      launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
+    }
   }
   mark(2);
   if ((st = launch_status())) return st;
@@ -1266,7 +1282,13 @@ int tprod_status(tprod_handle h, void* stream, int* bits) {
 int tprod_last_stage_ms(tprod_handle h, float* out) {
   if (!h || !out || !h->timed_last) return TPROD_EINVAL;
   CK(cudaEventSynchronize(h->ev[4]));
-  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
+  if (h->forked_last) {               // concurrent A / B chains: K0 + K1 as one stage (tprod.h)
+    CK(cudaEventElapsedTime(out, h->ev[0], h->ev[2]));
+    out[1] = 0.f;
+  } else {
+    for (int i = 0; i < 2; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
+  }
+  for (int i = 2; i < 4; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
   return TPROD_OK;
 }
 

@@ -64,3 +64,10 @@ def test_roofline_call_frac_and_stage_rates():
     assert abs(r["stages"]["K3 fill + inverse DFT"]["frac"] - (8 * h + 4 * n3) * n1 * n4 / 0.05e-3 / 1e9 / 6000) < 1e-9
     rs = bench.roofline(meas, peaks, "test", "c3", sustained=True)
     assert abs(rs["peak"] - 400.0) < 1e-9
+    # concurrent A / B chains: the library reports K0 + K1 as stage 0 and 0 for stage 1
+    meas2 = dict(meas, stage_ms=[0.12, 0.0, 0.2, 0.05])
+    r2 = bench.roofline(meas2, peaks, "test", "c3", sustained=False)
+    comb = r2["stages"]["K0 + K1 scales and forward DFTs (A, B chains concurrent)"]
+    sb = bench.stage_bytes(n1, n2, n3, n4)
+    assert abs(comb["GB/s"] - (sb["K0"] + sb["K1"]) / 0.12e-3 / 1e9) < 1e-6
+    assert "K1 forward DFT (A, B)" not in r2["stages"] and "K2 GEMM" in r2["stages"]
