@@ -210,7 +210,14 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
  * GEMM (a slower second GEMM on the same split operands; used to cross-check the tcgen05
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
-       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7, TPROD_OPT_SYNC_CHECKS = 8 };
+       TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7, TPROD_OPT_SYNC_CHECKS = 8,
+       TPROD_OPT_OVERLAP = 9 };
+/* TPROD_OPT_OVERLAP (tprod_f32 / tprod_f32_prepared): 1 (default) = when the per-frequency GEMM runs on
+ * CTA pairs in 2..8 tile rounds and K3 is the tube-pair register kernel (n3 <= 32), the GEMM takes
+ * its tiles frequency-fastest and counts finished (m, n) output tiles in a device array of the
+ * handle, and K3 is launched as a programmatic dependent whose blocks each wait for the tile they
+ * read: the inverse of finished tiles runs on the SMs the GEMM's last round leaves idle (Alg. 1
+ * steps 2-3 overlapped).  0 = K3 strictly after the GEMM.  Bitwise identical results. */
 /* TPROD_OPT_SYNC_CHECKS: 1 (default) = tprod_tinv_f32 waits for its stream and returns
  * TPROD_ESINGULAR for a singular tensor; 0 = it returns at once and reports singularity through
  * the status word (tprod_status). */
@@ -246,7 +253,8 @@ int tprod_set_option(tprod_handle h, int option, int64_t value);
  * [K0 scales, K1 forward DFTs, K2 per-frequency GEMMs, K3 inverse DFT], synchronising on the
  * last event.  When the call ran the A chain (K0 + K1 of A) concurrently with the B chain (operands
  * of at most 256M elements, no prepared A), the first entry covers K0 and K1 of both operands and
- * the second is exactly 0.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that
+ * the second is exactly 0; when K3 ran overlapped with the GEMM (TPROD_OPT_OVERLAP), the third entry
+ * covers K2 and K3 and the fourth is exactly 0.  `out` must hold 4 floats.  TPROD_EINVAL if timing was off for that
  * call. */
 int tprod_last_stage_ms(tprod_handle h, float* out);
 

@@ -54,6 +54,9 @@ struct tprod_ctx {
   bool timing = false;
   bool timed_last = false;
   bool forked_last = false;           // the last timed call ran the A / B chains concurrently
+  bool overlap = true;                // TPROD_OPT_OVERLAP: K3 as a programmatic dependent of the GEMM
+  bool overlapped_last = false;       // the last timed call overlapped K2 and K3 (one stage)
+  int* done = nullptr;                // OVERLAP_COUNTERS (m, n) tile counters (internal.h OverlapK3)
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   PreparedA prep;
   // pipelined host entry point (tprod_f32_host): copy streams, double-buffer events, its own A
@@ -461,7 +464,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   std::vector<int64_t> key = {1, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
                               (int64_t)(uintptr_t)h->ws, pa ? (int64_t)(uintptr_t)pa->Ab : 0,
                               pa ? (int64_t)(uintptr_t)pa->uA : 0, pa ? pa->lda : 0, h->engine, h->force_bn,
-                              h->force_cn, h->transform};
+                              h->force_cn, h->transform, h->overlap ? 1 : 0};
   return graph_run(h, std::move(key), s,
                    [&](cudaStream_t ls) { return launch_f32(h, A, B, C, n1, n2, n3, n4, ls, pa, L, T); });
 }
@@ -548,18 +551,26 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   mark(2);
   if ((st = launch_status())) return st;
   bool tc = h->engine == 0 && gemm_tc_supported();
+  OverlapK3 ov;
   if (tc) {
+    // the counters only where K3 is the tube-pair register kernel (the one that waits on them)
+    int* done = h->overlap && h->done && !T.tc && inv_dense_pair_ok(n3) ? h->done : nullptr;
     st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3 % 2 == 0 ? 1 : 0,
-                              h->force_bn, h->force_cn, h->num_sms, s);
+                              h->force_bn, h->force_cn, h->num_sms, s, done, &ov);
     if (st) return st;
   } else {
     launch_gemm_simt_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, s);
   }
   ++launches;                                                     // Alg.1 step 2
-  mark(3);
+  // K3 overlapped with the GEMM's last tile round (internal.h OverlapK3): no event between the two
+  // launches (it would serialise them), the stage timer reports K2 + K3 as one stage
+  h->overlapped_last = ov.done != nullptr;
+  if (!ov.done) mark(3);
   // Alg.1 step 2b + 3; each output tube (i, j) unscaled by uA[i] uB[j] after the inverse (R18)
-  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, OutUnscale{uA, uB}, C, h->num_sms, s);
+  launch_inv_f32(Cb, Cb + n4 * L.ldc, L.ldc, 2 * n4 * L.ldc, n1, n4, n3, T, OutUnscale{uA, uB}, C, h->num_sms, s,
+                 ov.done ? &ov : nullptr);
   ++launches;
+  if (ov.done) mark(3);
   mark(4);
   h->timed_last = h->timing;
   h->last_launches = launches;
@@ -778,7 +789,13 @@ int tprod_create(int device, tprod_handle* out) {
   int* status = nullptr;
   CK(cudaMalloc(&status, sizeof(int)));
   CK(cudaMemset(status, 0, sizeof(int)));
+  int* done = nullptr;
+  if (cudaMalloc(&done, sizeof(int) * OVERLAP_COUNTERS) != cudaSuccess) {
+    cudaFree(status);
+    return TPROD_ECUDA;
+  }
   tprod_ctx* h = new tprod_ctx;
+  h->done = done;
   h->device = device;
   h->num_sms = prop.multiProcessorCount;
   h->status = status;
@@ -813,6 +830,7 @@ int tprod_destroy(tprod_handle h) {
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ws) cudaFree(h->ws);
   if (h->status) cudaFree(h->status);
+  if (h->done) cudaFree(h->done);
   for (void* p : h->retired) cudaFree(p);
   delete h;
   return TPROD_OK;
@@ -1262,6 +1280,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       if (value != 0 && value != 1) return TPROD_EINVAL;
       h->sync_checks = value != 0;
       return TPROD_OK;
+    case TPROD_OPT_OVERLAP:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->overlap = value != 0;
+      return TPROD_OK;
     default:
       return TPROD_EINVAL;
   }
@@ -1288,7 +1310,12 @@ int tprod_last_stage_ms(tprod_handle h, float* out) {
   } else {
     for (int i = 0; i < 2; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
   }
-  for (int i = 2; i < 4; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
+  if (h->overlapped_last) {           // K2 and K3 overlapped: one stage (tprod.h)
+    CK(cudaEventElapsedTime(out + 2, h->ev[2], h->ev[4]));
+    out[3] = 0.f;
+  } else {
+    for (int i = 2; i < 4; ++i) CK(cudaEventElapsedTime(out + i, h->ev[i], h->ev[i + 1]));
+  }
   return TPROD_OK;
 }
 

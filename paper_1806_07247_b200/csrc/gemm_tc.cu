@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
 template <int SEGKB, int CM>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h, int nyq) {
+                    float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h, int nyq,
+                    int* __restrict__ done) {
   constexpr int BN = 128;
   constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
   constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
@@ -383,15 +384,26 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   cluster_sync();                 // both CTAs' barriers initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // K2 -> K3 overlap (internal.h OverlapK3): every CTA is resident now, so the dependent inverse may
+  // launch; its blocks take the SMs this grid leaves idle and wait on `done` per output tile.
+  if (done) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Tile order: n fastest, then m, then f; concurrently running pairs share the A_f panel.
   // (Measured on config 5, DRAM read per launch: n fastest 149-165 GB, m fastest 185 GB, groups of
   // 6 m-tiles per n sweep 180 GB -- the pairs drift apart in K by up to a tile, longer than an L2
   // residency, so no raster order recovers the reuse; the plain order stays.)
+  // With `done` (few tile rounds, K3 overlapped): f fastest, so the (m, n) output tiles complete
+  // one after another and the inverse of the first ones runs during the last round.
   const int64_t tpf = (int64_t)mt * nt;
   auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {   // m0: this pair's first row
-    f = (int)(t / tpf);
-    const int r = (int)(t - (int64_t)f * tpf);
+    int r;
+    if (done) {
+      r = (int)(t / h);
+      f = (int)(t - (int64_t)r * h);
+    } else {
+      f = (int)(t / tpf);
+      r = (int)(t - (int64_t)f * tpf);
+    }
     n0 = (r % nt) * BN;
     m0 = (r / nt) * (2 * CM * BM) + 2 * BM * (int)pr;
   };
@@ -535,6 +547,13 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
           }
         }
       }
+      if (done) {                                  // this warp's part of tile (m, n) at f is stored
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(done + (t / h), 1);
+        }
+      }
     }
   }
 
@@ -634,7 +653,7 @@ int launch_bn(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, i
 template <int SEGKB, int CM>
 int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb, int64_t ldc, int64_t n1,
                 int64_t n2, int64_t n4, int64_t h, int nyq, int num_sms,
-                cudaStream_t s) {
+                cudaStream_t s, int* done, OverlapK3* ov) {
   constexpr int BN = 128;
   constexpr int STAGE = NPLANES * (BK * BM * 2 + (BN / 2) * BK * 2);
   constexpr int STAGES = (227 * 1024 - 2048) / STAGE;
@@ -675,7 +694,20 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq) != cudaSuccess) return 4;
+  // K3 overlap only pays when the grid runs few tile rounds (the last one partial): the counters need
+  // the frequency-fastest order, which on long runs re-reads panels the n-fastest order shares
+  const int64_t mtl = (n1 + 2 * CM * BM - 1) / (2 * CM * BM), ntl = (n4 + BN - 1) / BN;
+  const int64_t rounds = (nct + max_cl - 1) / max_cl;
+  if (!(done && ov && rounds >= 2 && rounds <= 8 && mtl * ntl <= OVERLAP_COUNTERS)) done = nullptr;
+  if (done) {
+    if (cudaMemsetAsync(done, 0, sizeof(int) * mtl * ntl, s) != cudaSuccess) return 4;
+    ov->done = done;
+    ov->target = (int)(h * 2 * CM * EPI_WARPS);
+    ov->pb_per_m = CM;                               // 2 CM * 128 rows = CM blocks of 256 rows
+    ov->cols_per_n = BN;
+    ov->nt = (int)ntl;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq, done) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 
@@ -685,7 +717,7 @@ bool gemm_tc_supported() { return tc::encode_fn() != nullptr; }
 
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb, float* Cb,
                          int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h, int nyq, int force_bn, int force_cn,
-                         int num_sms, cudaStream_t s) {
+                         int num_sms, cudaStream_t s, int* done, OverlapK3* ov) {
   CUtensorMap ma;
   if (!tc::make_map(&ma, Ab, (uint64_t)n1, (uint64_t)n2, (uint64_t)(NPLANES * h), (uint64_t)lda, 64,
                     tc::BK, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -705,11 +737,11 @@ int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_
   // cluster tiles still fill the GPU several times over (fewer, larger tiles would lengthen the tail)
   if (cn == 4 || (cn == 0 && force_bn == 0 && n1 >= 1024 &&
                   ((n1 + 511) / 512) * ((n4 + 127) / 128) * h >= 4 * (num_sms / 4))) {
-    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 2>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s, done, ov);
   }
   if (cn == 3 || (cn == 0 && force_bn == 0 && n1 > 128 &&
                   ((n1 + 255) / 256) * ((n4 + 127) / 128) * h >= num_sms / 2)) {
-    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s);
+    if (pair_ok) return tc::launch_pair<tc::SEG_KB, 1>(ma, Bb, ldb, Cb, ldc, n1, n2, n4, h, nyq, num_sms, s, done, ov);
   }
   if (cn == 0) cn = (nt >= 2 && mt * ((nt + 1) / 2) * h >= num_sms / 2) ? 2 : 1;   // share A tiles
   if (bn == 128)

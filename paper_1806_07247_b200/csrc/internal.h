@@ -62,10 +62,25 @@ void launch_gemm_simt_split(const __half* Ab, int64_t lda, const __half* Bb, int
 bool gemm_tc_supported();
 // nyq = 1 if slice h-1 is a real Nyquist slice (n3 even): DC and Nyquist slices have exactly zero
 // Im planes and run only the Ar.Br products.
+// K2 -> K3 overlap (TPROD_OPT_OVERLAP): with `done` set, a CTA-pair GEMM of few tile
+// rounds runs its tiles frequency-fastest and counts finished (m, n) output tiles in done[m * nt + n]
+// (release: every epilogue warp of the pair adds 1 per frequency after its stores, `target` in
+// all); K3 is then launched as a programmatic dependent and each of its blocks waits (acquire) for
+// the counter of the tile it reads, so the inverse of finished tiles runs on the SMs the GEMM's
+// last partial round leaves idle.  `ov` is filled by the GEMM launch (used = false: no counters).
+constexpr int OVERLAP_COUNTERS = 1024;   // (m, n) tile counters per handle
+struct OverlapK3 {
+  const int* done = nullptr;
+  int target = 0;       // counter value of a finished (m, n) tile: h * 2 CM * epilogue warps
+  int pb_per_m = 1;     // 256-row K3 blocks per GEMM m tile (2 CM * 128 rows)
+  int cols_per_n = 128; // GEMM N tile
+  int nt = 0;           // GEMM n tiles
+  bool used = false;
+};
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
                          int nyq, int force_bn, int force_cn,
-                         int num_sms, cudaStream_t s);
+                         int num_sms, cudaStream_t s, int* done = nullptr, OverlapK3* ov = nullptr);
 
 // K3: fused conjugate fill + inverse DFT, C-bar planes [f][re|im][q][ld] -> real X (p x q x n3).
 // Cre/Cim: first planes; slice f at Cre + f*fstride (production: fstride = 2*Q*ld).  Output tube
@@ -76,7 +91,8 @@ struct OutUnscale {
   const float* col = nullptr;
 };
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s);
+                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s,
+                    OverlapK3* ov = nullptr);
 
 // TMA-staged persistent dense transforms for n3 <= 64 (transforms_tma.cu); false = not handled
 // (unaligned shapes fall back to the register kernels of transforms_dense.cu).  The inverse
@@ -180,7 +196,10 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
                       const unsigned* maxbits, __half* out, int64_t ld, float* unscale,
                       cudaStream_t s);
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s);
+                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s,
+                      OverlapK3* ov = nullptr);
+// true if launch_inv_dense takes the tube-pair kernel for this n3 (the one that honours OverlapK3)
+bool inv_dense_pair_ok(int64_t n3);
 
 // In-smem mixed-radix (16/8/4/2, 3, 5) Stockham FFT transforms for 5-smooth 64 < n3 <= 16384
 // (transforms_fft.cu).

@@ -412,7 +412,8 @@ __global__ void inv_kernel(const T* __restrict__ Cre, const T* __restrict__ Cim,
 }
 
 void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s) {
+                    int64_t Q, int64_t n3, Twiddles32 tw, OutUnscale u, float* X, int num_sms, cudaStream_t s,
+                    OverlapK3* ov) {
   const bool prod_layout = tw.staged && Cim == Cre + Q * ld && fstride == 2 * Q * ld;
   if (prod_layout && tw.tc && launch_inv_dft_tc(Cre, ld, P, Q, n3, u, X, num_sms, s)) return;
   cudaGetLastError();
@@ -422,7 +423,7 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   cudaGetLastError();
   if (prod_layout && launch_inv_4step(Cre, ld, P, Q, n3, tw, u, X, num_sms, s)) return;
   cudaGetLastError();
-  if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, u, X, s)) return;
+  if (launch_inv_dense(Cre, Cim, ld, fstride, P, Q, n3, u, X, s, ov)) return;
   if (launch_inv_fft(Cre, Cim, ld, fstride, P, Q, n3, tw.st, u, X, s)) return;
   cudaGetLastError();
   const int threads = 128;

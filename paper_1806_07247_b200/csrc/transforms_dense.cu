@@ -321,15 +321,49 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
   }
 }
 
+// OverlapK3 (ov.done != nullptr): launched as a programmatic dependent of the GEMM; block b takes
+// the (m, n) GEMM tile r = b / (128 pb_per_m) -- blocks ordered as the frequency-fastest GEMM
+// finishes its tiles -- and waits until done[r] reaches the tile's count (ld.acquire.gpu by one
+// thread, then a CTA barrier) before it reads C-bar through L2 (ld.global.cg: never a line an
+// L1 might hold from before the GEMM wrote it).
+struct OvArgs {
+  const int* done;
+  int target, pb_per_m, cols_per_n, nt;
+};
+
 template <int N>
 __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict__ Cre,
                                                          const float* __restrict__ Cim, int64_t ld,
                                                          int64_t fstride, int64_t P, int64_t Q,
-                                                         OutUnscale u, float* __restrict__ X) {
+                                                         OutUnscale u, float* __restrict__ X, OvArgs ov) {
   constexpr int H = N / 2 + 1;
   const int64_t pblocks = (P + 255) >> 8;
-  const int64_t q = blockIdx.x / pblocks;
-  const int64_t p = ((blockIdx.x - q * pblocks) * 128 + threadIdx.x) * 2;
+  int64_t q, pb;
+  if (ov.done) {
+    const int per = 128 * ov.pb_per_m;               // K3 blocks per (m, n) tile (cols_per_n = 128)
+    const int r = (int)(blockIdx.x / per), j = (int)(blockIdx.x % per);
+    q = (int64_t)(r % ov.nt) * ov.cols_per_n + (j % ov.cols_per_n);
+    pb = (int64_t)(r / ov.nt) * ov.pb_per_m + j / ov.cols_per_n;
+    if (q >= Q || pb >= pblocks) return;             // whole block: ragged edge of the tile grid
+    if (threadIdx.x == 0) {
+      const int* c = ov.done + r;
+      int v;
+      uint64_t t0, t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= ov.target) break;
+        __nanosleep(500);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 4000000000ull) __trap();       // 4 s: a counter that never completes is a bug, not a wait
+      }
+    }
+    __syncthreads();
+  } else {
+    q = blockIdx.x / pblocks;
+    pb = blockIdx.x - q * pblocks;
+  }
+  const int64_t p = (pb * 128 + threadIdx.x) * 2;
   if (p >= P) return;
   const float2* cr = reinterpret_cast<const float2*>(Cre + q * ld + p);
   const float2* ci = reinterpret_cast<const float2*>(Cim + q * ld + p);
@@ -342,8 +376,8 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
 #pragma unroll
     for (int f = 0; f < H; ++f) {
       const bool self = (f == 0 || 2 * f == N);
-      const float2 r = __ldg(cr + fs * f);
-      const float2 i = self ? make_float2(0.f, 0.f) : __ldg(ci + fs * f);
+      const float2 r = __ldcg(cr + fs * f);
+      const float2 i = self ? make_float2(0.f, 0.f) : __ldcg(ci + fs * f);
       X0[f] = make_float2(r.x, i.x);
       X1[f] = make_float2(r.y, i.y);
     }
@@ -359,12 +393,12 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
   for (int f = 0; f < H; ++f) {
     const bool self = (f == 0 || 2 * f == N);
     const float wf = self ? 1.f : 2.f;     // conjugate fill weight
-    const float2 r = __ldg(cr + fs * f);
+    const float2 r = __ldcg(cr + fs * f);
     R[f] = make_float2(wf * r.x, wf * r.y);
     if (self) {
       I[f] = make_float2(0.f, 0.f);         // Im of DC/Nyquist dropped (C2R)
     } else {
-      const float2 i = __ldg(ci + fs * f);
+      const float2 i = __ldcg(ci + fs * f);
       I[f] = make_float2(wf * i.x, wf * i.y);
     }
   }
@@ -390,6 +424,7 @@ __global__ void __launch_bounds__(128) inv_dense2_kernel(const float* __restrict
 // ------------------------------------------------------------------------------ dispatch tables
 using FwdFn = void (*)(const float*, int64_t, int64_t, const unsigned*, __half*, int64_t, float*);
 using InvFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, OutUnscale, float*);
+using InvPFn = void (*)(const float*, const float*, int64_t, int64_t, int64_t, int64_t, OutUnscale, float*, OvArgs);
 
 template <int N>
 struct DenseTable {
@@ -407,7 +442,7 @@ struct DenseTable<0> {
 
 template <int N>
 struct PairTable {
-  static void fill(FwdFn* f0, FwdFn* f1, InvFn* inv) {
+  static void fill(FwdFn* f0, FwdFn* f1, InvPFn* inv) {
     f0[N] = fwd_dense2_kernel<N, 0>;
     f1[N] = fwd_dense2_kernel<N, 1>;
     inv[N] = inv_dense2_kernel<N>;
@@ -416,7 +451,7 @@ struct PairTable {
 };
 template <>
 struct PairTable<0> {
-  static void fill(FwdFn*, FwdFn*, InvFn*) {}
+  static void fill(FwdFn*, FwdFn*, InvPFn*) {}
 };
 
 struct DenseFns {
@@ -425,7 +460,7 @@ struct DenseFns {
   InvFn inv[DENSE_MAX + 1] = {};
   FwdFn fwd0p[PAIR_MAX + 1] = {};
   FwdFn fwd1p[PAIR_MAX + 1] = {};
-  InvFn invp[PAIR_MAX + 1] = {};
+  InvPFn invp[PAIR_MAX + 1] = {};
   DenseFns() {
     DenseTable<DENSE_MAX>::fill(fwd0, fwd1, inv);
     PairTable<PAIR_MAX>::fill(fwd0p, fwd1p, invp);
@@ -470,15 +505,37 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
 }
 
+bool inv_dense_pair_ok(int64_t n3) { return n3 >= 1 && n3 <= PAIR_MAX; }
+
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
-                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s) {
+                      int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s, OverlapK3* ov) {
   if (!dense_supported(n3) || !ensure_dense_twiddles()) return false;
   const bool pair = n3 <= PAIR_MAX && P % 2 == 0 && ld % 2 == 0 && fstride % 2 == 0 &&
                     ((uintptr_t)X & 7) == 0 && ((uintptr_t)Cre & 7) == 0 && ((uintptr_t)Cim & 7) == 0;
-  InvFn fn = pair ? dense_fns().invp[n3] : dense_fns().inv[n3];
   int64_t blocks = (P + (pair ? 255 : 127)) / (pair ? 256 : 128) * Q;
-  void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&u, (void*)&X};
-  return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
+  if (!pair) {
+    InvFn fn = dense_fns().inv[n3];
+    void* args[] = {(void*)&Cre, (void*)&Cim, (void*)&ld, (void*)&fstride, (void*)&P, (void*)&Q, (void*)&u, (void*)&X};
+    return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
+  }
+  OvArgs oa = {nullptr, 0, 1, 128, 1};
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  if (ov && ov->done && ov->cols_per_n == 128) {
+    // programmatic dependent of the GEMM just launched on `s`: blocks start as its CTAs free SMs
+    oa = {ov->done, ov->target, ov->pb_per_m, ov->cols_per_n, ov->nt};
+    const int64_t mt = ((P + 255) / 256 + ov->pb_per_m - 1) / ov->pb_per_m;
+    blocks = mt * ov->nt * 128 * (int64_t)ov->pb_per_m;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ov->used = true;
+  }
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  return cudaLaunchKernelEx(&cfg, dense_fns().invp[n3], Cre, Cim, ld, fstride, P, Q, u, X, oa) == cudaSuccess;
 }
 
 }  // namespace tprod

@@ -181,6 +181,42 @@ def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
         assert np.array_equal(o, outs[0])
 
 
+@pytest.mark.parametrize("dims", [(600, 200, 31, 300), (600, 136, 32, 300), (1100, 200, 8, 300),
+                                  (1024, 1024, 31, 512), (520, 96, 5, 1030)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_k3_overlap_bitwise(T, dims):
+    """TPROD_OPT_OVERLAP: the GEMM on CTA pairs in 2..8 tile rounds runs frequency-fastest and counts
+    finished (m, n) tiles; K3 (tube-pair register kernel, n3 <= 32) launches as a programmatic
+    dependent and each block waits for its tile.  Scheduling only: bitwise equal to the serial
+    order, direct launch and graph replay, ragged m / n tiles (600 rows, 300 / 1030 columns),
+    CTA pairs and 4-CTA clusters; vs the oracle (Eq. (9)) on sampled lateral
+    slices; the stage timer reports K2 + K3 as one stage."""
+    import torch
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 21)
+    B = normal((n2, n4, n3), 22)
+    Ad, Bd = dev(A), dev(B)
+    outs = []
+    for ov, cn in ((0, 0), (1, 0), (1, 3), (1, 4)):
+        h = T.Handle()
+        h.set_option(T._lib.TPROD_OPT_OVERLAP, ov)
+        h.set_option(T._lib.TPROD_OPT_GEMM_CLUSTER, cn)
+        for _ in range(3):                                   # direct, capture, graph replay
+            outs.append(host(T.tprod(Ad, Bd, handle=h)))
+        h.set_option(T._lib.TPROD_OPT_TIMING, 1)
+        outs.append(host(T.tprod(Ad, Bd, handle=h)))
+        st = h.last_stage_ms()
+        assert all(x >= 0 for x in st) and st[2] > 0
+        if ov == 0:
+            assert st[3] > 0
+    cols = sample_columns(n4, 6, seed=3)
+    ref = O.tprod_columns(A, B, cols)
+    assert O.rel_err(outs[0][:, cols, :], ref) <= TOL32
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    torch.cuda.synchronize()
+
+
 # ------------------------------------------------------------------------------- stages
 @pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 65, 96, 100, 120, 128, 256, 375, 1000, 1536,
                                 2048, 4096, 6000, 8192, 15360,
