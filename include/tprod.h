@@ -211,7 +211,12 @@ int tprod_idft_f32(const float* Xre, const float* Xim, float* X, int64_t p, int6
  * kernel).  TPROD_OPT_GEMM_BN: force the tcgen05 N tile (0 = auto, else 64 or 128). */
 enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_OPT_GEMM_CLUSTER = 4,
        TPROD_OPT_TRANSFORM = 5, TPROD_OPT_GRAPHS = 6, TPROD_OPT_POISON = 7, TPROD_OPT_SYNC_CHECKS = 8,
-       TPROD_OPT_OVERLAP = 9 };
+       TPROD_OPT_OVERLAP = 9, TPROD_OPT_FUSED_SCALES = 10 };
+/* TPROD_OPT_FUSED_SCALES (tprod_f32 / tprod_f32_prepared): 1 (default) = for n3 <= 32 with n2 even and
+ * <= 2048 and B of at most 8M elements (where it measured faster), B's column scales (the K0 reduction max |B(:, j, :)|) are computed inside B's forward
+ * transform -- the blocks of one lateral slice form a thread-block cluster and exchange their partial
+ * maxima through distributed shared memory -- so B is read once instead of twice; 0 = a separate K0
+ * pass over B.  The same maxima either way: bitwise identical results. */
 /* TPROD_OPT_OVERLAP (tprod_f32 / tprod_f32_prepared): 1 (default) = when the per-frequency GEMM runs on
  * CTA pairs in 2..8 tile rounds and K3 is the tube-pair register kernel (n3 <= 32), the GEMM takes
  * its tiles frequency-fastest and counts finished (m, n) output tiles in a device array of the

@@ -14,7 +14,8 @@ TPROD_OK, TPROD_EINVAL, TPROD_EALIAS, TPROD_ENOMEM, TPROD_ECUDA, TPROD_ENCCL, \
     TPROD_EUNSUPPORTED, TPROD_ENOWORLD, TPROD_ESINGULAR = range(9)
 TPROD_DTYPE_F32, TPROD_DTYPE_F64 = 0, 1
 (TPROD_OPT_ENGINE, TPROD_OPT_GEMM_BN, TPROD_OPT_TIMING, TPROD_OPT_GEMM_CLUSTER, TPROD_OPT_TRANSFORM,
- TPROD_OPT_GRAPHS, TPROD_OPT_POISON, TPROD_OPT_SYNC_CHECKS, TPROD_OPT_OVERLAP) = 1, 2, 3, 4, 5, 6, 7, 8, 9
+ TPROD_OPT_GRAPHS, TPROD_OPT_POISON, TPROD_OPT_SYNC_CHECKS, TPROD_OPT_OVERLAP,
+ TPROD_OPT_FUSED_SCALES) = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 TPROD_STATUS_SINGULAR, TPROD_STATUS_NOCONVERGE = 1, 2
 
 # name -> (restype, argtypes); the full list of symbols include/tprod.h declares

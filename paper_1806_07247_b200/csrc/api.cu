@@ -55,6 +55,7 @@ struct tprod_ctx {
   bool timed_last = false;
   bool forked_last = false;           // the last timed call ran the A / B chains concurrently
   bool overlap = true;                // TPROD_OPT_OVERLAP: K3 as a programmatic dependent of the GEMM
+  bool fused_scales = true;           // TPROD_OPT_FUSED_SCALES: K0 of B inside K1 of B (n3 <= 32)
   bool overlapped_last = false;       // the last timed call overlapped K2 and K3 (one stage)
   int* done = nullptr;                // OVERLAP_COUNTERS (m, n) tile counters (internal.h OverlapK3)
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -464,7 +465,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   std::vector<int64_t> key = {1, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
                               (int64_t)(uintptr_t)h->ws, pa ? (int64_t)(uintptr_t)pa->Ab : 0,
                               pa ? (int64_t)(uintptr_t)pa->uA : 0, pa ? pa->lda : 0, h->engine, h->force_bn,
-                              h->force_cn, h->transform, h->overlap ? 1 : 0};
+                              h->force_cn, h->transform, h->overlap ? 1 : 0, h->fused_scales ? 1 : 0};
   return graph_run(h, std::move(key), s,
                    [&](cudaStream_t ls) { return launch_f32(h, A, B, C, n1, n2, n3, n4, ls, pa, L, T); });
 }
@@ -517,6 +518,17 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   // B just streamed by K0 is still resident in L2.
   const bool fork = !pa && fork_dims(n1, n2, n3, n4) && (!L.W_bytes || L.W2_bytes) && fork_ready(h);
   h->forked_last = fork;              // tprod_last_stage_ms: stage 0 = K0 + K1 of both chains, stage 1 = 0
+  // K0 of B fused into K1 of B (column scales reduced per lateral slice by a CTA cluster inside the
+  // tube-pair transform, n3 <= 32): B is read once instead of twice.  Small B only: measured
+  // config 2 (2M elements) 58.1 -> 57.2 us, config 3 (16M, next to the concurrent A chain) 276 -> 284
+  // us
+  const bool bfused = h->fused_scales && !T.tc && n2 * n4 * n3 <= ((int64_t)8 << 20) && fwd_colmax_ok(B, n2, n3);
+  auto k1_B = [&]() -> int {
+    if (bfused) return launch_fwd_dense_colmax(B, n2, n4, n3, Bb, L.ldb, uB, s) ? 0 : TPROD_ECUDA;
+    launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s);   // Alg.1 step 1 (B)
+    return 0;
+  };
+  const float* B0 = bfused ? nullptr : B;       // B's part of K0
   if (fork) {
     Twiddles32 TA = T;                                  // four-step: A's own intermediate
     if (L.W2_bytes) {
@@ -527,23 +539,32 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
       CK(cudaEventRecord(h->ev_fork, s));
       CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
       launch_absmax2(A, nullptr, n1, n2, n3, 1, maxA, nullptr, h->num_sms, h->aux); ++launches;
-      launch_absmax2(nullptr, B, n1, n2, n3, n4, nullptr, maxB, h->num_sms, s); ++launches;
+      if (B0) {
+        launch_absmax2(nullptr, B0, n1, n2, n3, n4, nullptr, maxB, h->num_sms, s);
+        ++launches;
+      }
     } else {                                            // fork after the shared K0 launch
-      launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);
-      launches += (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0 && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 2;
+      launch_absmax2(A0, B0, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);
+      launches += (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0 && n2 % 4 == 0 && (!B0 || ((uintptr_t)B0 & 15) == 0))
+                      ? 1 : (B0 ? 2 : 1);
       CK(cudaEventRecord(h->ev_fork, s));
       CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
     }
     launch_fwd_split(A, n1, n2, n3, 0, maxA, TA, Ab, L.lda, uA, h->num_sms, h->aux); ++launches;   // Alg.1 step 1 (A)
     CK(cudaEventRecord(h->ev_join, h->aux));
-    launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
+    if ((st = k1_B())) return st;
+    ++launches;
     CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   } else {
-    launch_absmax2(A0, B, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
-    const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 && ((uintptr_t)B & 15) == 0;
-    launches += vec ? 1 : (A0 ? 2 : 1);
+    if (A0 || B0) {
+      launch_absmax2(A0, B0, n1, n2, n3, n4, maxA, maxB, h->num_sms, s);   // row scales of A, col scales of B
+      const bool vec = (!A0 || (n1 % 4 == 0 && ((uintptr_t)A0 & 15) == 0)) && n2 % 4 == 0 &&
+                       (!B0 || ((uintptr_t)B0 & 15) == 0);
+      launches += vec ? 1 : ((A0 ? 1 : 0) + (B0 ? 1 : 0));
+    }
     mark(1);
-    launch_fwd_split(B, n2, n4, n3, 1, maxB, T, Bb, L.ldb, uB, h->num_sms, s); ++launches;   // Alg.1 step 1 (B)
+    if ((st = k1_B())) return st;
+    ++launches;
     if (!pa) {
       launch_fwd_split(A, n1, n2, n3, 0, maxA, T, Ab, L.lda, uA, h->num_sms, s); ++launches;   // Alg.1 step 1 (A)
     }
@@ -1283,6 +1304,10 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
     case TPROD_OPT_OVERLAP:
       if (value != 0 && value != 1) return TPROD_EINVAL;
       h->overlap = value != 0;
+      return TPROD_OK;
+    case TPROD_OPT_FUSED_SCALES:
+      if (value != 0 && value != 1) return TPROD_EINVAL;
+      h->fused_scales = value != 0;
       return TPROD_OK;
     default:
       return TPROD_EINVAL;

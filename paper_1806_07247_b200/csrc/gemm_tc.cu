@@ -329,7 +329,7 @@ template <int SEGKB, int CM>
 __global__ void __launch_bounds__(NTHREADS2, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ Cb, int64_t ldc, int n1, int n2, int n4, int h, int nyq,
-                    int* __restrict__ done) {
+                    int* __restrict__ done, int ovord) {
   constexpr int BN = 128;
   constexpr int A_PLANE = BK * BM * 2;              // 128 rows of this CTA
   constexpr int B_PLANE = (BN / 2) * BK * 2;        // 64 N rows of this CTA
@@ -395,11 +395,18 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   // With `done` (few tile rounds, K3 overlapped): f fastest, so the (m, n) output tiles complete
   // one after another and the inverse of the first ones runs during the last round.
   const int64_t tpf = (int64_t)mt * nt;
+  // (ovord = 1: m slowest, then f, n fastest -- concurrent pairs still share the A_f panel and
+  // the (m, n) tiles of an m row complete together.)
+  int r = 0;                                       // (m, n) index of the last tile_of2 call
   auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {   // m0: this pair's first row
-    int r;
-    if (done) {
+    if (done && ovord == 0) {
       r = (int)(t / h);
       f = (int)(t - (int64_t)r * h);
+    } else if (done) {
+      const int64_t hn = (int64_t)h * nt;
+      const int mm = (int)(t / hn), rem = (int)(t - mm * hn);
+      f = rem / nt;
+      r = mm * nt + (rem - f * nt);
     } else {
       f = (int)(t / tpf);
       r = (int)(t - (int64_t)f * tpf);
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
         __syncwarp();
         if (lane == 0) {
           __threadfence();
-          atomicAdd(done + (t / h), 1);
+          atomicAdd(done + r, 1);
         }
       }
     }
@@ -707,7 +714,8 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
     ov->cols_per_n = BN;
     ov->nt = (int)ntl;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq, done) != cudaSuccess) return 4;
+  static const int ovord = getenv("TPROD_OV_ORDER") ? atoi(getenv("TPROD_OV_ORDER")) : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq, done, ovord) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }
 

@@ -198,6 +198,11 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
 bool launch_inv_dense(const float* Cre, const float* Cim, int64_t ld, int64_t fstride, int64_t P,
                       int64_t Q, int64_t n3, OutUnscale u, float* X, cudaStream_t s,
                       OverlapK3* ov = nullptr);
+// K1 of B with K0 of B fused (n3 <= 32, P = n2 even and <= 2048, 8-byte aligned): the column scales
+// are reduced per lateral slice by a thread-block cluster inside the transform (no maxB pass).
+bool fwd_colmax_ok(const float* X, int64_t P, int64_t n3);
+bool launch_fwd_dense_colmax(const float* X, int64_t P, int64_t Q, int64_t n3, __half* out, int64_t ld,
+                             float* unscale, cudaStream_t s);
 // true if launch_inv_dense takes the tube-pair kernel for this n3 (the one that honours OverlapK3)
 bool inv_dense_pair_ok(int64_t n3);
 

@@ -237,6 +237,14 @@ __global__ void __launch_bounds__(128) inv_dense_kernel(const float* __restrict_
 // Requires P even (then every column start and every plane row stays 8-/4-byte aligned).
 constexpr int PAIR_MAX = 32;
 
+// ROLE 2 = B with its column scale computed here (K0 of B fused into K1 of B): the CTAs of one
+// lateral slice q (its P / 256 blocks of 256 tubes) form one thread-block cluster; each CTA reduces
+// max |B(:, q, :)| over its tubes, writes it into every peer's shared memory (DSMEM) and arrives on
+// the cluster barrier, runs its DFTs, then waits and takes the max of the cluster's partial maxima --
+// the exact K0 value (fmaxf of the same elements), so results are bitwise those of K0 + ROLE 1.
+__device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
 template <int N, int ROLE>
 __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict__ X, int64_t P,
                                                          int64_t Q, const unsigned* __restrict__ maxbits,
@@ -247,12 +255,38 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
   const int64_t pblocks = (P + 255) >> 8;
   const int64_t q = blockIdx.x / pblocks;
   const int64_t p = ((blockIdx.x - q * pblocks) * 128 + threadIdx.x) * 2;
-  if (p >= P) return;
+  if (ROLE != 2 && p >= P) return;
+  const bool act = p < P;                           // ROLE 2: every thread reaches the cluster barrier
   const int64_t PQh = (P * Q) >> 1;
-  const float2* x = reinterpret_cast<const float2*>(X + p + P * q);
+  const float2* x = reinterpret_cast<const float2*>(X + (act ? p : 0) + P * q);
   float2 v[N];
 #pragma unroll
-  for (int k = 0; k < N; ++k) v[k] = __ldg(x + PQh * k);
+  for (int k = 0; k < N; ++k) v[k] = act ? __ldg(x + PQh * k) : make_float2(0.f, 0.f);
+  __shared__ float cmax[8];                         // ROLE 2: partial maxima of the cluster's CTAs
+  uint32_t ncl = 1;
+  if constexpr (ROLE == 2) {
+    __shared__ float wmax[4];
+    float m = 0.f;
+#pragma unroll
+    for (int k = 0; k < N; ++k) m = fmaxf(m, fmaxf(fabsf(v[k].x), fabsf(v[k].y)));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      m = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+      uint32_t me;
+      asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(me));
+      const uint32_t local = (uint32_t)__cvta_generic_to_shared(cmax + me);
+      for (uint32_t r = 0; r < ncl; ++r) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(m) : "memory");
+      }
+    }
+    cl_arrive();
+  }
   float2 X0[H], X1[H];              // spectra of tube p (X0) and p+1 (X1)
   if constexpr (is_pow2(N) && N >= 8) {
     float t0[N], t1[N];
@@ -300,7 +334,16 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
       unscale[p + 1] = unscale_of(m1, e1);
     }
   } else {
-    const unsigned mq = __ldg(maxbits + q);
+    unsigned mq;
+    if constexpr (ROLE == 2) {
+      cl_wait();                                    // every CTA of the slice has written its maximum
+      float m = cmax[0];
+      for (uint32_t r = 1; r < ncl; ++r) m = fmaxf(m, cmax[r]);
+      mq = __float_as_uint(m);
+      if (!act) return;                             // no peer touches this CTA's shared memory now
+    } else {
+      mq = __ldg(maxbits + q);
+    }
     e0 = e1 = scale_exp(mq, N);
     if (p == 0) unscale[q] = unscale_of(mq, e0);
   }
@@ -442,16 +485,17 @@ struct DenseTable<0> {
 
 template <int N>
 struct PairTable {
-  static void fill(FwdFn* f0, FwdFn* f1, InvPFn* inv) {
+  static void fill(FwdFn* f0, FwdFn* f1, FwdFn* f2, InvPFn* inv) {
     f0[N] = fwd_dense2_kernel<N, 0>;
     f1[N] = fwd_dense2_kernel<N, 1>;
+    f2[N] = fwd_dense2_kernel<N, 2>;
     inv[N] = inv_dense2_kernel<N>;
-    PairTable<N - 1>::fill(f0, f1, inv);
+    PairTable<N - 1>::fill(f0, f1, f2, inv);
   }
 };
 template <>
 struct PairTable<0> {
-  static void fill(FwdFn*, FwdFn*, InvPFn*) {}
+  static void fill(FwdFn*, FwdFn*, FwdFn*, InvPFn*) {}
 };
 
 struct DenseFns {
@@ -460,10 +504,11 @@ struct DenseFns {
   InvFn inv[DENSE_MAX + 1] = {};
   FwdFn fwd0p[PAIR_MAX + 1] = {};
   FwdFn fwd1p[PAIR_MAX + 1] = {};
+  FwdFn fwd2p[PAIR_MAX + 1] = {};
   InvPFn invp[PAIR_MAX + 1] = {};
   DenseFns() {
     DenseTable<DENSE_MAX>::fill(fwd0, fwd1, inv);
-    PairTable<PAIR_MAX>::fill(fwd0p, fwd1p, invp);
+    PairTable<PAIR_MAX>::fill(fwd0p, fwd1p, fwd2p, invp);
   }
 };
 
@@ -503,6 +548,29 @@ bool launch_fwd_dense(const float* X, int64_t P, int64_t Q, int64_t n3, int role
   int64_t blocks = (P + (pair ? 255 : 127)) / (pair ? 256 : 128) * Q;
   void* args[] = {(void*)&X, (void*)&P, (void*)&Q, (void*)&maxbits, (void*)&out, (void*)&ld, (void*)&unscale};
   return cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(128), args, 0, s) == cudaSuccess;
+}
+
+bool fwd_colmax_ok(const float* X, int64_t P, int64_t n3) {
+  return n3 >= 1 && n3 <= PAIR_MAX && P % 2 == 0 && P <= 8 * 256 && ((uintptr_t)X & 7) == 0;
+}
+
+bool launch_fwd_dense_colmax(const float* X, int64_t P, int64_t Q, int64_t n3, __half* out, int64_t ld,
+                             float* unscale, cudaStream_t s) {
+  if (!fwd_colmax_ok(X, P, n3) || !ensure_dense_twiddles()) return false;
+  const int64_t pblocks = (P + 255) / 256;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)pblocks;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(pblocks * Q));
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  const unsigned* none = nullptr;
+  return cudaLaunchKernelEx(&cfg, dense_fns().fwd2p[n3], X, P, Q, none, out, ld, unscale) == cudaSuccess;
 }
 
 bool inv_dense_pair_ok(int64_t n3) { return n3 >= 1 && n3 <= PAIR_MAX; }

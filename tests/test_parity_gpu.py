@@ -217,6 +217,39 @@ def test_k3_overlap_bitwise(T, dims):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("dims", [(300, 1024, 31, 200), (256, 256, 32, 256), (64, 300, 7, 40), (40, 2048, 16, 24),
+                                  (40, 2050, 16, 24), (36, 301, 5, 20), (20, 6, 1, 9), (33, 200, 2, 70)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_fused_column_scales_bitwise(T, dims):
+    """TPROD_OPT_FUSED_SCALES: B's column scales reduced inside B's forward transform by a CTA cluster
+    per lateral slice (DSMEM exchange of partial maxima) give the same maxima as the K0 pass, so the
+    result is bitwise equal with the option off (1..8-CTA clusters, a ragged last CTA, n2 = 2050 and
+    odd n2 falling back to K0), with planted per-column magnitudes 2^-20..2^20 and a zero column;
+    prepared-operand path included; vs the oracle (Eq. (9))."""
+    n1, n2, n3, n4 = dims
+    A = normal((n1, n2, n3), 31)
+    B = normal((n2, n4, n3), 32)
+    B *= np.exp2(np.linspace(-20, 20, n4)).astype(np.float32)[None, :, None]
+    B[:, n4 // 2, :] = 0.0
+    Ad, Bd = dev(A), dev(B)
+    outs = []
+    for fused in (0, 1):
+        h = T.Handle()
+        h.set_option(T._lib.TPROD_OPT_FUSED_SCALES, fused)
+        outs.append(host(T.tprod(Ad, Bd, handle=h)))
+        outs.append(host(T.tprod(Ad, Bd, handle=h)))          # graph capture
+        h.prepare_a(Ad)
+        outs.append(host(T.tprod_prepared(Bd, handle=h)))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert not outs[0][:, n4 // 2, :].any()
+    cols = np.unique(np.array([0, 1, n4 // 2, n4 - 1]))
+    ref = O.tprod_columns(A.astype(np.float64), B.astype(np.float64), cols)
+    for j, c in enumerate(cols):                               # per column: each has its own scale
+        if ref[:, j, :].any():
+            assert O.rel_err(outs[0][:, c, :], ref[:, j, :]) <= TOL32
+
+
 # ------------------------------------------------------------------------------- stages
 @pytest.mark.parametrize("n3", [1, 2, 3, 10, 31, 32, 64, 65, 96, 100, 120, 128, 256, 375, 1000, 1536,
                                 2048, 4096, 6000, 8192, 15360,
