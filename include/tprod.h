@@ -219,7 +219,7 @@ enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_
  * pass over B.  The same maxima either way: bitwise identical results. */
 /* TPROD_OPT_OVERLAP (tprod_f32 / tprod_f32_prepared): 1 (default) = when the per-frequency GEMM runs on
  * CTA pairs in 2..8 tile rounds and K3 is the tube-pair register kernel (n3 <= 32), the GEMM takes
- * its tiles frequency-fastest and counts finished (m, n) output tiles in a device array of the
+ * its tiles m-row by m-row (frequencies inside a row) and counts finished (m, n) output tiles in a device array of the
  * handle, and K3 is launched as a programmatic dependent whose blocks each wait for the tile they
  * read: the inverse of finished tiles runs on the SMs the GEMM's last round leaves idle (Alg. 1
  * steps 2-3 overlapped).  0 = K3 strictly after the GEMM.  Bitwise identical results. */

@@ -392,14 +392,15 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
   // (Measured on config 5, DRAM read per launch: n fastest 149-165 GB, m fastest 185 GB, groups of
   // 6 m-tiles per n sweep 180 GB -- the pairs drift apart in K by up to a tile, longer than an L2
   // residency, so no raster order recovers the reuse; the plain order stays.)
-  // With `done` (few tile rounds, K3 overlapped): f fastest, so the (m, n) output tiles complete
-  // one after another and the inverse of the first ones runs during the last round.
+  // With `done` (few tile rounds, K3 overlapped): the (m, n) output tiles must complete one after
+  // another so that the inverse of the first ones runs during the last round -- f fastest
+  // (ovord & 1 == 0) or, the default, m slowest, then f, n fastest.
   const int64_t tpf = (int64_t)mt * nt;
   // (ovord = 1: m slowest, then f, n fastest -- concurrent pairs still share the A_f panel and
   // the (m, n) tiles of an m row complete together.)
   int r = 0;                                       // (m, n) index of the last tile_of2 call
   auto tile_of2 = [&](int64_t t, int& f, int& m0, int& n0) {   // m0: this pair's first row
-    if (done && ovord == 0) {
+    if (done && (ovord & 1) == 0) {
       r = (int)(t / h);
       f = (int)(t - (int64_t)r * h);
     } else if (done) {
@@ -554,7 +555,17 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
           }
         }
       }
-      if (done) {                                  // this warp's part of tile (m, n) at f is stored
+      if (done && (ovord & 2)) {                   // the CTA's part of tile (m, n) at f is stored:
+        asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");   // the 8 epilogue warps
+        if (warp == 2 && lane == 0) {
+          if (ovord & 4) {
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(done + r) : "memory");
+          } else {
+            __threadfence();
+            atomicAdd(done + r, 1);
+          }
+        }
+      } else if (done) {                           // this warp's part of tile (m, n) at f is stored
         __syncwarp();
         if (lane == 0) {
           __threadfence();
@@ -702,7 +713,7 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   cfg.numAttrs = 1;
   int in1 = (int)n1, in2 = (int)n2, in4 = (int)n4, ih = (int)h;
   // K3 overlap only pays when the grid runs few tile rounds (the last one partial): the counters need
-  // the frequency-fastest order, which on long runs re-reads panels the n-fastest order shares
+  // the row-by-row order, which on long runs re-reads panels the f-slowest order shares in L2
   const int64_t mtl = (n1 + 2 * CM * BM - 1) / (2 * CM * BM), ntl = (n4 + BN - 1) / BN;
   const int64_t rounds = (nct + max_cl - 1) / max_cl;
   if (!(done && ov && rounds >= 2 && rounds <= 8 && mtl * ntl <= OVERLAP_COUNTERS)) done = nullptr;
@@ -714,7 +725,13 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
     ov->cols_per_n = BN;
     ov->nt = (int)ntl;
   }
-  static const int ovord = getenv("TPROD_OV_ORDER") ? atoi(getenv("TPROD_OV_ORDER")) : 0;
+  // TPROD_OV_ORDER (measurement only) bits: 1 = (m, f, n) tile order instead of f fastest, 2 = one
+  // counter arrive per CTA after a named barrier of the epilogue warps instead of one per warp, 4 =
+  // red.release instead of fence + atomic.  Measured on config 3 (K2 + K3 stage, same box): 0: 164.9,
+  // 2: 163.5, 6: 163.4, 3: 162.5 us (default); the GEMM alone (ncu) ~151.5 us with counters in every
+  // variant vs 147.5 us without.
+  static const int ovord = getenv("TPROD_OV_ORDER") ? atoi(getenv("TPROD_OV_ORDER")) : 3;
+  if (done && (ovord & 2)) ov->target = (int)(h * 2 * CM);     // one arrival per CTA and frequency
   if (cudaLaunchKernelEx(&cfg, kern, ma, mb, Cb, ldc, in1, in2, in4, ih, nyq, done, ovord) != cudaSuccess) return 4;
   return cudaGetLastError() == cudaSuccess ? 0 : 4;
 }

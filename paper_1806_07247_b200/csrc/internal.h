@@ -63,15 +63,15 @@ bool gemm_tc_supported();
 // nyq = 1 if slice h-1 is a real Nyquist slice (n3 even): DC and Nyquist slices have exactly zero
 // Im planes and run only the Ar.Br products.
 // K2 -> K3 overlap (TPROD_OPT_OVERLAP): with `done` set, a CTA-pair GEMM of few tile
-// rounds runs its tiles frequency-fastest and counts finished (m, n) output tiles in done[m * nt + n]
-// (release: every epilogue warp of the pair adds 1 per frequency after its stores, `target` in
-// all); K3 is then launched as a programmatic dependent and each of its blocks waits (acquire) for
+// rounds runs its tiles m-row by m-row and counts finished (m, n) output tiles in done[m * nt + n]
+// (release: each CTA of the cluster adds 1 per frequency after its epilogue warps' stores, `target`
+// in all); K3 is then launched as a programmatic dependent and each of its blocks waits (acquire) for
 // the counter of the tile it reads, so the inverse of finished tiles runs on the SMs the GEMM's
 // last partial round leaves idle.  `ov` is filled by the GEMM launch (used = false: no counters).
 constexpr int OVERLAP_COUNTERS = 1024;   // (m, n) tile counters per handle
 struct OverlapK3 {
   const int* done = nullptr;
-  int target = 0;       // counter value of a finished (m, n) tile: h * 2 CM * epilogue warps
+  int target = 0;       // counter value of a finished (m, n) tile: h * 2 CM
   int pb_per_m = 1;     // 256-row K3 blocks per GEMM m tile (2 CM * 128 rows)
   int cols_per_n = 128; // GEMM N tile
   int nt = 0;           // GEMM n tiles

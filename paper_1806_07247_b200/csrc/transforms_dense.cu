@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(128) fwd_dense2_kernel(const float* __restrict
 }
 
 // OverlapK3 (ov.done != nullptr): launched as a programmatic dependent of the GEMM; block b takes
-// the (m, n) GEMM tile r = b / (128 pb_per_m) -- blocks ordered as the frequency-fastest GEMM
-// finishes its tiles -- and waits until done[r] reaches the tile's count (ld.acquire.gpu by one
+// the (m, n) GEMM tile r = b / (128 pb_per_m) -- blocks ordered as the GEMM finishes its tiles --
+// and waits until done[r] reaches the tile's count (ld.acquire.gpu by one
 // thread, then a CTA barrier) before it reads C-bar through L2 (ld.global.cg: never a line an
 // L1 might hold from before the GEMM wrote it).
 struct OvArgs {

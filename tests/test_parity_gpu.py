@@ -185,7 +185,7 @@ def test_gemm_tile_and_cluster_variants_bitwise(T, dims):
                                   (1024, 1024, 31, 512), (520, 96, 5, 1030)],
                          ids=lambda d: "x".join(map(str, d)))
 def test_k3_overlap_bitwise(T, dims):
-    """TPROD_OPT_OVERLAP: the GEMM on CTA pairs in 2..8 tile rounds runs frequency-fastest and counts
+    """TPROD_OPT_OVERLAP: the GEMM on CTA pairs in 2..8 tile rounds runs m-row by m-row and counts
     finished (m, n) tiles; K3 (tube-pair register kernel, n3 <= 32) launches as a programmatic
     dependent and each block waits for its tile.  Scheduling only: bitwise equal to the serial
     order, direct launch and graph replay, ragged m / n tiles (600 rows, 300 / 1030 columns),
