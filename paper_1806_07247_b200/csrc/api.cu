@@ -55,6 +55,7 @@ struct tprod_ctx {
   bool timed_last = false;
   bool forked_last = false;           // the last timed call ran the A / B chains concurrently
   bool overlap = true;                // TPROD_OPT_OVERLAP: K3 as a programmatic dependent of the GEMM
+  bool overlap_stream = false;        // ... also for many-round GEMMs with the streaming tube inverse (value 2: opt-in)
   bool fused_scales = true;           // TPROD_OPT_FUSED_SCALES: K0 of B inside K1 of B (n3 <= 32)
   bool overlapped_last = false;       // the last timed call overlapped K2 and K3 (one stage)
   int* done = nullptr;                // OVERLAP_COUNTERS (m, n) tile counters (internal.h OverlapK3)
@@ -465,7 +466,7 @@ int run_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n1, 
   std::vector<int64_t> key = {1, (int64_t)(uintptr_t)A, (int64_t)(uintptr_t)B, (int64_t)(uintptr_t)C, n1, n2, n3, n4,
                               (int64_t)(uintptr_t)h->ws, pa ? (int64_t)(uintptr_t)pa->Ab : 0,
                               pa ? (int64_t)(uintptr_t)pa->uA : 0, pa ? pa->lda : 0, h->engine, h->force_bn,
-                              h->force_cn, h->transform, h->overlap ? 1 : 0, h->fused_scales ? 1 : 0};
+                              h->force_cn, h->transform, (h->overlap ? 1 : 0) + (h->overlap_stream ? 2 : 0), h->fused_scales ? 1 : 0};
   return graph_run(h, std::move(key), s,
                    [&](cudaStream_t ls) { return launch_f32(h, A, B, C, n1, n2, n3, n4, ls, pa, L, T); });
 }
@@ -575,7 +576,9 @@ int launch_f32(tprod_ctx* h, const float* A, const float* B, float* C, int64_t n
   OverlapK3 ov;
   if (tc) {
     // the counters only where K3 is the tube-pair register kernel (the one that waits on them)
-    int* done = h->overlap && h->done && !T.tc && inv_dense_pair_ok(n3) ? h->done : nullptr;
+    // ... or the streaming tube inverse of n3 = 64 (any number of tile rounds: config 5)
+    ov.stream = h->overlap_stream && T.staged && !T.tc && inv_tube_stream_ok(n1, n3, L.ldc, C);
+    int* done = h->overlap && h->done && !T.tc && (inv_dense_pair_ok(n3) || ov.stream) ? h->done : nullptr;
     st = launch_gemm_tc_split(Ab, L.lda, Bb, L.ldb, Cb, L.ldc, n1, n2, n4, L.h, n3 % 2 == 0 ? 1 : 0,
                               h->force_bn, h->force_cn, h->num_sms, s, done, &ov);
     if (st) return st;
@@ -811,7 +814,7 @@ int tprod_create(int device, tprod_handle* out) {
   CK(cudaMalloc(&status, sizeof(int)));
   CK(cudaMemset(status, 0, sizeof(int)));
   int* done = nullptr;
-  if (cudaMalloc(&done, sizeof(int) * OVERLAP_COUNTERS) != cudaSuccess) {
+  if (cudaMalloc(&done, sizeof(int) * (OVERLAP_COUNTERS + 1)) != cudaSuccess) {   // + the K3 work counter
     cudaFree(status);
     return TPROD_ECUDA;
   }
@@ -1302,8 +1305,9 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
       h->sync_checks = value != 0;
       return TPROD_OK;
     case TPROD_OPT_OVERLAP:
-      if (value != 0 && value != 1) return TPROD_EINVAL;
+      if (value < 0 || value > 2) return TPROD_EINVAL;
       h->overlap = value != 0;
+      h->overlap_stream = value == 2;
       return TPROD_OK;
     case TPROD_OPT_FUSED_SCALES:
       if (value != 0 && value != 1) return TPROD_EINVAL;

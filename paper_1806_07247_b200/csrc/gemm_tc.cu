@@ -716,10 +716,14 @@ int launch_pair(const CUtensorMap& ma, const __half* Bb, int64_t ldb, float* Cb,
   // the row-by-row order, which on long runs re-reads panels the f-slowest order shares in L2
   const int64_t mtl = (n1 + 2 * CM * BM - 1) / (2 * CM * BM), ntl = (n4 + BN - 1) / BN;
   const int64_t rounds = (nct + max_cl - 1) / max_cl;
-  if (!(done && ov && rounds >= 2 && rounds <= 8 && mtl * ntl <= OVERLAP_COUNTERS)) done = nullptr;
+  // (a streaming K3 consumer -- OverlapK3::stream -- follows the row-by-row order over any number of
+  // rounds: with m slowest, then f, n fastest, the concurrent clusters still share the A_f rows and
+  // B_f is read once per m-row, as in the f-slowest order)
+  if (!(done && ov && rounds >= 2 && (rounds <= 8 || ov->stream) && mtl * ntl <= OVERLAP_COUNTERS)) done = nullptr;
   if (done) {
-    if (cudaMemsetAsync(done, 0, sizeof(int) * mtl * ntl, s) != cudaSuccess) return 4;
+    if (cudaMemsetAsync(done, 0, sizeof(int) * (mtl * ntl + 1), s) != cudaSuccess) return 4;
     ov->done = done;
+    ov->work = done + mtl * ntl;                     // K3's item counter (streaming consumer)
     ov->target = (int)(h * 2 * CM * EPI_WARPS);
     ov->pb_per_m = CM;                               // 2 CM * 128 rows = CM blocks of 256 rows
     ov->cols_per_n = BN;

@@ -76,6 +76,11 @@ struct OverlapK3 {
   int cols_per_n = 128; // GEMM N tile
   int nt = 0;           // GEMM n tiles
   bool used = false;
+  // Streaming consumer (the tube inverse of n3 = 64, config 5): K3's CTAs take their items from
+  // the work counter `work` in the GEMM's tile-completion order, so the overlap holds over any
+  // number of tile rounds (set by the caller before the GEMM launch; `work` by the GEMM launch).
+  bool stream = false;
+  int* work = nullptr;
 };
 int launch_gemm_tc_split(const __half* Ab, int64_t lda, const __half* Bb, int64_t ldb,
                          float* Cb, int64_t ldc, int64_t n1, int64_t n2, int64_t n4, int64_t h,
@@ -123,7 +128,9 @@ bool launch_inv_cluster(const float* Cre, int64_t ld, int64_t P, int64_t Q, int6
 bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role, const unsigned* maxbits,
                      const float2* st, __half* out, int64_t ld, float* unscale, int num_sms, cudaStream_t s);
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st,
-                     OutUnscale u, float* X, int num_sms, cudaStream_t s);
+                     OutUnscale u, float* X, int num_sms, cudaStream_t s, OverlapK3* ov = nullptr);
+// the shapes whose K3 is the streaming tube inverse (OverlapK3::stream)
+bool inv_tube_stream_ok(int64_t P, int64_t n3, int64_t ld, const float* X);
 
 // ------------------------------------------------------------------ NEXT-4 (tensor_ops.cu)
 template <typename T>

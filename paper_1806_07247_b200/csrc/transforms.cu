@@ -417,7 +417,7 @@ void launch_inv_f32(const float* Cre, const float* Cim, int64_t ld, int64_t fstr
   const bool prod_layout = tw.staged && Cim == Cre + Q * ld && fstride == 2 * Q * ld;
   if (prod_layout && tw.tc && launch_inv_dft_tc(Cre, ld, P, Q, n3, u, X, num_sms, s)) return;
   cudaGetLastError();
-  if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, u, X, num_sms, s)) return;
+  if (prod_layout && launch_inv_tube(Cre, ld, P, Q, n3, tw.st, u, X, num_sms, s, ov)) return;
   cudaGetLastError();
   if (prod_layout && tw.cluster && launch_inv_cluster(Cre, ld, P, Q, n3, tw.tw, u, X, num_sms, s)) return;
   cudaGetLastError();

@@ -116,6 +116,81 @@ __device__ __forceinline__ void tma_pipeline(const CUtensorMap* m, int64_t P, in
   }
 }
 
+// K2 -> K3 overlap, streaming consumer (internal.h OverlapK3::stream): the items are numbered in the
+// GEMM's tile-completion order -- (m, n) tile r = m * nt + n slowest, inside a tile the 128 lateral
+// slices of each of its `ppm` tube blocks -- and handed out by the device counter `work`; thread 0
+// waits (acquire, bounded: a counter that never completes traps) for the tile's counter before it
+// issues the TMA load (fence.proxy.async: the GEMM's generic-proxy stores, acquired by this thread,
+// ordered before the async-proxy read).  CTAs resident while the GEMM still runs (on the SMs its
+// cluster grid leaves idle) thus invert finished m-rows; the rest join when the GEMM's CTAs exit.
+struct TubeOv {
+  const int* done;
+  int* work;
+  int target, ppm, nt;
+};
+template <int BUF, int TPI, typename Body>
+__device__ __forceinline__ void tma_pipeline_ov(const CUtensorMap* m, int64_t P, int64_t Q, float* smem,
+                                                uint64_t* full, const TubeOv& ov, Body&& body) {
+  __shared__ long long s_item[2];                    // (q << 32) | p0 of the item in buffer b, -1 = none
+  const int tid = threadIdx.x;
+  const int64_t pblocks = (P + TPI - 1) / TPI;
+  const int per = 128 * ov.ppm;                      // items per (m, n) tile (GEMM N tile = 128)
+  const int64_t total = ((pblocks + ov.ppm - 1) / ov.ppm) * ov.nt * per;
+  if (tid == 0) {
+    bar_init(&full[0], 1);
+    bar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int ready = -1;                                    // last tile seen complete (thread 0)
+  auto fetch = [&](int slot) {                       // thread 0: next item into buffer `slot`
+    for (;;) {
+      const int64_t i = atomicAdd(ov.work, 1);
+      if (i >= total) {
+        s_item[slot] = -1;
+        return;
+      }
+      const int r = (int)(i / per), j = (int)(i - (int64_t)r * per);
+      const int64_t q = (int64_t)(r % ov.nt) * 128 + (j & 127);
+      const int64_t pb = (int64_t)(r / ov.nt) * ov.ppm + (j >> 7);
+      if (q >= Q || pb >= pblocks) continue;         // ragged edge of the tile grid
+      if (r != ready) {
+        const int* c = ov.done + r;
+        int v;
+        uint64_t t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+          if (v >= ov.target) break;
+          __nanosleep(1000);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 8000000000ull) __trap();
+        }
+        ready = r;
+      }
+      asm volatile("fence.proxy.async;" ::: "memory");
+      bar_expect(&full[slot], BUF * 4);
+      tma3d(smem + slot * BUF, m, &full[slot], (int)(pb * TPI), (int)q, 0);
+      s_item[slot] = (long long)((q << 32) | (pb * TPI));
+      return;
+    }
+  };
+  if (tid == 0) fetch(0);
+  __syncthreads();
+  for (int n = 0;; ++n) {
+    const int b = n & 1;
+    const long long cur = s_item[b];
+    if (cur < 0) break;
+    if (tid == 0) fetch(b ^ 1);                      // prefetch (buffer b ^ 1 was released by the last barrier)
+    bar_wait(&full[b], (n >> 1) & 1);
+    Item it;
+    it.q = cur >> 32;
+    it.p0 = cur & 0xffffffffll;
+    body(it, smem + b * BUF);
+    __syncthreads();
+  }
+}
+
 // load TPT adjacent floats of row r of a [rows][TP] smem tile
 template <int TPT>
 __device__ __forceinline__ void lds(const float* s, int r, int tid, float (&o)[TPT]) {
@@ -389,7 +464,8 @@ __global__ void __launch_bounds__(TUBE_NT) fwd_tube_kernel(const __grid_constant
 template <int N>
 __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant__ CUtensorMap mC,
                                                           const __grid_constant__ CUtensorMap mXo, int64_t P,
-                                                          int64_t Q, const float2* __restrict__ st, OutUnscale u) {
+                                                          int64_t Q, const float2* __restrict__ st, OutUnscale u,
+                                                          TubeOv ov) {
   using C = TubeCfg<N>;
   constexpr int F = C::F, TUB = C::TUB, H = N / 2 + 1;
   constexpr int BUF = TUB * 2 * H;                  // C-bar tile: rows [f][re|im], TUB floats each
@@ -397,7 +473,7 @@ __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant
   __shared__ uint64_t full[2];
   float2* z = reinterpret_cast<float2*>(smem + 2 * BUF);     // z[k][c], separate from the TMA buffers
   const float inv_n = 1.f / (float)N;
-  tma_pipeline<BUF, TUB>(&mC, P, Q, smem, full, [&](const Item& cur, const float* s) {
+  auto body = [&](const Item& cur, const float* s) {
     if (threadIdx.x == 0) bulk_wait_read();                  // the previous item's store has read z
     __syncthreads();
     // Z / N = (X + i Y) / N with the conjugate fill (Im of DC / Nyquist dropped: C2R)
@@ -424,7 +500,9 @@ __global__ void __launch_bounds__(TUBE_NT) inv_tube_kernel(const __grid_constant
       tma_store3d(&mXo, z, (int)cur.p0, (int)cur.q, 0);
       bulk_commit();
     }
-  });
+  };
+  if (ov.done) tma_pipeline_ov<BUF, TUB>(&mC, P, Q, smem, full, ov, body);
+  else tma_pipeline<BUF, TUB>(&mC, P, Q, smem, full, body);
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
@@ -894,7 +972,7 @@ bool launch_fwd_tube_n(const float* X, int64_t P, int64_t Q, int role, const uns
 
 template <int N>
 bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const float2* st, OutUnscale u, float* X,
-                       int num_sms, cudaStream_t s) {
+                       int num_sms, cudaStream_t s, OverlapK3* ov) {
   using C = TubeCfg<N>;
   constexpr int H = N / 2 + 1;
   CUtensorMap m, mo;
@@ -907,7 +985,25 @@ bool launch_inv_tube_n(const float* Cre, int64_t ld, int64_t P, int64_t Q, const
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
   const int64_t items = (P + C::TUB - 1) / C::TUB * Q;
   const int grid = grid_occ(fn, items, smem, num_sms);
-  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&st, (void*)&u};
+  TubeOv to = {nullptr, nullptr, 0, 1, 1};
+  void* args[] = {(void*)&m, (void*)&mo, (void*)&P, (void*)&Q, (void*)&st, (void*)&u, (void*)&to};
+  if (ov && ov->done && ov->stream && ov->work && ov->cols_per_n == 128 && (256 * ov->pb_per_m) % C::TUB == 0) {
+    // programmatic dependent of the GEMM just launched on `s` (internal.h OverlapK3): its CTAs start
+    // once every GEMM CTA is resident, on the SMs the GEMM's cluster grid leaves free
+    to = {ov->done, ov->work, ov->target, 256 * ov->pb_per_m / C::TUB, ov->nt};
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(TUBE_NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    ov->used = true;
+    return cudaLaunchKernelExC(&cfg, fn, args) == cudaSuccess;
+  }
   return cudaLaunchKernel(fn, dim3(grid), dim3(TUBE_NT), args, smem, s) == cudaSuccess;
 }
 
@@ -1108,14 +1204,18 @@ bool launch_fwd_tube(const float* X, int64_t P, int64_t Q, int64_t n3, int role,
   }
 }
 
+bool inv_tube_stream_ok(int64_t P, int64_t n3, int64_t ld, const float* X) {
+  return n3 == 64 && tube_inv_pick(n3) && P % 4 == 0 && ((uintptr_t)X & 15) == 0 && (ld * 4) % 16 == 0;
+}
+
 bool launch_inv_tube(const float* Cre, int64_t ld, int64_t P, int64_t Q, int64_t n3, const float2* st,
-                     OutUnscale u, float* X, int num_sms, cudaStream_t s) {
+                     OutUnscale u, float* X, int num_sms, cudaStream_t s, OverlapK3* ov) {
   if (!st || !tube_inv_pick(n3) || P % 4 != 0 || ((uintptr_t)X & 15) != 0 || (ld * 4) % 16 != 0) return false;
   switch (n3) {
-    case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, u, X, num_sms, s);
-    case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, u, X, num_sms, s);
-    case 128: return launch_inv_tube_n<128>(Cre, ld, P, Q, st, u, X, num_sms, s);
-    default: return launch_inv_tube_n<256>(Cre, ld, P, Q, st, u, X, num_sms, s);
+    case 32: return launch_inv_tube_n<32>(Cre, ld, P, Q, st, u, X, num_sms, s, ov);
+    case 64: return launch_inv_tube_n<64>(Cre, ld, P, Q, st, u, X, num_sms, s, ov);
+    case 128: return launch_inv_tube_n<128>(Cre, ld, P, Q, st, u, X, num_sms, s, ov);
+    default: return launch_inv_tube_n<256>(Cre, ld, P, Q, st, u, X, num_sms, s, ov);
   }
 }
 
