@@ -222,12 +222,12 @@ enum { TPROD_OPT_ENGINE = 1, TPROD_OPT_GEMM_BN = 2, TPROD_OPT_TIMING = 3, TPROD_
  * its tiles m-row by m-row (frequencies inside a row) and counts finished (m, n) output tiles in a device array of the
  * handle, and K3 is launched as a programmatic dependent whose blocks each wait for the tile they
  * read: the inverse of finished tiles runs on the SMs the GEMM's last round leaves idle (Alg. 1
- * steps 2-3 overlapped).  0 = K3 strictly after the GEMM.  2 (opt-in) = as 1, and with
- * n3 = 64 (K3 = the TMA tube inverse; config 5) the same for a GEMM of any number of tile rounds:
- * K3's CTAs take their work items from a device counter in the GEMM's tile-completion order (m-row
- * by m-row), so the inverse of one m-row runs on the SMs the cluster grid leaves idle while the GEMM
- * works on the next (measured on config 5: no gain under the power cap, hence not the
- * default).  Bitwise identical results in every setting. */
+ * steps 2-3 overlapped).  With n3 = 64 (K3 = the TMA tube inverse; config 5) the same
+ * holds for a GEMM of any number of tile rounds: K3's CTAs take their work items from a device
+ * counter in the GEMM's tile-completion order (m-row by m-row), so the inverse of one m-row runs on
+ * the SMs the cluster grid leaves idle while the GEMM works on the next (config 5, same box, arms
+ * alternated: 95.2 -> 94.0 ms per step).  2 = as 1 without that many-round case (measurement).
+ * 0 = K3 strictly after the GEMM.  Bitwise identical results in every setting. */
 /* TPROD_OPT_SYNC_CHECKS: 1 (default) = tprod_tinv_f32 waits for its stream and returns
  * TPROD_ESINGULAR for a singular tensor; 0 = it returns at once and reports singularity through
  * the status word (tprod_status). */

@@ -55,7 +55,7 @@ struct tprod_ctx {
   bool timed_last = false;
   bool forked_last = false;           // the last timed call ran the A / B chains concurrently
   bool overlap = true;                // TPROD_OPT_OVERLAP: K3 as a programmatic dependent of the GEMM
-  bool overlap_stream = false;        // ... also for many-round GEMMs with the streaming tube inverse (value 2: opt-in)
+  bool overlap_stream = true;         // ... also for many-round GEMMs with the streaming tube inverse (off with value 2)
   bool fused_scales = true;           // TPROD_OPT_FUSED_SCALES: K0 of B inside K1 of B (n3 <= 32)
   bool overlapped_last = false;       // the last timed call overlapped K2 and K3 (one stage)
   int* done = nullptr;                // OVERLAP_COUNTERS (m, n) tile counters (internal.h OverlapK3)
@@ -1307,7 +1307,7 @@ int tprod_set_option(tprod_handle h, int option, int64_t value) {
     case TPROD_OPT_OVERLAP:
       if (value < 0 || value > 2) return TPROD_EINVAL;
       h->overlap = value != 0;
-      h->overlap_stream = value == 2;
+      h->overlap_stream = value == 1;
       return TPROD_OK;
     case TPROD_OPT_FUSED_SCALES:
       if (value != 0 && value != 1) return TPROD_EINVAL;
